@@ -1,0 +1,405 @@
+#!/usr/bin/env python
+"""bench.py — publish -> all-rollouts weight-sync latency of the relay tier (arxiv 2510.12633 §4).
+
+One step = one pass of the whole hot path over a fresh version:
+  lam_publish(v)   fp32 master shard -> bf16 RNE -> chunked bucket image in the master's slot
+  lam_relay_step   chain-pipelined hops master -> relay 1 -> ... (N > 1), version commit
+  lam_pull         every rollout pulls v and reshards it into its TP buffers
+and the step's time is publish -> every rollout's pull completed.
+
+Workload (BASELINE.json configs[1]): Qwen2.5-7B-shaped snapshot (7.62 G params, 15.23 GB bf16),
+actor FSDP-1 on GPU 0.  N = 1: master node on GPU 0, one TP=1 rollout pulling from it.
+N > 1 (torchrun, one process per GPU): relays on GPUs 1..N-1 in a chain, one TP=1 rollout per relay
+GPU (config 2 at N = 8).  Weak scaling: each added GPU adds one relay + one rollout.
+
+`--impl reference` times the CPU oracle (the reference arm of this tier) on a bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "publish->all-rollouts sync latency"
+UNIT = "s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="lam", choices=["lam", "reference"])
+    ap.add_argument("--model", default="7b")
+    ap.add_argument("--chunk-mb", type=int, default=0, help="chunk size; 0 = Appendix D k*")
+    ap.add_argument("--hop-ctas", type=int, default=0)
+    ap.add_argument("--pack-ctas", type=int, default=0)
+    ap.add_argument("--pull-ctas", type=int, default=0)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the oracle sample")
+    ap.add_argument("--quick", action="store_true", help="profiling mode: no e2e, no cpu baseline, no clocks")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------------------ CPU oracle leg
+def oracle_sample(model: str, seconds: float, version: int = 1):
+    """Time the oracle (as it stands) on a bounded sample of the workload, scaled to one full step.
+
+    Sample: the leading segments of the 7B image (inputs pre-generated, like resident masters):
+    publish = RNE cast + pack into the image + chunk checksums; pull = inverse bucket map + TP=1 rule.
+    """
+    import numpy as np
+
+    from oracle.bf16 import rne_bf16
+    from oracle.checksum import chunk_checksum
+    from oracle.image import image_plan, unpack_tensor
+    from oracle.model import MODELS, numel, tensors
+    from synth import SEED, gen_bits
+
+    d = MODELS[model]
+    tl = tensors(d)
+    shapes = [s for _, s in tl]
+    P = sum(numel(s) for s in shapes)
+    C = 64 << 20
+    plan = image_plan(shapes, 1, C)
+    # pick whole tensors from the start of the layer stack until ~seconds/6 of generation work
+    budget_elems = int(1.5e7 * seconds)          # ~15 M params/s through the numpy oracle
+    chosen, n = [], 0
+    for t in range(1, len(tl)):               # skip the 545M-element embedding: keep the sample bounded
+        if n >= budget_elems:
+            break
+        chosen.append(t)
+        n += numel(shapes[t])
+    segs = [s for s in plan.segments if s.tensor_id in set(chosen)]
+    inputs = {s.tensor_id: gen_bits(SEED, version, s.tensor_id, s.elem0, s.count) for s in segs}
+    lo = min(plan.image_offset(s) for s in segs)
+    hi = max(plan.image_offset(s) + 2 * s.count for s in segs)
+    img = np.zeros(hi - lo + 4096, dtype=np.uint8)
+    t0 = time.perf_counter()
+    for s in segs:                               # publish: cast + pack
+        o = plan.image_offset(s) - lo
+        img[o:o + 2 * s.count] = rne_bf16(inputs[s.tensor_id]).view(np.uint8)
+    for a in range(0, img.size, C):              # checksums of the produced bytes
+        chunk_checksum(img[a:a + C])
+    t_pub = time.perf_counter() - t0
+    rd = lambda o, k: img[o - lo:o - lo + k]
+    t0 = time.perf_counter()
+    for t in chosen:                             # pull at TP=1: inverse bucket map
+        unpack_tensor(rd, plan, t, shapes[t]).copy()
+    t_pull = time.perf_counter() - t0
+    frac = n / P
+    full = (t_pub + t_pull) / frac
+    return full, dict(kind="oracle", cores=1, value=full, unit=UNIT,
+                      sample=f"{len(chosen)} tensors / {n / 1e6:.1f} M params of {model} "
+                             f"({100 * frac:.2f}%): publish {t_pub:.2f} s + pull {t_pull:.2f} s, "
+                             f"scaled to the full snapshot; numpy, single thread")
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    per = max(2.0, args.cpu_seconds / max(1, args.steps + args.warmup))
+    for _ in range(args.warmup):
+        oracle_sample(args.model, per)
+    vals = []
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        v, info = oracle_sample(args.model, per)
+        vals.append(v)
+    wall = time.perf_counter() - t0
+    value = sum(vals) / len(vals)
+    cpu = os.cpu_count()
+    out = dict(metric=METRIC, value=value, unit=UNIT, impl="reference", n_gpus=args.gpus, steps=args.steps,
+               warmup=args.warmup, ms_per_step=value * 1e3, higher_is_better=False, scaling="weak",
+               vs_baseline=None, dtype="bf16", data="synthetic",
+               config=dict(workload=f"{args.model}: oracle publish+pull, bounded sample scaled to one step",
+                           model=f"Qwen2.5-{args.model.upper()}-shaped"),
+               cpu_baseline=dict(info, value=value, host_cpus=cpu, wall_s=wall),
+               e2e=dict(value=value, unit=UNIT, h2d_bytes_per_step=0, d2h_bytes_per_step=0))
+    print(json.dumps(out))
+    return 0
+
+
+# ------------------------------------------------------------------------------------ clocks
+class Clocks:
+    def __init__(self, device: int):
+        self.samples, self.proc = [], None
+        self.device = device
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return dict(sm_mhz=None, sm_max_mhz=None, reasons=["unavailable"], samples=0)
+        sm = sorted(float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit())
+        mx = max((float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()), default=None)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 4 + i and s[4 + i].lower().startswith("active")})
+        return dict(sm_mhz=sm[len(sm) // 2] if sm else None, sm_max_mhz=mx, reasons=reasons, samples=len(self.samples))
+
+
+# -------------------------------------------------------------------------------- GPU leg
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+
+    from paper_2510_12633_b200 import lam
+    from paper_2510_12633_b200.workload import MODELS, ActorShard, RolloutBuffers
+    from synth import SEED
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    N = world
+    if N != args.gpus:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}; using {N}", file=sys.stderr)
+    torch.cuda.set_device(rank)
+    gloo = None
+    if N > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", rank))
+        gloo = dist.new_group(backend="gloo")
+
+    def barrier():
+        if gloo is not None:
+            dist.barrier(group=gloo)
+
+    model = MODELS[args.model]
+    relays = [[d] for d in range(1, N)]
+    rollouts = [(0, 0)] if N == 1 else [(i, i) for i in range(1, N)]
+    port = os.environ.get("MASTER_PORT", "0")
+    cfg = lam.Config(model=model, fsdp_size=1, actor_devices=[0], relays=relays, rollouts=rollouts,
+                     chunk_bytes=args.chunk_mb << 20, proc_rank=rank, n_procs=N,
+                     proc_of_device={d: d for d in range(N)}, shm_name=f"lam_bench_{port}_{os.getppid()}",
+                     hop_ctas=args.hop_ctas, pack_ctas=args.pack_ctas, pull_ctas=args.pull_ctas)
+    ctx = lam.Context(cfg)
+    if N > 1:
+        blobs = [None] * N
+        dist.all_gather_object(blobs, ctx.export_ipc(), group=gloo)
+        for p, b in enumerate(blobs):
+            if p != rank:
+                ctx.import_ipc(p, b)
+        ctx.connect()
+        barrier()
+    info = ctx.plan_info()
+    M = info.snapshot_bytes
+    params = info.params
+
+    shard = None
+    if rank == 0:
+        shard = ActorShard(model, 1, 0, 0)
+        shard.fill(SEED, 1)
+    mine = [rid for rid, (_, dev) in enumerate(rollouts) if dev == rank]
+    bufs = {rid: RolloutBuffers(model, 1, 0, rank) for rid in mine}
+    stream = torch.cuda.Stream()
+    actor_stream = torch.cuda.Stream() if rank == 0 else None
+    torch.cuda.synchronize()
+
+    state = {"v": 0}
+
+    def step(h2d=None, d2h=None):
+        state["v"] += 1
+        v = state["v"]
+        if rank == 0:
+            if h2d is not None:                        # e2e: the step's inputs arrive from host memory
+                with torch.cuda.stream(actor_stream):
+                    shard.buf.copy_(h2d, non_blocking=True)
+            while ctx.publish(v, 0, shard.shards(), actor_stream.cuda_stream) == lam.LAM_EBUSY:
+                ctx.relay_step()
+        pending = list(mine)
+        while True:
+            ctx.relay_step()
+            for rid in list(pending):
+                if ctx.latest(rollouts[rid][0]) >= v:
+                    got = ctx.pull(rid, bufs[rid].tp, stream.cuda_stream)
+                    assert got >= v, (got, v)
+                    if d2h is not None:
+                        with torch.cuda.stream(stream):
+                            for name, t in bufs[rid].bufs.items():
+                                d2h[name].copy_(t, non_blocking=True)
+                    pending.remove(rid)
+            if not pending and (rank != 0 or ctx.latest(0) >= v):
+                break
+        stream.synchronize()
+        ctx.relay_step()
+        barrier()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    ctx.kernel_times()
+    ctx.set_profiling(True)
+    st0 = ctx.stats()
+    clk = Clocks(rank)
+    barrier()
+    torch.cuda.synchronize()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    lat = []
+    with (clk if not args.quick else _Null()):
+        start.record(stream)
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            step()
+            lat.append(time.perf_counter() - t0)
+        torch.cuda.synchronize()
+        end.record(stream)
+        end.synchronize()
+    ms = start.elapsed_time(end)
+    kt = ctx.kernel_times()
+    ctx.set_profiling(False)
+    st1 = ctx.stats()
+    launches = sum(n for _, n in kt.values())
+
+    def allmax(x):
+        if gloo is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=gloo)
+        return float(t.item())
+
+    def allsum(x):
+        if gloo is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=gloo)
+        return float(t.item())
+
+    ms_max = allmax(ms)
+    launches_all = int(allsum(launches))
+    pack_ms = allmax(kt["pack"][0] / max(1, kt["pack"][1]) if kt["pack"][1] else 0.0)
+    hop_ms = allmax(kt["hop"][0] / max(1, kt["hop"][1]) if kt["hop"][1] else 0.0)
+    pull_ms = allmax(kt["pull"][0] / max(1, kt["pull"][1]) if kt["pull"][1] else 0.0)
+
+    # e2e through the public API with host buffers: H2D of the masters, publish, relay, pull, D2H
+    e2e = None
+    if not args.quick and not args.no_e2e:
+        e2e = run_e2e(args, rank, N, shard, bufs, mine, step, barrier, allmax, torch)
+
+    if rank == 0:
+        import json as _json
+        peaks = {}
+        try:
+            peaks = _json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        except Exception:
+            pass
+        hbm_peak = peaks.get("hbm_gbs", 6650.0)
+        sec = ms_max / 1e3 / args.steps
+        if N == 1:
+            pack_gbs = 6.0 * params / (pack_ms / 1e3) / 1e9 if pack_ms else None
+            roof = dict(bound="hbm", kernel="k_pack", achieved=pack_gbs, peak=hbm_peak, unit="GB/s",
+                        frac=(pack_gbs / hbm_peak) if pack_gbs else None, traffic=None,
+                        algorithmic_bytes_per_launch=6 * params,
+                        peak_source="MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6.65 TB/s")
+        else:
+            nvl_peak = 770.0
+            hop_gbs = 2.0 * params / (hop_ms / 1e3) / 1e9 if hop_ms else None
+            roof = dict(bound="nvlink", kernel="k_hop", achieved=hop_gbs, peak=nvl_peak, unit="GB/s",
+                        frac=(hop_gbs / nvl_peak) if hop_gbs else None, traffic=None,
+                        algorithmic_bytes_per_launch=2 * params,
+                        peak_source="B200_PROFILING.md measured peer copy 770 GB/s/dir (nominal 900)")
+        cpu = None
+        if N == 1 and not args.quick and not args.no_cpu_baseline:
+            _, cpu = oracle_sample(args.model, args.cpu_seconds)
+        lat.sort()
+        out = dict(
+            metric=METRIC, value=sec, unit=UNIT, n_gpus=N, steps=args.steps, warmup=args.warmup,
+            ms_per_step=sec * 1e3, higher_is_better=False, scaling="weak", vs_baseline=None, dtype="bf16",
+            data="synthetic",
+            config=dict(workload=(f"{args.model}: actor FSDP-1 on GPU0, " +
+                                  ("master node + 1 TP=1 rollout on GPU0" if N == 1 else
+                                   f"chain of {N - 1} relays on GPUs 1..{N - 1}, one TP=1 rollout per relay")),
+                        model=f"Qwen2.5-{args.model.upper()}-shaped", params=params, snapshot_bytes=M,
+                        chunk_bytes=info.chunk_bytes, chunks=info.total_chunks, global_batch=None, seq_len=None,
+                        parallelism=f"relay-chain p={N}", l2="inputs (fp32 masters, slots) >> 126 MB L2"),
+            roofline=roof,
+            kernels_ms=dict(pack=pack_ms, hop=hop_ms, pull=pull_ms),
+            host_latency_ms=dict(p50=lat[len(lat) // 2] * 1e3, max=lat[-1] * 1e3),
+            paper_context="actor stall 0.64 s (32B) / 1.40 s (72B); 72B to 127 relays < 1.6 s on 128x8 H800 + RDMA",
+            cpu_baseline=cpu, e2e=e2e, gpu_launches=launches_all,
+            stats=dict(publishes=st1["publishes"] - st0["publishes"], hops=st1["hops_launched"] - st0["hops_launched"],
+                       pulls=st1["pulls"] - st0["pulls"], skipped=st1["versions_skipped"] - st0["versions_skipped"]),
+            clocks=None if args.quick else clk.summary())
+        print(json.dumps(out))
+    ctx.close()
+    if N > 1:
+        dist.barrier(group=gloo)
+        dist.destroy_process_group()
+    return 0
+
+
+class _Null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
+def run_e2e(args, rank, N, shard, bufs, mine, step, barrier, allmax, torch):
+    import psutil
+    need = (shard.buf.numel() * 4 if shard is not None else 0) + sum(b.bytes for b in bufs.values())
+    ok = psutil.virtual_memory().available > 2 * need + (8 << 30)
+    okall = allmax(0.0 if ok else 1.0) == 0.0
+    if not okall:
+        return dict(value=None, unit=UNIT, reason="not enough host RAM for pinned buffers")
+    h2d = shard.buf.to("cpu").pin_memory() if shard is not None else None
+    d2h = None
+    if mine:
+        d2h = {n: torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for n, t in bufs[mine[0]].bufs.items()}
+    step(h2d, d2h)  # warm-up with host buffers
+    torch.cuda.synchronize()
+    barrier()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    st = torch.cuda.current_stream()
+    s.record(st)
+    for _ in range(args.e2e_steps):
+        step(h2d, d2h)
+    torch.cuda.synchronize()
+    e.record(st)
+    e.synchronize()
+    ms = allmax(s.elapsed_time(e))
+    hb = int(allmax(float(shard.buf.numel() * 4) if shard is not None else 0.0))
+    db = int(allmax(float(sum(b.bytes for b in bufs.values()))))
+    return dict(value=ms / 1e3 / args.e2e_steps, unit=UNIT, h2d_bytes_per_step=hb,
+                d2h_bytes_per_step=db * max(1, N - 1), steps=args.e2e_steps,
+                note="pinned host fp32 masters -> H2D -> lam_publish -> relay -> lam_pull -> D2H of every rollout")
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,265 @@
+/*
+ * lam.h — C ABI of liblam.so: B200-native relay-tier weight synchronization
+ * (arxiv 2510.12633, "Asynchronous Weight Synchronization Using Relay Workers", §4).
+ *
+ * The path (§3.2 steps 5-7; L652-670, §4.2):
+ *   lam_publish     step 5  "the trainer pushes the new actor weights to the master relay and
+ *                           immediately resumes its next training iteration" (L548): casts the
+ *                           actor's fp32 master shard to bf16 (RNE) and packs it into the
+ *                           version's chunked bucket image in the master node's ring slot.
+ *   lam_relay_step  step 6  "the master relay then broadcasts the new weights directly to all
+ *                           other relays" (L549) as "a chain-based pipelined broadcast" (L661-665):
+ *                           non-blocking progress engine; launches chain-hop kernels that pull
+ *                           chunk j from the predecessor over NVLink while it receives j+1.
+ *   lam_pull        step 7  "A rollout can fetch the latest weights from its colocated relay at
+ *                           any time" (L550), "without waiting for the resharding and broadcast to
+ *                           complete" (L670); the reshard to the rollout's TP layout (L654) runs
+ *                           here, at pull time, in one copy-plan-driven kernel.
+ *
+ * Conventions:
+ *   - Versions are uint64, strictly increasing per publish, starting at 1; 0 means "none".
+ *   - Ownership: the caller owns the fp32 shards (unmodified until `reads_done` fires) and the
+ *     pull destination buffers (valid once `stream` reaches the enqueued work).  The library owns
+ *     the relay rings, flags, headers and plans.
+ *   - lam_publish never blocks on a relay: it enqueues and returns.  A pull never
+ *     waits on a broadcast: it serves the newest COMPLETE version at call time.
+ *   - Nothing is partially applied on error.  A corrupt chunk means the version is never marked
+ *     complete at that relay, which keeps serving its previous version.
+ *   - All calls are thread-safe (one mutex per context, process-shared across ranks).
+ *   - No CPU fallback: every byte of the snapshot is moved by kernels in this library; calls
+ *     return LAM_ECUDA when no CUDA device is usable.
+ *   - Streams and events are passed as `void*` (cudaStream_t / cudaEvent_t) so this header does
+ *     not depend on cuda_runtime.h.
+ */
+#ifndef LAM_H
+#define LAM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct lam_ctx lam_ctx;  /* opaque; owns relay rings, publish slots, flags, plans */
+typedef int32_t lam_status;      /* 0 LAM_OK; >0 informational; <0 error */
+
+enum {
+  LAM_OK = 0,
+  LAM_ENOVERSION = 1,   /* pull/latest: nothing complete yet (version_out = 0) */
+  LAM_IDLE = 2,         /* relay_step: quiescent, nothing in flight */
+  LAM_EINVAL = -1,      /* bad argument / configuration */
+  LAM_ESTALE = -2,      /* publish: version <= last published */
+  LAM_ECUDA = -3,       /* CUDA error (or no device) */
+  LAM_ECHECKSUM = -4,   /* a relay received a corrupt chunk: version not committed there */
+  LAM_ENOMEM = -5,      /* device or host allocation failed */
+  LAM_ESHUTDOWN = -6,   /* context is being destroyed */
+  LAM_EBUSY = -7,       /* publish: both master slots are in use (one is latest, the other is
+                           still being read by the chain); nothing was enqueued, retry later */
+  LAM_ETIMEOUT = -8,    /* a chain hop waited longer than spin_timeout_s for its predecessor */
+  LAM_EIPC = -9         /* shared-memory / IPC setup between rank processes failed */
+};
+
+/* Actor partition layouts ("FSDP"). */
+enum { LAM_FSDP2_DIM0 = 0, LAM_FSDP1_FLAT = 1 };
+
+/* TP rules of a destination part (vLLM convention). */
+enum { LAM_REPLICATE = 0, LAM_SHARD_DIM0 = 1, LAM_SHARD_DIM1 = 2, LAM_VOCAB_DIM0 = 3 };
+
+#define LAM_MAX_RANKS 64
+#define LAM_MAX_NODES 32
+#define LAM_MAX_ROLLOUTS 64
+#define LAM_MAX_DEVICES 16
+#define LAM_MAX_SLOTS 4
+
+/* Qwen2-family model dimensions ("Qwen2.5").  Tensor table = HF state-dict order:
+ * embed, per layer {q,q_b,k,k_b,v,v_b,o,gate,up,down,ln1,ln2}, final norm, lm_head (untied). */
+typedef struct {
+  int64_t hidden, intermediate, layers, heads, kv_heads, head_dim, vocab;
+} lam_model_dims;
+
+/* A relay node ("one relay per rollout machine"): for each actor rank r, the CUDA
+ * device that stores rank r's region of the bucket image in this node.  All entries equal = the
+ * node holds the full image on one GPU; different entries = range-sharded over several GPUs. */
+typedef struct {
+  int32_t part_device[LAM_MAX_RANKS];
+} lam_node_desc;
+
+/* A rollout: the node it pulls from (0 = the master/publish node) and the GPU its pull runs on. */
+typedef struct {
+  int32_t node;
+  int32_t device;
+} lam_rollout_desc;
+
+typedef struct {
+  lam_model_dims model;
+  int32_t actor_layout;                    /* LAM_FSDP2_DIM0 | LAM_FSDP1_FLAT */
+  int32_t fsdp_size;                       /* N actor ranks, 1..LAM_MAX_RANKS */
+  int32_t actor_device[LAM_MAX_RANKS];     /* device of actor rank r (= node 0's part devices) */
+  int32_t n_relays;                        /* relay nodes 1..n_relays, chain order 0->1->... */
+  lam_node_desc relay[LAM_MAX_NODES];      /* relay[i-1] describes node i */
+  int32_t slots;                           /* ring slots per node, 2..LAM_MAX_SLOTS */
+  uint64_t chunk_bytes;                    /* C, multiple of 4096; 0 => Appendix D k* (below) */
+  double t_start_s, t_byte_s;              /* Appendix D parameters used when chunk_bytes == 0 */
+  int32_t n_rollouts;
+  lam_rollout_desc rollout[LAM_MAX_ROLLOUTS];
+  /* processes: one per GPU (torchrun) or one for all (single-process mode: n_procs = 1) */
+  int32_t proc_rank, n_procs;
+  int32_t proc_of_device[LAM_MAX_DEVICES]; /* owning process of each device; -1 = unused */
+  char shm_name[64];                       /* POSIX shm name for the control block (n_procs > 1) */
+  /* tuning (0 => default) */
+  int32_t pack_ctas, hop_ctas, pull_ctas;
+  double spin_timeout_s;                   /* chain-hop wait limit (default 60 s) */
+} lam_config;
+
+/* One fp32 master shard piece owned by the caller: elements [elem_offset, elem_offset+elem_count)
+ * of the flattened tensor `tensor_id`, at `ptr` (device memory of the actor rank's GPU). */
+typedef struct {
+  uint32_t tensor_id;
+  uint32_t _pad;
+  uint64_t elem_offset, elem_count;
+  const float* ptr;
+} lam_shard;
+
+/* A destination buffer of a rollout TP rank: the parts' TP slices concatenated along dim 0
+ * (e.g. qkv = [q_r; k_r; v_r]).  dst_row_pitch_bytes = 0 means dense rows. */
+typedef struct {
+  uint32_t tensor_id;
+  int32_t rule;
+} lam_part;
+
+typedef struct {
+  const lam_part* parts;
+  int32_t n_parts;
+  int32_t transpose;                       /* reserved: must be 0 */
+  void* dst;                               /* device pointer on the rollout's GPU */
+  int64_t dst_row_pitch_bytes;
+} lam_dst;
+
+typedef struct {
+  int32_t tp_size, tp_rank;
+  const lam_dst* dsts;
+  int32_t n_dsts;
+} lam_tp_layout;
+
+/* Per-chunk header carried with every chunk: checksum (S1, S2) of C3. */
+typedef struct {
+  uint64_t version, idx, n, bytes, s1, s2, _pad[2];
+} lam_chunk_header;
+
+typedef struct {
+  uint64_t image_bytes;       /* C * total_chunks */
+  uint64_t chunk_bytes;       /* C */
+  uint64_t total_chunks;
+  uint64_t snapshot_bytes;    /* 2 * parameter count (the paper's M) */
+  uint64_t params;
+  int32_t n_tensors, n_nodes;
+} lam_plan_info;
+
+typedef struct {
+  uint64_t publishes, publish_busy, hops_launched, versions_skipped, pulls, checksum_errors,
+      timeouts, plan_cache_hits, plan_cache_misses;
+} lam_stats;
+
+/* ---- lifecycle ------------------------------------------------------------------------- */
+/* Validates cfg, builds the image plan, allocates this process's ring slots (S per node part on
+ * its devices, zero-filled) and the control block.  n_procs > 1: rank 0 creates the shm block
+ * `shm_name`, the others attach (waiting up to 60 s); then exchange handles with lam_export_ipc /
+ * lam_import_ipc and call lam_connect.  n_procs == 1: connected on return. */
+lam_status lam_init(const lam_config* cfg, lam_ctx** out);
+/* Serialize this process's CUDA IPC handles into buf (cap bytes); *len = bytes written. */
+lam_status lam_export_ipc(lam_ctx*, void* buf, size_t cap, size_t* len);
+/* Import the blob another process exported (call once per other process, any order). */
+lam_status lam_import_ipc(lam_ctx*, int32_t proc, const void* buf, size_t len);
+/* Open peer mappings and build the per-slot link tables; required before publish/step/pull. */
+lam_status lam_connect(lam_ctx*);
+/* Waits for this process's in-flight work, unmaps and frees. */
+void lam_destroy(lam_ctx*);
+const char* lam_strerror(lam_status);
+
+/* ---- the path -------------------------------------------------------------------------- */
+/* Publish `version` for actor rank `actor_rank` (owned by this process).  `shards` must cover
+ * every element the rank owns under cfg.actor_layout.  The pack runs on a library side stream
+ * after the work already queued on `actor_stream`; `reads_done` (caller-created event on the
+ * rank's device, may be NULL) is recorded when the shards have been read — the optimizer must
+ * wait on it before overwriting the masters.  Returns immediately (host cost: microseconds).
+ * With FSDP-N every rank calls lam_publish with the same version; the version becomes COMPLETE
+ * at node 0 when all N packs finished.  Errors: LAM_ESTALE (version not newer), LAM_EBUSY. */
+lam_status lam_publish(lam_ctx*, uint64_t version, int32_t actor_rank, const lam_shard* shards,
+                       int32_t n_shards, void* actor_stream, void* reads_done);
+
+/* Non-blocking progress: polls completions of this process's kernels, commits versions, starts
+ * chain hops for relay nodes whose predecessor holds a newer version (latest-wins), releases
+ * pins.  *n_transitions (may be NULL) = state changes made.  Returns LAM_IDLE when nothing is in
+ * flight anywhere, LAM_OK otherwise, or the first error seen (LAM_ECHECKSUM / LAM_ETIMEOUT). */
+lam_status lam_relay_step(lam_ctx*, int32_t* n_transitions);
+
+/* Pull the newest COMPLETE version at rollout `rollout_id`'s node into `layout`'s destination
+ * buffers, resharded to the TP rank, on `stream` (rollout's device).  *version_out = version
+ * pulled, or 0 with LAM_ENOVERSION.  The slot is pinned until the kernel completes. */
+lam_status lam_pull(lam_ctx*, int32_t rollout_id, const lam_tp_layout* layout, void* stream,
+                    uint64_t* version_out);
+
+/* Newest COMPLETE version at a node (0 if none; node 0 = master). */
+lam_status lam_latest(lam_ctx*, int32_t node, uint64_t* version_out);
+
+/* ---- introspection / helpers ----------------------------------------------------------- */
+lam_status lam_get_plan_info(lam_ctx*, lam_plan_info* out);
+lam_status lam_get_stats(lam_ctx*, lam_stats* out);
+/* Copy nbytes of image bytes [offset, offset+nbytes) of node `node`'s COMPLETE `version` to host
+ * memory (synchronous; debugging and parity tests).  LAM_ENOVERSION if not held complete. */
+lam_status lam_read_image(lam_ctx*, int32_t node, uint64_t version, uint64_t offset, uint64_t nbytes,
+                          void* host_dst);
+lam_status lam_read_headers(lam_ctx*, int32_t node, uint64_t version, lam_chunk_header* host_dst,
+                            uint64_t first_chunk, uint64_t n_chunks);
+
+/* Kernel timing (for the roofline report): when enabled, every pack / hop / pull launch of this
+ * process is bracketed by timing events on the stream it runs on.  lam_kernel_times returns, per
+ * kind (0 = pack, 1 = hop, 2 = pull), the summed device milliseconds and launch count of launches
+ * that completed since the last call, and resets them. */
+lam_status lam_set_profiling(lam_ctx*, int32_t on);
+lam_status lam_kernel_times(lam_ctx*, double ms_out[3], uint64_t count_out[3]);
+
+/* Test hook: device pointer (valid in this process) of actor rank `rank`'s region of the slot
+ * holding `version` (FILLING or COMPLETE) at `node`.  Used by fault-injection tests only. */
+lam_status lam_debug_region(lam_ctx*, int32_t node, uint64_t version, int32_t rank, void** dev_ptr);
+
+/* Model table of the library (independent of any caller-side copy). */
+int32_t lam_model_n_tensors(const lam_model_dims*);
+lam_status lam_model_tensor(const lam_model_dims*, int32_t tensor_id, char* name, int32_t name_cap,
+                            int64_t shape[2], int32_t* ndim);
+/* vLLM-convention destination list of one TP rank: fills up to cap_dsts dsts (dst = NULL,
+ * pitch 0) and their parts (parts array of cap_parts, referenced by the dsts), names
+ * (name_cap bytes each, in `names`), and each dst's (rows, cols) with cols = 1 for 1-D.
+ * Returns the number of dsts, or <0 on error. */
+int32_t lam_vllm_layout(const lam_model_dims*, int32_t tp_size, lam_dst* dsts, int32_t cap_dsts,
+                        lam_part* parts, int32_t cap_parts, char* names, int32_t name_cap,
+                        int64_t* rows, int64_t* cols);
+/* Host-only plan introspection (no GPU needed; used by the CPU test-suite to check the planner).
+ * Image layout: segments of cfg-equivalent (dims, layout, N, C); returns the count (or <0).  With
+ * out == NULL only counts.  image_off = byte offset of the segment in IMG(v). */
+typedef struct {
+  uint32_t tensor_id, rank;
+  uint64_t elem0, count, image_off;
+} lam_segment_info;
+int64_t lam_plan_segments(const lam_model_dims*, int32_t actor_layout, int32_t fsdp_size, uint64_t chunk_bytes,
+                          lam_segment_info* out, int64_t cap);
+/* The pull copy plan for a TP layout (destination pointers are taken as plain integers):
+ * each tile copies `rows` rows of `row_bytes` from image rank region `src_rank` at byte
+ * `src_off` (row stride src_pitch) to address `dst` (row stride dst_pitch). */
+typedef struct {
+  uint64_t src_off, dst;
+  uint32_t src_pitch, dst_pitch, rows, row_bytes, src_rank, align;
+} lam_copy_tile_info;
+int64_t lam_plan_copy_tiles(const lam_model_dims*, int32_t actor_layout, int32_t fsdp_size, uint64_t chunk_bytes,
+                            const lam_tp_layout*, lam_copy_tile_info* out, int64_t cap);
+
+/* Appendix D: chunk count k = clamp(round(sqrt((p-2) M T_byte / T_start)),
+ * 1, k_cap); and T(p, k) = (p + k - 2)(M/k T_byte + T_start). */
+int64_t lam_optimal_chunks(int32_t p, double M, double t_byte, double t_start, int64_t k_cap);
+double lam_chain_latency(int32_t p, int64_t k, double M, double t_byte, double t_start);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LAM_H */

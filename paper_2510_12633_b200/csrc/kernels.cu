@@ -1,0 +1,350 @@
+// sm_100a kernels of the relay-tier weight synchronization path.
+//
+//   k_pack  — publish: fp32 master shard -> bf16 RNE (integer
+//             arithmetic, NaN -> 0x7FC0) -> 16-B stores into the version's bucket image, per-chunk
+//             checksum (S1, S2) by warp shuffles + one u64 atomic pair per unit; the CTA finishing a
+//             chunk publishes its header and flag (st.release.sys) so the next relay, on another
+//             GPU, can start pulling that chunk while later chunks are still being packed.
+//   k_hop   — chain-pipelined broadcast hop (A3/A4): receiver-driven.  For
+//             each chunk of its part, the node waits (ld.acquire.sys on the predecessor's flag,
+//             over NVLink), copies the chunk from the predecessor's slot with 16-B peer loads into
+//             local HBM, recomputes the checksum on the way, and releases its own flag only if it
+//             matches the predecessor's header.  Few CTAs (SM-light).
+//   k_pull  — pull-time TP reshard (A6): copy-plan driven 2-D block copy from
+//             the pinned relay slot (local HBM or peer GPU) into the rollout's TP buffers.
+#include <cuda_runtime.h>
+
+#include "lam_internal.h"
+
+namespace lam {
+
+// ------------------------------------------------------------------------------- primitives
+__device__ __forceinline__ uint4 ld_stream_v4(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void st_v4(void* p, uint4 v) {
+  asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t ld_relaxed_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// fp32 bits -> bf16 bits, round to nearest even; every NaN -> 0x7FC0 (reading R1).
+__device__ __forceinline__ uint32_t rne_bf16(uint32_t u) {
+  uint32_t r = (u + 0x7FFFu + ((u >> 16) & 1u)) >> 16;
+  return ((u & 0x7FFFFFFFu) > 0x7F800000u) ? 0x7FC0u : r;
+}
+__device__ __forceinline__ uint32_t pack2(uint32_t lo, uint32_t hi) { return rne_bf16(lo) | (rne_bf16(hi) << 16); }
+
+// checksum contribution of 4 consecutive words starting at word index i0:
+//   S1 += sum w, S2 += sum (i+1) w = (i0+1)*sum + w1 + 2 w2 + 3 w3      (mod 2^64)
+__device__ __forceinline__ void cks4(uint64_t i0, uint4 w, uint64_t& s1, uint64_t& s2) {
+  uint64_t sum = (uint64_t)w.x + w.y + w.z + w.w;
+  s1 += sum;
+  s2 += (i0 + 1) * sum + (uint64_t)w.y + 2ull * w.z + 3ull * w.w;
+}
+
+template <int THREADS>
+__device__ __forceinline__ void block_reduce2(uint64_t& a, uint64_t& b, uint64_t (*sh)[THREADS / 32]) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) { sh[0][w] = a; sh[1][w] = b; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    a = 0; b = 0;
+#pragma unroll
+    for (int i = 0; i < THREADS / 32; ++i) { a += sh[0][i]; b += sh[1][i]; }
+  }
+}
+
+// ------------------------------------------------------------------------------------ k_pack
+constexpr int kPackThreads = 256;
+
+__global__ void __launch_bounds__(kPackThreads) k_pack(const PackUnit* __restrict__ units, uint32_t n_units,
+                                                       const float* const* __restrict__ shard_ptrs,
+                                                       uint8_t* __restrict__ dst, ChunkMeta meta,
+                                                       const uint32_t* __restrict__ units_per_chunk,
+                                                       uint64_t version, uint64_t n_total,
+                                                       const uint64_t* __restrict__ chunk_len) {
+  __shared__ uint64_t red[2][kPackThreads / 32];
+  for (uint32_t ui = blockIdx.x; ui < n_units; ui += gridDim.x) {
+    const PackUnit u = units[ui];
+    const float* src = shard_ptrs[u.shard] + u.src_elem;
+    uint8_t* out = dst + u.dst_off;
+    uint64_t s1 = 0, s2 = 0;
+    const uint32_t nvec = u.n >> 3;  // groups of 8 elements = 32 B in, 16 B out
+    if ((((uintptr_t)src) & 15) == 0) {
+      uint32_t v = threadIdx.x;
+      for (; v + kPackThreads < nvec; v += 2 * kPackThreads) {  // 2 groups in flight per thread
+        const uint4 a0 = ld_stream_v4(src + 8 * (size_t)v), b0 = ld_stream_v4(src + 8 * (size_t)v + 4);
+        const uint32_t v1 = v + kPackThreads;
+        const uint4 a1 = ld_stream_v4(src + 8 * (size_t)v1), b1 = ld_stream_v4(src + 8 * (size_t)v1 + 4);
+        const uint4 w0 = make_uint4(pack2(a0.x, a0.y), pack2(a0.z, a0.w), pack2(b0.x, b0.y), pack2(b0.z, b0.w));
+        const uint4 w1 = make_uint4(pack2(a1.x, a1.y), pack2(a1.z, a1.w), pack2(b1.x, b1.y), pack2(b1.z, b1.w));
+        st_v4(out + 16 * (size_t)v, w0);
+        st_v4(out + 16 * (size_t)v1, w1);
+        cks4((uint64_t)u.word0 + 4ull * v, w0, s1, s2);
+        cks4((uint64_t)u.word0 + 4ull * v1, w1, s1, s2);
+      }
+      for (; v < nvec; v += kPackThreads) {
+        const uint4 a = ld_stream_v4(src + 8 * (size_t)v), b = ld_stream_v4(src + 8 * (size_t)v + 4);
+        const uint4 w = make_uint4(pack2(a.x, a.y), pack2(a.z, a.w), pack2(b.x, b.y), pack2(b.z, b.w));
+        st_v4(out + 16 * (size_t)v, w);
+        cks4((uint64_t)u.word0 + 4ull * v, w, s1, s2);
+      }
+    } else {  // caller's shard pointer not 16-B aligned: scalar loads, same 16-B stores
+      const uint32_t* s32 = reinterpret_cast<const uint32_t*>(src);
+      for (uint32_t v = threadIdx.x; v < nvec; v += kPackThreads) {
+        const uint32_t* q = s32 + 8 * (size_t)v;
+        const uint4 w = make_uint4(pack2(q[0], q[1]), pack2(q[2], q[3]), pack2(q[4], q[5]), pack2(q[6], q[7]));
+        st_v4(out + 16 * (size_t)v, w);
+        cks4((uint64_t)u.word0 + 4ull * v, w, s1, s2);
+      }
+    }
+    // ragged tail (< 8 elements, only at a segment end): element pairs -> words, zero high half
+    {
+      const uint32_t* s32 = reinterpret_cast<const uint32_t*>(src);
+      uint16_t* o16 = reinterpret_cast<uint16_t*>(out);
+      for (uint32_t e = nvec * 8 + 2 * threadIdx.x; e < u.n; e += 2 * kPackThreads) {
+        const uint32_t lo = rne_bf16(s32[e]);
+        const uint32_t hi = (e + 1 < u.n) ? rne_bf16(s32[e + 1]) : 0u;
+        o16[e] = (uint16_t)lo;
+        if (e + 1 < u.n) o16[e + 1] = (uint16_t)hi;
+        const uint64_t w = lo | (hi << 16);
+        s1 += w;
+        s2 += ((uint64_t)u.word0 + e / 2 + 1) * w;
+      }
+    }
+    __threadfence_system();  // this thread's image stores before the chunk's completion count
+    block_reduce2<kPackThreads>(s1, s2, red);
+    if (threadIdx.x == 0) {
+      lam_chunk_header* h = meta.hdr + u.chunk;
+      atomicAdd((unsigned long long*)&h->s1, (unsigned long long)s1);
+      atomicAdd((unsigned long long*)&h->s2, (unsigned long long)s2);
+      __threadfence_system();
+      const uint32_t prev = atomicAdd(meta.cnt + u.chunk, 1u);
+      if (prev + 1 == units_per_chunk[u.chunk]) {  // last unit of the chunk: publish it
+        __threadfence_system();
+        h->version = version;
+        h->idx = u.chunk;
+        h->n = n_total;
+        h->bytes = chunk_len[u.chunk];
+        __threadfence_system();
+        st_release_sys(meta.flags + u.chunk, version);
+      }
+    }
+    __syncthreads();  // red[] reuse
+  }
+}
+
+int launch_pack(const PackUnit* units, uint32_t n_units, const float* const* shard_ptrs, uint8_t* dst,
+                ChunkMeta meta, const uint32_t* units_per_chunk, uint64_t version, uint64_t n_total,
+                const uint64_t* chunk_len, int ctas, void* stream) {
+  if (n_units == 0) return 0;
+  unsigned grid = (unsigned)(n_units < (uint32_t)ctas ? n_units : (uint32_t)ctas);
+  k_pack<<<grid, kPackThreads, 0, (cudaStream_t)stream>>>(units, n_units, shard_ptrs, dst, meta,
+                                                          units_per_chunk, version, n_total, chunk_len);
+  return (int)cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------- k_hop
+constexpr int kHopThreads = 512;
+constexpr int kHopUnroll = 8;  // 8 x 16 B peer loads in flight per thread (64 KiB per CTA)
+
+enum : int { kHopOk = 0, kHopPoison = 1, kHopAbort = 2, kHopTimeout = 3 };
+
+__device__ void hop_fail(ChunkMeta meta, uint32_t* err_word, uint32_t chunk, uint64_t version, int why) {
+  atomicExch(meta.abort_flag, 1);
+  const uint32_t code = (why == kHopTimeout) ? (uint32_t)(-LAM_ETIMEOUT) : (uint32_t)(-LAM_ECHECKSUM);
+  atomicCAS(err_word, 0u, code);
+  st_release_sys(meta.flags + chunk, version | kPoison);  // tell our successor
+  __threadfence_system();
+}
+
+__global__ void __launch_bounds__(kHopThreads) k_hop(const HopTile* __restrict__ tiles, uint32_t n_tiles,
+                                                     const RankLink* __restrict__ links, ChunkMeta meta,
+                                                     const uint32_t* __restrict__ tiles_per_chunk,
+                                                     uint64_t version, uint32_t* err_word, uint64_t timeout_ns) {
+  __shared__ uint64_t red[2][kHopThreads / 32];
+  __shared__ uint32_t ready_chunk;
+  __shared__ int status;
+  if (threadIdx.x == 0) ready_chunk = 0xFFFFFFFFu;
+  __syncthreads();
+  const uint64_t deadline = globaltimer() + timeout_ns;
+  for (uint32_t ti = blockIdx.x; ti < n_tiles; ti += gridDim.x) {
+    const HopTile T = tiles[ti];
+    const RankLink L = links[T.rank];
+    if (T.chunk != ready_chunk) {
+      if (threadIdx.x == 0) {
+        int st = kHopOk;
+        for (uint32_t spin = 0;; ++spin) {
+          const uint64_t f = ld_acquire_sys(L.src_flags + T.chunk);
+          if (f == version) break;
+          if (f == (version | kPoison)) { st = kHopPoison; break; }
+          if (*(volatile int32_t*)meta.abort_flag) { st = kHopAbort; break; }
+          if ((spin & 63) == 63 && globaltimer() > deadline) { st = kHopTimeout; break; }
+          __nanosleep(spin < 64 ? 64 : 512);
+        }
+        status = st;
+        ready_chunk = T.chunk;
+        if (st != kHopOk) hop_fail(meta, err_word, T.chunk, version, st);
+      }
+      __syncthreads();
+      if (status != kHopOk) return;
+    }
+    const uint8_t* src = L.src + T.region_off;
+    uint8_t* dst = L.dst + T.region_off;
+    const uint32_t nvec = T.bytes >> 4;
+    uint64_t s1 = 0, s2 = 0;
+    for (uint32_t v0 = threadIdx.x; v0 < nvec; v0 += kHopThreads * kHopUnroll) {
+      uint4 w[kHopUnroll];
+#pragma unroll
+      for (int k = 0; k < kHopUnroll; ++k) {
+        const uint32_t v = v0 + k * kHopThreads;
+        if (v < nvec) w[k] = ld_stream_v4(src + 16 * (size_t)v);
+      }
+#pragma unroll
+      for (int k = 0; k < kHopUnroll; ++k) {
+        const uint32_t v = v0 + k * kHopThreads;
+        if (v < nvec) {
+          st_v4(dst + 16 * (size_t)v, w[k]);
+          cks4((uint64_t)T.word0 + 4ull * v, w[k], s1, s2);
+        }
+      }
+    }
+    __threadfence_system();
+    block_reduce2<kHopThreads>(s1, s2, red);
+    if (threadIdx.x == 0) {
+      lam_chunk_header* h = meta.hdr + T.chunk;
+      atomicAdd((unsigned long long*)&h->s1, (unsigned long long)s1);
+      atomicAdd((unsigned long long*)&h->s2, (unsigned long long)s2);
+      __threadfence_system();
+      const uint32_t prev = atomicAdd(meta.cnt + T.chunk, 1u);
+      if (prev + 1 == tiles_per_chunk[T.chunk]) {  // last tile: verify against the predecessor
+        __threadfence_system();
+        const uint64_t got1 = atomicAdd((unsigned long long*)&h->s1, 0ull);
+        const uint64_t got2 = atomicAdd((unsigned long long*)&h->s2, 0ull);
+        const lam_chunk_header* ph = L.src_hdr + T.chunk;
+        const uint64_t want1 = ld_relaxed_sys(&ph->s1), want2 = ld_relaxed_sys(&ph->s2);
+        if (got1 == want1 && got2 == want2) {
+          h->version = ld_relaxed_sys(&ph->version);
+          h->idx = ld_relaxed_sys(&ph->idx);
+          h->n = ld_relaxed_sys(&ph->n);
+          h->bytes = ld_relaxed_sys(&ph->bytes);
+          __threadfence_system();
+          st_release_sys(meta.flags + T.chunk, version);
+        } else {
+          hop_fail(meta, err_word, T.chunk, version, kHopPoison);
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+int launch_hop(const HopTile* tiles, uint32_t n_tiles, const RankLink* links, ChunkMeta meta,
+               const uint32_t* tiles_per_chunk, uint64_t version, uint32_t* err_word, uint64_t timeout_ns,
+               int ctas, void* stream) {
+  if (n_tiles == 0) return 0;
+  unsigned grid = (unsigned)(n_tiles < (uint32_t)ctas ? n_tiles : (uint32_t)ctas);
+  k_hop<<<grid, kHopThreads, 0, (cudaStream_t)stream>>>(tiles, n_tiles, links, meta, tiles_per_chunk, version,
+                                                        err_word, timeout_ns);
+  return (int)cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------ k_pull
+constexpr int kPullThreads = 512;
+constexpr int kPullUnroll = 4;
+
+__global__ void __launch_bounds__(kPullThreads) k_pull(const CopyTile* __restrict__ tiles, uint32_t n_tiles,
+                                                       const uint8_t* const* __restrict__ rank_base) {
+  for (uint32_t ti = blockIdx.x; ti < n_tiles; ti += gridDim.x) {
+    const CopyTile T = tiles[ti];
+    const uint8_t* src = rank_base[T.src_rank] + T.src_off;
+    uint8_t* dst = reinterpret_cast<uint8_t*>(T.dst);
+    if (T.align == 16) {
+      const uint32_t vpr = T.row_bytes >> 4, total = vpr * T.rows;
+      if (T.rows == 1) {
+        for (uint32_t v0 = threadIdx.x; v0 < total; v0 += kPullThreads * kPullUnroll) {
+          uint4 w[kPullUnroll];
+#pragma unroll
+          for (int k = 0; k < kPullUnroll; ++k) {
+            const uint32_t v = v0 + k * kPullThreads;
+            if (v < total) w[k] = ld_stream_v4(src + 16 * (size_t)v);
+          }
+#pragma unroll
+          for (int k = 0; k < kPullUnroll; ++k) {
+            const uint32_t v = v0 + k * kPullThreads;
+            if (v < total) st_v4(dst + 16 * (size_t)v, w[k]);
+          }
+        }
+      } else {
+        for (uint32_t v0 = threadIdx.x; v0 < total; v0 += kPullThreads * kPullUnroll) {
+          uint4 w[kPullUnroll];
+#pragma unroll
+          for (int k = 0; k < kPullUnroll; ++k) {
+            const uint32_t v = v0 + k * kPullThreads;
+            if (v < total) {
+              const uint32_t r = v / vpr, c = v - r * vpr;
+              w[k] = ld_stream_v4(src + (size_t)r * T.src_pitch + 16 * (size_t)c);
+            }
+          }
+#pragma unroll
+          for (int k = 0; k < kPullUnroll; ++k) {
+            const uint32_t v = v0 + k * kPullThreads;
+            if (v < total) {
+              const uint32_t r = v / vpr, c = v - r * vpr;
+              st_v4(dst + (size_t)r * T.dst_pitch + 16 * (size_t)c, w[k]);
+            }
+          }
+        }
+      }
+    } else if (T.align == 4) {
+      const uint32_t wpr = T.row_bytes >> 2, total = wpr * T.rows;
+      for (uint32_t v = threadIdx.x; v < total; v += kPullThreads) {
+        const uint32_t r = v / wpr, c = v - r * wpr;
+        *reinterpret_cast<uint32_t*>(dst + (size_t)r * T.dst_pitch + 4 * (size_t)c) =
+            *reinterpret_cast<const uint32_t*>(src + (size_t)r * T.src_pitch + 4 * (size_t)c);
+      }
+    } else {
+      const uint32_t hpr = T.row_bytes >> 1, total = hpr * T.rows;
+      for (uint32_t v = threadIdx.x; v < total; v += kPullThreads) {
+        const uint32_t r = v / hpr, c = v - r * hpr;
+        *reinterpret_cast<uint16_t*>(dst + (size_t)r * T.dst_pitch + 2 * (size_t)c) =
+            *reinterpret_cast<const uint16_t*>(src + (size_t)r * T.src_pitch + 2 * (size_t)c);
+      }
+    }
+  }
+}
+
+int launch_pull(const CopyTile* tiles, uint32_t n_tiles, const uint8_t* const* rank_base, int ctas, void* stream) {
+  if (n_tiles == 0) return 0;
+  unsigned grid = (unsigned)(n_tiles < (uint32_t)ctas ? n_tiles : (uint32_t)ctas);
+  k_pull<<<grid, kPullThreads, 0, (cudaStream_t)stream>>>(tiles, n_tiles, rank_base);
+  return (int)cudaGetLastError();
+}
+
+}  // namespace lam

@@ -1,0 +1,303 @@
+// Host planning: actor layout -> chunked bucket image, and the work-descriptor tables the kernels
+// consume (pack units, chain-hop tiles, pull copy tiles).  Written for the library; the oracle's
+// definitions live elsewhere and share nothing with this file.
+//
+// Image format ("chunks them", L1467 "divided into k smaller
+// chunks"): rank regions in rank order, each holding the rank's FSDP segments in tensor order at
+// 256-B aligned offsets, region length rounded to 256 B, cut into chunks of C bytes (last short),
+// regions placed chunk-aligned.
+#include <algorithm>
+#include <map>
+
+#include "lam_internal.h"
+
+namespace lam {
+
+uint64_t ImagePlan::chunk_len(uint64_t g) const {
+  uint32_t r = chunk_rank[g];
+  uint64_t j = g - chunk_base[r];
+  uint64_t rem = region_len[r] - j * C;
+  return rem < C ? rem : C;
+}
+
+bool build_image_plan(const std::vector<Tensor>& ts, int N, int layout, uint64_t C, ImagePlan* out) {
+  if (N < 1 || N > LAM_MAX_RANKS || C == 0 || C % kChunkAlign) return false;
+  ImagePlan p;
+  p.C = C;
+  p.N = N;
+  p.by_tensor.assign(ts.size(), {});
+  // per rank: (tensor, elem0, count)
+  std::vector<std::vector<Segment>> per(N);
+  if (layout == LAM_FSDP2_DIM0) {
+    for (uint32_t t = 0; t < ts.size(); ++t) {
+      uint64_t d0 = ts[t].d0, row = ts[t].d1, rows = cdiv(d0, N);
+      for (int r = 0; r < N; ++r) {
+        uint64_t a = (uint64_t)r * rows, b = std::min<uint64_t>(d0, (uint64_t)(r + 1) * rows);
+        if (b > a) per[r].push_back({t, (uint32_t)r, a * row, (b - a) * row, 0});
+      }
+    }
+  } else if (layout == LAM_FSDP1_FLAT) {
+    uint64_t P = 0;
+    std::vector<uint64_t> start(ts.size() + 1, 0);
+    for (size_t t = 0; t < ts.size(); ++t) start[t + 1] = start[t] + ts[t].numel();
+    P = start.back();
+    uint64_t each = cdiv(P, N);
+    for (int r = 0; r < N; ++r) {
+      uint64_t a = (uint64_t)r * each, b = std::min<uint64_t>(P, (uint64_t)(r + 1) * each);
+      for (uint32_t t = 0; t < ts.size(); ++t) {
+        uint64_t lo = std::max(a, start[t]), hi = std::min(b, start[t + 1]);
+        if (hi > lo) per[r].push_back({t, (uint32_t)r, lo - start[t], hi - lo, 0});
+      }
+    }
+  } else {
+    return false;
+  }
+  uint64_t base = 0;
+  for (int r = 0; r < N; ++r) {
+    uint64_t off = 0;
+    for (auto s : per[r]) {
+      off = align_up(off, kSegAlign);
+      s.off = off;
+      off += 2 * s.count;
+      p.by_tensor[s.tensor].push_back((uint32_t)p.segs.size());
+      p.segs.push_back(s);
+    }
+    uint64_t L = align_up(off, kSegAlign);
+    p.region_len.push_back(L);
+    p.n_chunks.push_back(cdiv(L, C));
+    p.chunk_base.push_back(base);
+    base += p.n_chunks.back();
+    for (uint64_t j = 0; j < p.n_chunks.back(); ++j) p.chunk_rank.push_back((uint32_t)r);
+  }
+  p.total_chunks = base;
+  if (p.total_chunks >= (1ull << 32)) return false;
+  *out = std::move(p);
+  return true;
+}
+
+bool build_pack_units(const ImagePlan& p, const std::vector<Tensor>& ts, int rank,
+                      const std::vector<lam_shard>& shards, uint64_t region_base_in_part,
+                      std::vector<PackUnit>* units, std::vector<uint32_t>* units_per_chunk,
+                      std::string* err) {
+  (void)ts;
+  units->clear();
+  units_per_chunk->assign(p.total_chunks, 0);
+  std::map<uint32_t, std::vector<uint32_t>> by_t;
+  for (uint32_t i = 0; i < shards.size(); ++i) by_t[shards[i].tensor_id].push_back(i);
+  for (const Segment& s : p.segs) {
+    if ((int)s.rank != rank) continue;
+    // find the shard covering [elem0, elem0+count)
+    int found = -1;
+    for (uint32_t i : by_t[s.tensor]) {
+      const lam_shard& sh = shards[i];
+      if (sh.elem_offset <= s.elem0 && s.elem0 + s.count <= sh.elem_offset + sh.elem_count) {
+        found = (int)i;
+        break;
+      }
+    }
+    if (found < 0) {
+      *err = "no shard covers tensor " + std::to_string(s.tensor) + " elements [" +
+             std::to_string(s.elem0) + ", " + std::to_string(s.elem0 + s.count) + ") of rank " +
+             std::to_string(rank);
+      return false;
+    }
+    uint64_t src0 = s.elem0 - shards[found].elem_offset;
+    uint64_t e = 0;
+    while (e < s.count) {
+      uint64_t byte = s.off + 2 * e;                 // region offset of this unit's first output byte
+      uint64_t g = p.chunk_base[rank] + byte / p.C;
+      uint64_t chunk_end = (byte / p.C + 1) * p.C;   // region offset where the chunk ends
+      uint64_t n = std::min<uint64_t>(kPackUnitElems, s.count - e);
+      n = std::min<uint64_t>(n, (chunk_end - byte) / 2);
+      PackUnit u;
+      u.src_elem = src0 + e;
+      u.dst_off = region_base_in_part + byte;
+      u.shard = (uint32_t)found;
+      u.n = (uint32_t)n;
+      u.chunk = (uint32_t)g;
+      u.word0 = (uint32_t)((byte % p.C) / 4);
+      units->push_back(u);
+      (*units_per_chunk)[g]++;
+      e += n;
+    }
+  }
+  return true;
+}
+
+void build_hop_tiles(const ImagePlan& p, const std::vector<int>& ranks, std::vector<HopTile>* tiles,
+                     std::vector<uint32_t>* tiles_per_chunk) {
+  tiles->clear();
+  tiles_per_chunk->assign(p.total_chunks, 0);
+  for (int r : ranks) {
+    for (uint64_t j = 0; j < p.n_chunks[r]; ++j) {
+      uint64_t g = p.chunk_base[r] + j;
+      uint64_t len = p.chunk_len(g);
+      for (uint64_t o = 0; o < len; o += kHopTileBytes) {
+        HopTile t;
+        t.region_off = j * p.C + o;
+        t.chunk = (uint32_t)g;
+        t.rank = (uint32_t)r;
+        t.bytes = (uint32_t)std::min<uint64_t>(kHopTileBytes, len - o);
+        t.word0 = (uint32_t)(o / 4);
+        tiles->push_back(t);
+        (*tiles_per_chunk)[g]++;
+      }
+    }
+  }
+  // order tiles by chunk so the pipeline advances chunk by chunk across all ranks of the part
+  std::stable_sort(tiles->begin(), tiles->end(),
+                   [](const HopTile& a, const HopTile& b) { return a.chunk < b.chunk; });
+}
+
+static uint32_t widest_align(uint64_t a, uint64_t b, uint64_t c, uint64_t d, uint64_t e) {
+  uint64_t x = a | b | c | d | e;
+  if (x % 16 == 0) return 16;
+  if (x % 4 == 0) return 4;
+  return 2;
+}
+
+// Emit the 2-D block {rows x row_bytes} in tiles of <= kPullTileBytes.
+static void emit_block(std::vector<CopyTile>* out, uint32_t rank, uint64_t src_off, uint64_t dst,
+                       uint64_t src_pitch, uint64_t dst_pitch, uint64_t rows, uint64_t row_bytes) {
+  if (rows == 0 || row_bytes == 0) return;
+  if (row_bytes >= kPullTileBytes || rows == 1) {
+    for (uint64_t r = 0; r < rows; ++r)
+      for (uint64_t o = 0; o < row_bytes; o += kPullTileBytes) {
+        uint64_t n = std::min<uint64_t>(kPullTileBytes, row_bytes - o);
+        CopyTile t{src_off + r * src_pitch + o, dst + r * dst_pitch + o, 0, 0, 1, (uint32_t)n, rank, 0};
+        t.align = widest_align(t.src_off, t.dst, n, 0, 0);
+        out->push_back(t);
+      }
+    return;
+  }
+  uint64_t per = std::max<uint64_t>(1, kPullTileBytes / row_bytes);
+  for (uint64_t r = 0; r < rows; r += per) {
+    uint64_t n = std::min<uint64_t>(per, rows - r);
+    CopyTile t{src_off + r * src_pitch, dst + r * dst_pitch, (uint32_t)src_pitch, (uint32_t)dst_pitch,
+               (uint32_t)n, (uint32_t)row_bytes, rank, 0};
+    t.align = widest_align(t.src_off, t.dst, row_bytes, src_pitch, dst_pitch);
+    out->push_back(t);
+  }
+}
+
+bool build_copy_tiles(const ImagePlan& p, const std::vector<Tensor>& ts, const lam_tp_layout& L,
+                      std::vector<CopyTile>* tiles, uint64_t* bytes, std::string* err) {
+  tiles->clear();
+  *bytes = 0;
+  if (L.tp_size < 1 || L.tp_rank < 0 || L.tp_rank >= L.tp_size || L.n_dsts < 0 || (L.n_dsts && !L.dsts)) {
+    *err = "bad tp layout";
+    return false;
+  }
+  for (int k = 0; k < L.n_dsts; ++k) {
+    const lam_dst& d = L.dsts[k];
+    if (d.transpose) { *err = "transpose destinations are not supported yet"; return false; }
+    if (!d.dst || d.n_parts < 1 || !d.parts) { *err = "dst " + std::to_string(k) + ": empty"; return false; }
+    int64_t width = -1;
+    uint64_t row0 = 0;   // destination row where the current part starts
+    for (int q = 0; q < d.n_parts; ++q) {
+      if (d.parts[q].tensor_id >= ts.size()) { *err = "bad tensor id"; return false; }
+      const Tensor& t = ts[d.parts[q].tensor_id];
+      int64_t r0, r1, c0, c1;
+      if (!part_slice(t, d.parts[q].rule, L.tp_size, L.tp_rank, &r0, &r1, &c0, &c1)) {
+        *err = "rule not applicable to " + t.name;
+        return false;
+      }
+      int64_t w = c1 - c0;
+      if (width >= 0 && w != width) { *err = "parts of different widths in one dst"; return false; }
+      width = w;
+      uint64_t dpitch = d.dst_row_pitch_bytes ? (uint64_t)d.dst_row_pitch_bytes : (uint64_t)w * 2;
+      if (dpitch < (uint64_t)w * 2) { *err = "row pitch smaller than the row"; return false; }
+      const uint64_t dbase = (uint64_t)(uintptr_t)d.dst;
+      // The slice as runs in the flattened source tensor: run k = [start_k, start_k + run) with
+      // start_k = (r0 + k) * d1 + c0; a full-row slice is one contiguous run.
+      bool full = (c0 == 0 && c1 == t.d1);
+      uint64_t run = full ? (uint64_t)(r1 - r0) * t.d1 : (uint64_t)w;
+      uint64_t nrun = full ? 1 : (uint64_t)(r1 - r0);
+      uint64_t first = (uint64_t)r0 * t.d1 + c0, stride = (uint64_t)t.d1;
+      for (uint32_t si : p.by_tensor[d.parts[q].tensor_id]) {
+        const Segment& s = p.segs[si];
+        uint64_t e0 = s.elem0, e1 = s.elem0 + s.count;
+        // runs overlapping [e0, e1): start_k + run > e0 and start_k < e1
+        uint64_t klo = 0, khi = nrun;  // [klo, khi)
+        if (nrun > 1) {
+          klo = (e0 + 1 > first + run) ? (e0 + 1 - run - first + stride - 1) / stride : 0;
+          khi = (e1 > first) ? std::min<uint64_t>(nrun, (e1 - first + stride - 1) / stride) : 0;
+        } else if (!(first + run > e0 && first < e1)) {
+          continue;
+        }
+        auto dst_of = [&](uint64_t k, uint64_t col) {   // dst address of run k, element col
+          return full ? dbase + (row0 * (uint64_t)w + col) * 2  // contiguous: col indexes the run
+                      : dbase + (row0 + k) * dpitch + col * 2;
+        };
+        auto src_of = [&](uint64_t el) { return s.off + (el - e0) * 2; };
+        uint64_t k = klo;
+        while (k < khi) {
+          uint64_t a = first + k * stride, b = a + run;  // run k's elements
+          uint64_t lo = std::max(a, e0), hi = std::min(b, e1);
+          if (lo >= hi) { ++k; continue; }
+          if (lo == a && hi == b && !full) {
+            // maximal stretch of whole runs inside the segment
+            uint64_t k2 = k;
+            while (k2 < khi && first + k2 * stride >= e0 && first + k2 * stride + run <= e1) ++k2;
+            emit_block(tiles, s.rank, src_of(a), dst_of(k, 0), stride * 2, dpitch, k2 - k, run * 2);
+            *bytes += (k2 - k) * run * 2;
+            k = k2;
+            continue;
+          }
+          if (full && dpitch != (uint64_t)w * 2) {
+            // pitched destination with full-row source: emit row by row pieces
+            for (uint64_t el = lo; el < hi;) {
+              uint64_t row = el / t.d1, col = el % t.d1;
+              uint64_t n = std::min<uint64_t>(hi - el, t.d1 - col);
+              emit_block(tiles, s.rank, src_of(el), dbase + (row0 + row - r0) * dpitch + col * 2, 0, 0, 1, n * 2);
+              el += n;
+            }
+          } else {
+            emit_block(tiles, s.rank, src_of(lo), dst_of(k, lo - a), 0, 0, 1, (hi - lo) * 2);
+          }
+          *bytes += (hi - lo) * 2;
+          ++k;
+        }
+      }
+      row0 += (uint64_t)(r1 - r0);
+    }
+  }
+  return true;
+}
+
+}  // namespace lam
+
+using namespace lam;
+
+extern "C" int64_t lam_plan_segments(const lam_model_dims* d, int32_t layout, int32_t N, uint64_t C,
+                                     lam_segment_info* out, int64_t cap) {
+  if (!d || !model_valid(*d)) return LAM_EINVAL;
+  ImagePlan p;
+  if (!build_image_plan(model_tensors(*d), N, layout, C, &p)) return LAM_EINVAL;
+  if (out) {
+    for (size_t i = 0; i < p.segs.size() && (int64_t)i < cap; ++i) {
+      const Segment& s = p.segs[i];
+      out[i] = lam_segment_info{s.tensor, s.rank, s.elem0, s.count, p.chunk_base[s.rank] * p.C + s.off};
+    }
+  }
+  return (int64_t)p.segs.size();
+}
+
+extern "C" int64_t lam_plan_copy_tiles(const lam_model_dims* d, int32_t layout, int32_t N, uint64_t C,
+                                       const lam_tp_layout* L, lam_copy_tile_info* out, int64_t cap) {
+  if (!d || !L || !model_valid(*d)) return LAM_EINVAL;
+  std::vector<Tensor> ts = model_tensors(*d);
+  ImagePlan p;
+  if (!build_image_plan(ts, N, layout, C, &p)) return LAM_EINVAL;
+  std::vector<CopyTile> tiles;
+  uint64_t bytes = 0;
+  std::string err;
+  if (!build_copy_tiles(p, ts, *L, &tiles, &bytes, &err)) return LAM_EINVAL;
+  if (out) {
+    for (size_t i = 0; i < tiles.size() && (int64_t)i < cap; ++i) {
+      const CopyTile& t = tiles[i];
+      out[i] = lam_copy_tile_info{t.src_off, t.dst, t.src_pitch, t.dst_pitch, t.rows, t.row_bytes, t.src_rank, t.align};
+    }
+  }
+  return (int64_t)tiles.size();
+}

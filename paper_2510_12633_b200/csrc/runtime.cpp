@@ -1,0 +1,1122 @@
+// liblam runtime: relay rings + version tables, publish, progress engine, pull, IPC.
+//
+// Control plane (PAPER L526-529 relays; L548-550 steps 5-7; SPEC L527-663 relay semantics):
+//   * node 0 = the master: the actor's publish slots on the actor GPUs (the chain head);
+//     nodes 1..R = relays in chain order.  Every node has S ring slots ("retain 2").
+//   * slot states FREE -> FILLING(v) -> COMPLETE(v); `latest` only moves up and only
+//     to COMPLETE versions (SPEC L633 complete-only serving).
+//   * a node starts receiving the NEWEST version its predecessor holds (FILLING or COMPLETE) into a
+//     FREE slot or a COMPLETE slot with no readers that is not its latest (latest-wins),
+//     pinning the predecessor's slot until its hop kernels finish.
+//   * a pull pins the latest slot (readers++) until its reshard kernel completes.
+// The block lives in POSIX shared memory when there is one process per GPU (torchrun), guarded by
+// a robust process-shared mutex; peer slots are mapped with CUDA IPC handles.
+#include <cuda_runtime.h>
+#include <errno.h>
+#include <fcntl.h>
+#include <pthread.h>
+#include <stdio.h>
+#include <string.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <time.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <map>
+#include <memory>
+#include <set>
+#include <string>
+#include <vector>
+
+#include "lam_internal.h"
+
+namespace lam {
+
+enum : int32_t { S_FREE = 0, S_FILLING = 1, S_COMPLETE = 2 };
+
+struct ShmSlot {
+  uint64_t version;
+  int32_t state, readers;
+  int32_t parts_done, parts_finished;  // node 0: ranks packed; relays: parts completed ok / at all
+  int32_t err, src_slot;               // first error; predecessor slot pinned while FILLING
+  uint64_t launched_mask;              // node 0: ranks published; relays: parts launched
+};
+struct ShmNode {
+  ShmSlot slot[LAM_MAX_SLOTS];
+  uint64_t latest, started, skipped;
+};
+struct Shm {
+  uint64_t magic;
+  pthread_mutex_t mu;
+  uint64_t last_published;
+  int32_t ready_procs;
+  lam_stats stats;
+  ShmNode node[LAM_MAX_NODES + 1];
+};
+constexpr uint64_t kMagic = 0x4c414d5f53484d31ull;  // "LAM_SHM1"
+
+struct SlotMeta {   // byte offsets inside a slot's metadata block
+  uint64_t flags, hdr, cnt, abort, bytes;
+};
+
+struct Part {
+  int node = 0, device = 0, index = 0, pos = 0;  // pos: index within its node (launch-mask bit)
+  std::vector<int> ranks;            // actor ranks whose regions this part stores
+  std::vector<int64_t> rank_off;     // [N] offset of rank r's region in slot data, -1 if not here
+  uint64_t slot_data = 0, slot_stride = 0, meta_base = 0, meta_stride = 0, alloc_bytes = 0;
+  bool local = false;
+  uint8_t* base = nullptr;           // valid in this process (own allocation or IPC mapping)
+  bool ipc_opened = false;
+  // local-only
+  cudaStream_t stream = nullptr;
+  cudaEvent_t done_ev[LAM_MAX_SLOTS] = {};
+  uint64_t inflight_version[LAM_MAX_SLOTS] = {};   // version of the kernel in flight (0 none)
+  uint32_t* err_host = nullptr;      // [S] host-mapped error words
+  uint32_t* err_dev = nullptr;
+  HopTile* d_tiles = nullptr;
+  uint32_t n_tiles = 0;
+  uint32_t* d_tiles_per_chunk = nullptr;
+  RankLink* d_links = nullptr;       // [S][S][N] (my slot, pred slot, rank)
+};
+
+struct RankPub {   // per local actor rank (node 0)
+  cudaEvent_t ev[LAM_MAX_SLOTS] = {};
+  uint64_t inflight_version[LAM_MAX_SLOTS] = {};
+  std::vector<lam_shard> key;        // cached shard list of the last unit build
+  PackUnit* d_units = nullptr;
+  uint32_t n_units = 0, cap_units = 0;
+  uint32_t* d_units_per_chunk = nullptr;
+  const float** d_ptrs = nullptr;
+  uint32_t cap_ptrs = 0;
+  const float** h_ptrs = nullptr;    // pinned staging of the shard pointer table
+};
+
+struct PullPlan {
+  CopyTile* d_tiles = nullptr;
+  uint32_t n_tiles = 0;
+  uint64_t bytes = 0;
+};
+
+struct PendingPull {
+  cudaEvent_t ev;
+  int node, slot, device;
+};
+
+struct DevLocal {
+  uint64_t* d_chunk_len = nullptr;   // per device: [total_chunks]
+  cudaStream_t side = nullptr;
+};
+
+}  // namespace lam
+
+using namespace lam;
+
+struct lam_ctx {
+  lam_config cfg;
+  std::vector<Tensor> ts;
+  ImagePlan plan;
+  uint64_t params = 0;
+  int S = 2, n_nodes = 1;
+  SlotMeta sm;
+  std::vector<std::vector<int>> node_parts;   // node -> part indices
+  std::vector<std::vector<int>> node_rank_part;  // node -> [N] part index holding rank r
+  std::vector<Part> parts;
+  std::vector<RankPub> pubs;                  // [N]; local ranks only used
+  std::map<int, DevLocal> dev;                // devices owned by this process
+  std::map<std::string, PullPlan> plans;
+  std::map<std::pair<int, int>, const uint8_t**> d_rank_base;  // (node*S+slot, device) -> device array
+  std::vector<PendingPull> pending;
+  std::map<int, std::vector<cudaEvent_t>> ev_pool;  // per device
+  Shm* shm = nullptr;
+  bool shm_owner = false, shm_mapped = false;
+  bool connected = false;
+  lam_status pending_error = LAM_OK;
+  uint64_t timeout_ns = 60ull * 1000000000ull;
+  int pack_ctas = 0, hop_ctas = 0, pull_ctas = 0;
+  // kernel timing (lam_set_profiling)
+  bool profiling = false;
+  struct Timed { int kind, dev; cudaEvent_t a, b; };
+  std::vector<Timed> timed;
+  std::map<int, std::vector<cudaEvent_t>> tev_pool;  // timing-enabled events per device
+};
+
+namespace {
+
+struct Lock {
+  pthread_mutex_t* m;
+  explicit Lock(Shm* s) : m(&s->mu) {
+    int rc = pthread_mutex_lock(m);
+    if (rc == EOWNERDEAD) pthread_mutex_consistent(m);
+  }
+  ~Lock() { pthread_mutex_unlock(m); }
+};
+
+bool owns(const lam_ctx* c, int device) {
+  return device >= 0 && device < LAM_MAX_DEVICES && c->cfg.proc_of_device[device] == c->cfg.proc_rank;
+}
+
+int node_part_device(const lam_ctx* c, int node, int rank) {
+  return node == 0 ? c->cfg.actor_device[rank] : c->cfg.relay[node - 1].part_device[rank];
+}
+
+#define CK(x)                                             \
+  do {                                                    \
+    cudaError_t e_ = (x);                                 \
+    if (e_ != cudaSuccess) {                              \
+      fprintf(stderr, "liblam: %s failed: %s (%s:%d)\n", #x, cudaGetErrorString(e_), __FILE__, __LINE__); \
+      return LAM_ECUDA;                                   \
+    }                                                     \
+  } while (0)
+
+// events belong to the device current at creation: pool them per device (caller set the device)
+cudaEvent_t get_event(lam_ctx* c, int dev) {
+  auto& pool = c->ev_pool[dev];
+  if (!pool.empty()) {
+    cudaEvent_t e = pool.back();
+    pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  return e;
+}
+
+cudaEvent_t prof_begin(lam_ctx* c, int dev, cudaStream_t st) {
+  if (!c->profiling) return nullptr;
+  auto& pool = c->tev_pool[dev];
+  cudaEvent_t e = nullptr;
+  if (!pool.empty()) { e = pool.back(); pool.pop_back(); } else { cudaEventCreate(&e); }
+  cudaEventRecord(e, st);
+  return e;
+}
+
+void prof_end(lam_ctx* c, int kind, int dev, cudaStream_t st, cudaEvent_t a) {
+  if (!a) return;
+  auto& pool = c->tev_pool[dev];
+  cudaEvent_t e = nullptr;
+  if (!pool.empty()) { e = pool.back(); pool.pop_back(); } else { cudaEventCreate(&e); }
+  cudaEventRecord(e, st);
+  c->timed.push_back({kind, dev, a, e});
+}
+
+ChunkMeta meta_of(const lam_ctx* c, const Part& p, int slot) {
+  uint8_t* m = p.base + p.meta_base + (uint64_t)slot * p.meta_stride;
+  ChunkMeta cm;
+  cm.flags = reinterpret_cast<uint64_t*>(m + c->sm.flags);
+  cm.hdr = reinterpret_cast<lam_chunk_header*>(m + c->sm.hdr);
+  cm.cnt = reinterpret_cast<uint32_t*>(m + c->sm.cnt);
+  cm.abort_flag = reinterpret_cast<int32_t*>(m + c->sm.abort);
+  return cm;
+}
+
+uint8_t* slot_data(const Part& p, int slot) { return p.base + (uint64_t)slot * p.slot_stride; }
+
+int find_slot(const ShmNode& n, int S, uint64_t v, int32_t state) {
+  for (int i = 0; i < S; ++i)
+    if (n.slot[i].version == v && n.slot[i].state == state) return i;
+  return -1;
+}
+
+int acquire_slot(const ShmNode& n, int S) {
+  for (int i = 0; i < S; ++i)
+    if (n.slot[i].state == S_FREE && n.slot[i].readers == 0) return i;
+  for (int i = 0; i < S; ++i)
+    if (n.slot[i].state == S_COMPLETE && n.slot[i].readers == 0 && n.slot[i].version != n.latest) return i;
+  return -1;
+}
+
+uint64_t newest_held(const ShmNode& n, int S, int* slot) {
+  uint64_t best = 0;
+  *slot = -1;
+  for (int i = 0; i < S; ++i)
+    if ((n.slot[i].state == S_FILLING || n.slot[i].state == S_COMPLETE) && n.slot[i].version > best) {
+      best = n.slot[i].version;
+      *slot = i;
+    }
+  return best;
+}
+
+lam_status validate(const lam_config& c, std::string* why) {
+  auto bad = [&](const std::string& s) { *why = s; return LAM_EINVAL; };
+  if (!model_valid(c.model)) return bad("model dims");
+  if (c.actor_layout != LAM_FSDP2_DIM0 && c.actor_layout != LAM_FSDP1_FLAT) return bad("actor_layout");
+  if (c.fsdp_size < 1 || c.fsdp_size > LAM_MAX_RANKS) return bad("fsdp_size");
+  if (c.n_relays < 0 || c.n_relays > LAM_MAX_NODES) return bad("n_relays");
+  if (c.slots < 2 || c.slots > LAM_MAX_SLOTS) return bad("slots");
+  if (c.chunk_bytes % kChunkAlign) return bad("chunk_bytes must be a multiple of 4096");
+  if (c.n_procs < 1 || c.proc_rank < 0 || c.proc_rank >= c.n_procs) return bad("proc_rank/n_procs");
+  auto dev_ok = [&](int d) { return d >= 0 && d < LAM_MAX_DEVICES && c.proc_of_device[d] >= 0 && c.proc_of_device[d] < c.n_procs; };
+  for (int r = 0; r < c.fsdp_size; ++r)
+    if (!dev_ok(c.actor_device[r])) return bad("actor_device[" + std::to_string(r) + "]");
+  for (int i = 0; i < c.n_relays; ++i)
+    for (int r = 0; r < c.fsdp_size; ++r)
+      if (!dev_ok(c.relay[i].part_device[r])) return bad("relay part_device");
+  if (c.n_rollouts < 0 || c.n_rollouts > LAM_MAX_ROLLOUTS) return bad("n_rollouts");
+  for (int i = 0; i < c.n_rollouts; ++i)
+    if (c.rollout[i].node < 0 || c.rollout[i].node > c.n_relays || !dev_ok(c.rollout[i].device))
+      return bad("rollout " + std::to_string(i));
+  if (c.n_procs > 1 && c.shm_name[0] == 0) return bad("shm_name required with n_procs > 1");
+  return LAM_OK;
+}
+
+lam_status setup_shm(lam_ctx* c) {
+  if (c->cfg.n_procs == 1) {
+    c->shm = new Shm();
+    memset(c->shm, 0, sizeof(Shm));
+    pthread_mutexattr_t a;
+    pthread_mutexattr_init(&a);
+    pthread_mutexattr_settype(&a, PTHREAD_MUTEX_RECURSIVE);
+    pthread_mutex_init(&c->shm->mu, &a);
+    c->shm->magic = kMagic;
+    return LAM_OK;
+  }
+  char name[80];
+  snprintf(name, sizeof name, "/%s", c->cfg.shm_name);
+  int fd = -1;
+  if (c->cfg.proc_rank == 0) {
+    shm_unlink(name);
+    fd = shm_open(name, O_CREAT | O_EXCL | O_RDWR, 0600);
+    if (fd < 0 || ftruncate(fd, sizeof(Shm)) != 0) return LAM_EIPC;
+    c->shm_owner = true;
+  } else {
+    for (int i = 0; i < 6000 && fd < 0; ++i) {
+      fd = shm_open(name, O_RDWR, 0600);
+      if (fd < 0) usleep(10000);
+    }
+    if (fd < 0) return LAM_EIPC;
+    struct stat st;
+    for (int i = 0; i < 6000; ++i) {
+      if (fstat(fd, &st) == 0 && (size_t)st.st_size >= sizeof(Shm)) break;
+      usleep(10000);
+    }
+  }
+  void* p = mmap(nullptr, sizeof(Shm), PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+  close(fd);
+  if (p == MAP_FAILED) return LAM_EIPC;
+  c->shm = reinterpret_cast<Shm*>(p);
+  c->shm_mapped = true;
+  if (c->cfg.proc_rank == 0) {
+    pthread_mutexattr_t a;
+    pthread_mutexattr_init(&a);
+    pthread_mutexattr_setpshared(&a, PTHREAD_PROCESS_SHARED);
+    pthread_mutexattr_setrobust(&a, PTHREAD_MUTEX_ROBUST);
+    pthread_mutexattr_settype(&a, PTHREAD_MUTEX_RECURSIVE);
+    pthread_mutex_init(&c->shm->mu, &a);
+    __atomic_store_n(&c->shm->magic, kMagic, __ATOMIC_RELEASE);
+  } else {
+    for (int i = 0; i < 6000 && __atomic_load_n(&c->shm->magic, __ATOMIC_ACQUIRE) != kMagic; ++i) usleep(10000);
+    if (__atomic_load_n(&c->shm->magic, __ATOMIC_ACQUIRE) != kMagic) return LAM_EIPC;
+  }
+  return LAM_OK;
+}
+
+lam_status alloc_parts(lam_ctx* c) {
+  const int N = c->cfg.fsdp_size, S = c->S;
+  const uint64_t total = c->plan.total_chunks;
+  c->sm.flags = 0;
+  c->sm.hdr = align_up(c->sm.flags + 8 * total, 64);
+  c->sm.cnt = align_up(c->sm.hdr + sizeof(lam_chunk_header) * total, 64);
+  c->sm.abort = align_up(c->sm.cnt + 4 * total, 64);
+  c->sm.bytes = align_up(c->sm.abort + 64, 4096);
+  c->node_parts.assign(c->n_nodes, {});
+  c->node_rank_part.assign(c->n_nodes, std::vector<int>(N, -1));
+  for (int node = 0; node < c->n_nodes; ++node) {
+    std::map<int, int> by_dev;
+    for (int r = 0; r < N; ++r) {
+      int d = node_part_device(c, node, r);
+      auto it = by_dev.find(d);
+      if (it == by_dev.end()) {
+        Part p;
+        p.node = node;
+        p.device = d;
+        p.index = (int)c->parts.size();
+        p.pos = (int)c->node_parts[node].size();
+        p.rank_off.assign(N, -1);
+        p.local = owns(c, d);
+        by_dev[d] = p.index;
+        c->node_parts[node].push_back(p.index);
+        c->parts.push_back(p);
+        it = by_dev.find(d);
+      }
+      Part& p = c->parts[it->second];
+      p.rank_off[r] = (int64_t)p.slot_data;
+      p.slot_data += c->plan.n_chunks[r] * c->plan.C;
+      p.ranks.push_back(r);
+      c->node_rank_part[node][r] = it->second;
+    }
+  }
+  for (Part& p : c->parts) {
+    p.slot_stride = align_up(std::max<uint64_t>(p.slot_data, 1), kSlotAlign);
+    p.meta_base = p.slot_stride * S;
+    p.meta_stride = c->sm.bytes;
+    p.alloc_bytes = p.meta_base + p.meta_stride * S;
+    if (!p.local) continue;
+    CK(cudaSetDevice(p.device));
+    if (cudaMalloc(&p.base, p.alloc_bytes) != cudaSuccess) {
+      fprintf(stderr, "liblam: cudaMalloc(%.2f GB) failed on device %d\n", p.alloc_bytes / 1e9, p.device);
+      return LAM_ENOMEM;
+    }
+    CK(cudaMemset(p.base, 0, p.alloc_bytes));
+    int lo = 0, hi = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CK(cudaStreamCreateWithPriority(&p.stream, cudaStreamNonBlocking, lo));  // lowest priority: SM-light
+    for (int s = 0; s < S; ++s) CK(cudaEventCreateWithFlags(&p.done_ev[s], cudaEventDisableTiming));
+    CK(cudaHostAlloc(&p.err_host, sizeof(uint32_t) * LAM_MAX_SLOTS, cudaHostAllocMapped | cudaHostAllocPortable));
+    memset(p.err_host, 0, sizeof(uint32_t) * LAM_MAX_SLOTS);
+    CK(cudaHostGetDevicePointer((void**)&p.err_dev, p.err_host, 0));
+    if (!c->dev.count(p.device)) {
+      DevLocal dl;
+      std::vector<uint64_t> len(total);
+      for (uint64_t g = 0; g < total; ++g) len[g] = c->plan.chunk_len(g);
+      CK(cudaMalloc(&dl.d_chunk_len, 8 * std::max<uint64_t>(total, 1)));
+      if (total) CK(cudaMemcpy(dl.d_chunk_len, len.data(), 8 * total, cudaMemcpyHostToDevice));
+      CK(cudaStreamCreateWithPriority(&dl.side, cudaStreamNonBlocking, lo));
+      c->dev[p.device] = dl;
+    }
+    if (p.node > 0) {
+      std::vector<HopTile> tiles;
+      std::vector<uint32_t> tpc;
+      build_hop_tiles(c->plan, p.ranks, &tiles, &tpc);
+      p.n_tiles = (uint32_t)tiles.size();
+      CK(cudaMalloc(&p.d_tiles, sizeof(HopTile) * std::max<size_t>(tiles.size(), 1)));
+      if (!tiles.empty()) CK(cudaMemcpy(p.d_tiles, tiles.data(), sizeof(HopTile) * tiles.size(), cudaMemcpyHostToDevice));
+      CK(cudaMalloc(&p.d_tiles_per_chunk, 4 * std::max<uint64_t>(total, 1)));
+      if (total) CK(cudaMemcpy(p.d_tiles_per_chunk, tpc.data(), 4 * total, cudaMemcpyHostToDevice));
+    }
+  }
+  return LAM_OK;
+}
+
+lam_status connect_links(lam_ctx* c) {
+  const int N = c->cfg.fsdp_size, S = c->S;
+  // single process: enable peer access among every pair of used devices
+  if (c->cfg.n_procs == 1) {
+    std::set<int> devs;
+    for (auto& p : c->parts) devs.insert(p.device);
+    for (int i = 0; i < c->cfg.n_rollouts; ++i) devs.insert(c->cfg.rollout[i].device);
+    for (int a : devs)
+      for (int b : devs) {
+        if (a == b) continue;
+        int can = 0;
+        cudaDeviceCanAccessPeer(&can, a, b);
+        if (!can) continue;
+        cudaSetDevice(a);
+        cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return LAM_ECUDA;
+        cudaGetLastError();
+      }
+  }
+  for (auto& p : c->parts)
+    if (!p.base) {
+      fprintf(stderr, "liblam: part of node %d on device %d not mapped (missing lam_import_ipc?)\n", p.node, p.device);
+      return LAM_EIPC;
+    }
+  // hop link tables: [my slot][pred slot][rank]
+  for (Part& p : c->parts) {
+    if (!p.local || p.node == 0) continue;
+    std::vector<RankLink> links((size_t)S * S * N);
+    for (int s = 0; s < S; ++s)
+      for (int ps = 0; ps < S; ++ps)
+        for (int r : p.ranks) {
+          const Part& q = c->parts[c->node_rank_part[p.node - 1][r]];
+          ChunkMeta qm = meta_of(c, q, ps);
+          RankLink& L = links[((size_t)s * S + ps) * N + r];
+          L.src = slot_data(q, ps) + q.rank_off[r];
+          L.src_flags = qm.flags;
+          L.src_hdr = qm.hdr;
+          L.dst = slot_data(p, s) + p.rank_off[r];
+        }
+    CK(cudaSetDevice(p.device));
+    CK(cudaMalloc(&p.d_links, sizeof(RankLink) * links.size()));
+    CK(cudaMemcpy(p.d_links, links.data(), sizeof(RankLink) * links.size(), cudaMemcpyHostToDevice));
+  }
+  // pull source tables: per (node, slot, rollout device)
+  std::set<std::pair<int, int>> need;
+  for (int i = 0; i < c->cfg.n_rollouts; ++i)
+    if (owns(c, c->cfg.rollout[i].device)) need.insert({c->cfg.rollout[i].node, c->cfg.rollout[i].device});
+  for (auto nd : need) {
+    for (int s = 0; s < S; ++s) {
+      std::vector<const uint8_t*> base(N);
+      for (int r = 0; r < N; ++r) {
+        const Part& q = c->parts[c->node_rank_part[nd.first][r]];
+        base[r] = slot_data(q, s) + q.rank_off[r];
+      }
+      CK(cudaSetDevice(nd.second));
+      const uint8_t** d = nullptr;
+      CK(cudaMalloc(&d, sizeof(void*) * N));
+      CK(cudaMemcpy(d, base.data(), sizeof(void*) * N, cudaMemcpyHostToDevice));
+      c->d_rank_base[{nd.first * LAM_MAX_SLOTS + s, nd.second}] = d;
+    }
+  }
+  c->connected = true;
+  return LAM_OK;
+}
+
+// ----------------------------------------------------------------------------- progress engine
+// Launch the hop kernel of local part p (node >= 1) for FILLING slot s.  Returns true if launched.
+lam_status launch_hop_part(lam_ctx* c, Part& p, int s, bool* launched) {
+  *launched = false;
+  ShmNode& n = c->shm->node[p.node];
+  ShmSlot& sl = n.slot[s];
+  const int ps = sl.src_slot;
+  const uint64_t u = sl.version;
+  CK(cudaSetDevice(p.device));
+  // predecessor parts on the same GPU must have finished (never spin on a kernel of the same GPU)
+  std::set<int> waits;
+  for (int r : p.ranks) {
+    int qi = c->node_rank_part[p.node - 1][r];
+    const Part& q = c->parts[qi];
+    if (q.device != p.device) continue;
+    if (!q.local) return LAM_EINVAL;  // one process per GPU: cannot happen
+    if (p.node - 1 == 0) {
+      if (!(c->shm->node[0].slot[ps].launched_mask >> r & 1ull)) return LAM_OK;  // not yet published
+      if (c->pubs[r].inflight_version[ps] == u) CK(cudaStreamWaitEvent(p.stream, c->pubs[r].ev[ps], 0));
+    } else {
+      waits.insert(qi);
+    }
+  }
+  for (int qi : waits) {
+    const Part& q = c->parts[qi];
+    const ShmSlot& qs = c->shm->node[q.node].slot[ps];
+    if (qs.state == S_FILLING && !(qs.launched_mask >> q.pos & 1ull)) return LAM_OK;  // wait
+    if (q.inflight_version[ps] == u) CK(cudaStreamWaitEvent(p.stream, q.done_ev[ps], 0));
+  }
+  ChunkMeta m = meta_of(c, p, s);
+  CK(cudaMemsetAsync((uint8_t*)m.hdr, 0, c->sm.abort + 64 - c->sm.hdr, p.stream));  // hdr, cnt, abort
+  p.err_host[s] = 0;
+  const RankLink* links = p.d_links + (size_t)(s * c->S + ps) * c->cfg.fsdp_size;
+  cudaEvent_t t0 = prof_begin(c, p.device, p.stream);
+  int rc = launch_hop(p.d_tiles, p.n_tiles, links, m, p.d_tiles_per_chunk, u, p.err_dev + s, c->timeout_ns,
+                      c->hop_ctas, p.stream);
+  if (rc) {
+    fprintf(stderr, "liblam: hop launch failed: %s\n", cudaGetErrorString((cudaError_t)rc));
+    return LAM_ECUDA;
+  }
+  prof_end(c, 1, p.device, p.stream, t0);
+  CK(cudaEventRecord(p.done_ev[s], p.stream));
+  p.inflight_version[s] = u;
+  sl.launched_mask |= 1ull << p.pos;
+  c->shm->stats.hops_launched++;
+  *launched = true;
+  return LAM_OK;
+}
+
+lam_status step_locked(lam_ctx* c, int* transitions, bool* busy) {
+  Shm* sh = c->shm;
+  const int S = c->S;
+  lam_status first_err = LAM_OK;
+  *busy = false;
+  // (1) completions of local packs (node 0)
+  for (int r = 0; r < c->cfg.fsdp_size; ++r) {
+    if (!owns(c, c->cfg.actor_device[r])) continue;
+    RankPub& rp = c->pubs[r];
+    for (int s = 0; s < S; ++s) {
+      if (!rp.inflight_version[s]) continue;
+      cudaError_t q = cudaEventQuery(rp.ev[s]);
+      if (q == cudaErrorNotReady) { *busy = true; continue; }
+      if (q != cudaSuccess) return LAM_ECUDA;
+      ShmSlot& sl = sh->node[0].slot[s];
+      if (sl.version == rp.inflight_version[s] && sl.state == S_FILLING) {
+        sl.parts_done++;
+        if (sl.parts_done == c->cfg.fsdp_size) {
+          sl.state = S_COMPLETE;
+          if (sl.version > sh->node[0].latest) sh->node[0].latest = sl.version;
+        }
+        (*transitions)++;
+      }
+      rp.inflight_version[s] = 0;
+    }
+  }
+  // (2) completions of local hop kernels
+  for (Part& p : c->parts) {
+    if (!p.local || p.node == 0) continue;
+    for (int s = 0; s < S; ++s) {
+      if (!p.inflight_version[s]) continue;
+      cudaError_t q = cudaEventQuery(p.done_ev[s]);
+      if (q == cudaErrorNotReady) { *busy = true; continue; }
+      if (q != cudaSuccess) return LAM_ECUDA;
+      ShmNode& n = sh->node[p.node];
+      ShmSlot& sl = n.slot[s];
+      uint32_t err = p.err_host[s];
+      if (sl.version == p.inflight_version[s] && sl.state == S_FILLING) {
+        sl.parts_finished++;
+        if (err) {
+          lam_status e = -(lam_status)err;
+          if (!sl.err) sl.err = e;
+          if (e == LAM_ETIMEOUT) sh->stats.timeouts++; else sh->stats.checksum_errors++;
+          if (first_err == LAM_OK) first_err = e;
+        } else {
+          sl.parts_done++;
+        }
+        const int np = (int)c->node_parts[p.node].size();
+        if (sl.parts_finished == np) {
+          ShmSlot& src = sh->node[p.node - 1].slot[sl.src_slot];
+          if (src.readers > 0) src.readers--;
+          if (sl.err == 0) {
+            sl.state = S_COMPLETE;
+            if (sl.version > n.latest) n.latest = sl.version;
+          } else {
+            sl.state = S_FREE;  // never committed: keep serving the previous version
+            sl.version = 0;
+          }
+          sl.src_slot = -1;
+        }
+        (*transitions)++;
+      }
+      p.inflight_version[s] = 0;
+    }
+  }
+  // (3) pull pins
+  for (size_t i = 0; i < c->pending.size();) {
+    cudaError_t q = cudaEventQuery(c->pending[i].ev);
+    if (q == cudaErrorNotReady) { *busy = true; ++i; continue; }
+    if (q != cudaSuccess) return LAM_ECUDA;
+    ShmSlot& sl = sh->node[c->pending[i].node].slot[c->pending[i].slot];
+    if (sl.readers > 0) sl.readers--;
+    c->ev_pool[c->pending[i].device].push_back(c->pending[i].ev);
+    c->pending[i] = c->pending.back();
+    c->pending.pop_back();
+    (*transitions)++;
+  }
+  // (4) start new versions (latest-wins) and launch local parts
+  for (int node = 1; node < c->n_nodes; ++node) {
+    ShmNode& n = sh->node[node];
+    ShmNode& pred = sh->node[node - 1];
+    int fill = -1;
+    for (int s = 0; s < S; ++s)
+      if (n.slot[s].state == S_FILLING) fill = s;
+    if (fill < 0) {
+      int ps = -1;
+      uint64_t u = newest_held(pred, S, &ps);
+      if (u > n.started) {
+        int s = acquire_slot(n, S);
+        if (s >= 0) {
+          if (n.started && u > n.started + 1) {
+            n.skipped += u - n.started - 1;
+            sh->stats.versions_skipped += u - n.started - 1;
+          }
+          ShmSlot& sl = n.slot[s];
+          sl.version = u;
+          sl.state = S_FILLING;
+          sl.readers = 0;
+          sl.parts_done = sl.parts_finished = 0;
+          sl.err = 0;
+          sl.src_slot = ps;
+          sl.launched_mask = 0;
+          pred.slot[ps].readers++;
+          n.started = u;
+          fill = s;
+          (*transitions)++;
+        }
+      }
+    }
+    if (fill >= 0) {
+      for (int pi : c->node_parts[node]) {
+        Part& p = c->parts[pi];
+        if (!p.local || (n.slot[fill].launched_mask >> p.pos & 1ull)) continue;
+        bool launched = false;
+        lam_status st = launch_hop_part(c, p, fill, &launched);
+        if (st != LAM_OK) return st;
+        if (launched) (*transitions)++;
+      }
+    }
+  }
+  // (5) anything still moving anywhere?
+  for (int node = 0; node < c->n_nodes && !*busy; ++node) {
+    for (int s = 0; s < S; ++s)
+      if (sh->node[node].slot[s].state == S_FILLING) *busy = true;
+    if (node > 0) {
+      int ps;
+      if (newest_held(sh->node[node - 1], S, &ps) > sh->node[node].started) *busy = true;
+    }
+  }
+  return first_err;
+}
+
+std::string layout_key(int node, const lam_tp_layout& L) {
+  std::string k = std::to_string(node) + ":" + std::to_string(L.tp_size) + ":" + std::to_string(L.tp_rank);
+  for (int i = 0; i < L.n_dsts; ++i) {
+    const lam_dst& d = L.dsts[i];
+    char b[96];
+    snprintf(b, sizeof b, "|%p,%lld,%d", d.dst, (long long)d.dst_row_pitch_bytes, d.transpose);
+    k += b;
+    for (int j = 0; j < d.n_parts; ++j) k += "," + std::to_string(d.parts[j].tensor_id) + "/" + std::to_string(d.parts[j].rule);
+  }
+  return k;
+}
+
+}  // namespace
+
+// ===================================================================================== C ABI
+extern "C" const char* lam_strerror(lam_status s) {
+  switch (s) {
+    case LAM_OK: return "ok";
+    case LAM_ENOVERSION: return "no complete version yet";
+    case LAM_IDLE: return "idle";
+    case LAM_EINVAL: return "invalid argument";
+    case LAM_ESTALE: return "version not newer than the last published";
+    case LAM_ECUDA: return "CUDA error";
+    case LAM_ECHECKSUM: return "chunk checksum mismatch (version not committed)";
+    case LAM_ENOMEM: return "out of memory";
+    case LAM_ESHUTDOWN: return "shutting down";
+    case LAM_EBUSY: return "publish slots busy";
+    case LAM_ETIMEOUT: return "chain hop timed out waiting for its predecessor";
+    case LAM_EIPC: return "shared memory / IPC setup failed";
+    default: return "unknown status";
+  }
+}
+
+extern "C" lam_status lam_init(const lam_config* cfg, lam_ctx** out) {
+  if (!cfg || !out) return LAM_EINVAL;
+  *out = nullptr;
+  std::string why;
+  lam_status st = validate(*cfg, &why);
+  if (st != LAM_OK) {
+    fprintf(stderr, "liblam: invalid config: %s\n", why.c_str());
+    return st;
+  }
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    fprintf(stderr, "liblam: no CUDA device (this library has no CPU fallback)\n");
+    return LAM_ECUDA;
+  }
+  auto c = std::make_unique<lam_ctx>();
+  c->cfg = *cfg;
+  c->S = cfg->slots;
+  c->n_nodes = cfg->n_relays + 1;
+  c->ts = model_tensors(cfg->model);
+  for (auto& t : c->ts) c->params += t.numel();
+  uint64_t C = cfg->chunk_bytes;
+  if (C == 0) {
+    double tb = cfg->t_byte_s > 0 ? cfg->t_byte_s : 1.0 / 750e9;
+    double tsu = cfg->t_start_s > 0 ? cfg->t_start_s : 5e-6;
+    // the pack is one more pipeline stage ahead of the chain (reading R12)
+    int64_t k = lam_optimal_chunks(c->n_nodes + 1, 2.0 * (double)c->params, tb, tsu, 1024);
+    C = align_up(cdiv(2 * c->params, (uint64_t)k), kChunkAlign);
+    // practical cap: the chunk is also the checksum / completion-signal unit
+    C = std::min<uint64_t>(C, 256ull << 20);
+  }
+  if (!build_image_plan(c->ts, cfg->fsdp_size, cfg->actor_layout, C, &c->plan)) return LAM_EINVAL;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  c->pack_ctas = cfg->pack_ctas > 0 ? cfg->pack_ctas : sms * 6;
+  c->hop_ctas = cfg->hop_ctas > 0 ? cfg->hop_ctas : 48;
+  c->pull_ctas = cfg->pull_ctas > 0 ? cfg->pull_ctas : sms * 4;
+  if (cfg->spin_timeout_s > 0) c->timeout_ns = (uint64_t)(cfg->spin_timeout_s * 1e9);
+  c->pubs.resize(cfg->fsdp_size);
+  st = setup_shm(c.get());
+  if (st != LAM_OK) return st;
+  st = alloc_parts(c.get());
+  if (st != LAM_OK) {
+    lam_destroy(c.release());
+    return st;
+  }
+  for (int r = 0; r < cfg->fsdp_size; ++r) {
+    if (!owns(c.get(), cfg->actor_device[r])) continue;
+    cudaSetDevice(cfg->actor_device[r]);
+    for (int s = 0; s < c->S; ++s) cudaEventCreateWithFlags(&c->pubs[r].ev[s], cudaEventDisableTiming);
+  }
+  if (cfg->n_procs == 1) {
+    st = connect_links(c.get());
+    if (st != LAM_OK) {
+      lam_destroy(c.release());
+      return st;
+    }
+  }
+  *out = c.release();
+  return LAM_OK;
+}
+
+struct IpcEntry {
+  int32_t part, device;
+  cudaIpcMemHandle_t h;
+};
+
+extern "C" lam_status lam_export_ipc(lam_ctx* c, void* buf, size_t cap, size_t* len) {
+  if (!c || !len) return LAM_EINVAL;
+  std::vector<IpcEntry> v;
+  for (Part& p : c->parts)
+    if (p.local) {
+      IpcEntry e{p.index, p.device, {}};
+      cudaSetDevice(p.device);
+      CK(cudaIpcGetMemHandle(&e.h, p.base));
+      v.push_back(e);
+    }
+  size_t need = sizeof(int32_t) + v.size() * sizeof(IpcEntry);
+  *len = need;
+  if (!buf || cap < need) return buf ? LAM_EINVAL : LAM_OK;
+  int32_t n = (int32_t)v.size();
+  memcpy(buf, &n, sizeof n);
+  if (!v.empty()) memcpy((char*)buf + sizeof n, v.data(), v.size() * sizeof(IpcEntry));
+  return LAM_OK;
+}
+
+extern "C" lam_status lam_import_ipc(lam_ctx* c, int32_t proc, const void* buf, size_t len) {
+  if (!c || !buf || len < sizeof(int32_t)) return LAM_EINVAL;
+  if (proc == c->cfg.proc_rank) return LAM_OK;
+  int32_t n = 0;
+  memcpy(&n, buf, sizeof n);
+  if (len < sizeof n + (size_t)n * sizeof(IpcEntry)) return LAM_EINVAL;
+  int my_dev = -1;
+  for (int d = 0; d < LAM_MAX_DEVICES; ++d)
+    if (owns(c, d)) { my_dev = d; break; }
+  if (my_dev < 0) return LAM_OK;  // this process owns no GPU work
+  CK(cudaSetDevice(my_dev));
+  for (int i = 0; i < n; ++i) {
+    IpcEntry e;
+    memcpy(&e, (const char*)buf + sizeof n + (size_t)i * sizeof(IpcEntry), sizeof e);
+    if (e.part < 0 || e.part >= (int)c->parts.size()) return LAM_EINVAL;
+    Part& p = c->parts[e.part];
+    if (p.local || p.base) continue;
+    void* ptr = nullptr;
+    cudaError_t err = cudaIpcOpenMemHandle(&ptr, e.h, cudaIpcMemLazyEnablePeerAccess);
+    if (err != cudaSuccess) {
+      fprintf(stderr, "liblam: cudaIpcOpenMemHandle(part %d, dev %d): %s\n", e.part, e.device, cudaGetErrorString(err));
+      return LAM_EIPC;
+    }
+    p.base = (uint8_t*)ptr;
+    p.ipc_opened = true;
+  }
+  return LAM_OK;
+}
+
+extern "C" lam_status lam_connect(lam_ctx* c) {
+  if (!c) return LAM_EINVAL;
+  if (c->connected) return LAM_OK;
+  Lock l(c->shm);
+  return connect_links(c);
+}
+
+extern "C" lam_status lam_publish(lam_ctx* c, uint64_t v, int32_t rank, const lam_shard* shards, int32_t n,
+                                  void* actor_stream, void* reads_done) {
+  if (!c || !c->connected || rank < 0 || rank >= c->cfg.fsdp_size || n < 0 || (n && !shards) || v == 0)
+    return LAM_EINVAL;
+  if (!owns(c, c->cfg.actor_device[rank])) return LAM_EINVAL;
+  const int dev = c->cfg.actor_device[rank];
+  RankPub& rp = c->pubs[rank];
+  Part& p = c->parts[c->node_rank_part[0][rank]];
+  CK(cudaSetDevice(dev));
+  // (re)build the pack units when the shard list changed (outside the lock: host-only work)
+  std::vector<lam_shard> key(shards, shards + n);
+  bool same = key.size() == rp.key.size() &&
+              (key.empty() || memcmp(key.data(), rp.key.data(), sizeof(lam_shard) * key.size()) == 0);
+  if (!same) {
+    std::vector<PackUnit> units;
+    std::vector<uint32_t> upc;
+    std::string err;
+    if (!build_pack_units(c->plan, c->ts, rank, key, (uint64_t)p.rank_off[rank], &units, &upc, &err)) {
+      fprintf(stderr, "liblam: lam_publish: %s\n", err.c_str());
+      return LAM_EINVAL;
+    }
+    CK(cudaStreamSynchronize(c->dev[dev].side));  // tables may be in use by an earlier pack
+    if (units.size() > rp.cap_units) {
+      if (rp.d_units) cudaFree(rp.d_units);
+      CK(cudaMalloc(&rp.d_units, sizeof(PackUnit) * units.size()));
+      rp.cap_units = (uint32_t)units.size();
+    }
+    if (!units.empty()) CK(cudaMemcpy(rp.d_units, units.data(), sizeof(PackUnit) * units.size(), cudaMemcpyHostToDevice));
+    rp.n_units = (uint32_t)units.size();
+    if (!rp.d_units_per_chunk) CK(cudaMalloc(&rp.d_units_per_chunk, 4 * std::max<uint64_t>(c->plan.total_chunks, 1)));
+    if (c->plan.total_chunks) CK(cudaMemcpy(rp.d_units_per_chunk, upc.data(), 4 * c->plan.total_chunks, cudaMemcpyHostToDevice));
+    if ((uint32_t)n > rp.cap_ptrs) {
+      if (rp.d_ptrs) cudaFree(rp.d_ptrs);
+      CK(cudaMalloc((void**)&rp.d_ptrs, sizeof(float*) * std::max(n, 1)));
+      rp.cap_ptrs = (uint32_t)std::max(n, 1);
+    }
+    std::vector<const float*> ptrs(n);
+    for (int i = 0; i < n; ++i) ptrs[i] = shards[i].ptr;
+    if (n) CK(cudaMemcpy((void*)rp.d_ptrs, ptrs.data(), sizeof(float*) * n, cudaMemcpyHostToDevice));
+    rp.key = key;
+  }
+  Lock l(c->shm);
+  Shm* sh = c->shm;
+  ShmNode& n0 = sh->node[0];
+  int s = -1;
+  if (v < sh->last_published) return LAM_ESTALE;
+  if (v == sh->last_published) {
+    s = find_slot(n0, c->S, v, S_FILLING);
+    if (s < 0 || (n0.slot[s].launched_mask >> rank & 1ull)) return LAM_ESTALE;
+  } else {
+    for (int i = 0; i < c->S; ++i)  // previous version still waiting for some ranks: refuse
+      if (n0.slot[i].state == S_FILLING &&
+          n0.slot[i].launched_mask != ((c->cfg.fsdp_size == 64) ? ~0ull : ((1ull << c->cfg.fsdp_size) - 1)))
+        return LAM_EBUSY;
+    s = acquire_slot(n0, c->S);
+    if (s < 0) {
+      sh->stats.publish_busy++;
+      return LAM_EBUSY;
+    }
+    ShmSlot& sl = n0.slot[s];
+    sl.version = v;
+    sl.state = S_FILLING;
+    sl.readers = 0;
+    sl.parts_done = sl.parts_finished = 0;
+    sl.err = 0;
+    sl.src_slot = -1;
+    sl.launched_mask = 0;
+    sh->last_published = v;
+    n0.started = v;
+    sh->stats.publishes++;
+  }
+  n0.slot[s].launched_mask |= 1ull << rank;
+  // enqueue: side stream waits for the work already on the actor stream, then packs
+  cudaStream_t side = c->dev[dev].side;
+  cudaEvent_t fork = get_event(c, dev);
+  CK(cudaEventRecord(fork, (cudaStream_t)actor_stream));
+  CK(cudaStreamWaitEvent(side, fork, 0));
+  c->ev_pool[dev].push_back(fork);  // reuse is safe: a later record only affects later waits
+  ChunkMeta m = meta_of(c, p, s);
+  const uint64_t g0 = c->plan.chunk_base[rank], ng = c->plan.n_chunks[rank];
+  if (ng) {
+    CK(cudaMemsetAsync(m.hdr + g0, 0, sizeof(lam_chunk_header) * ng, side));
+    CK(cudaMemsetAsync(m.cnt + g0, 0, 4 * ng, side));
+  }
+  cudaEvent_t t0 = prof_begin(c, dev, side);
+  int rc = launch_pack(rp.d_units, rp.n_units, rp.d_ptrs, slot_data(p, s), m, rp.d_units_per_chunk, v,
+                       c->plan.total_chunks, c->dev[dev].d_chunk_len, c->pack_ctas, side);
+  if (rc) {
+    fprintf(stderr, "liblam: pack launch failed: %s\n", cudaGetErrorString((cudaError_t)rc));
+    return LAM_ECUDA;
+  }
+  prof_end(c, 0, dev, side, t0);
+  if (reads_done) CK(cudaEventRecord((cudaEvent_t)reads_done, side));
+  CK(cudaEventRecord(rp.ev[s], side));
+  rp.inflight_version[s] = v;
+  return LAM_OK;
+}
+
+extern "C" lam_status lam_relay_step(lam_ctx* c, int32_t* n_transitions) {
+  if (!c || !c->connected) return LAM_EINVAL;
+  Lock l(c->shm);
+  int t = 0;
+  bool busy = false;
+  lam_status st = step_locked(c, &t, &busy);
+  if (n_transitions) *n_transitions = t;
+  if (st != LAM_OK) return st;
+  return busy ? LAM_OK : LAM_IDLE;
+}
+
+extern "C" lam_status lam_pull(lam_ctx* c, int32_t rid, const lam_tp_layout* L, void* stream, uint64_t* vout) {
+  if (vout) *vout = 0;
+  if (!c || !c->connected || !L || rid < 0 || rid >= c->cfg.n_rollouts) return LAM_EINVAL;
+  const lam_rollout_desc ro = c->cfg.rollout[rid];
+  if (!owns(c, ro.device)) return LAM_EINVAL;
+  CK(cudaSetDevice(ro.device));
+  std::string key = layout_key(ro.node, *L);
+  Lock l(c->shm);
+  auto it = c->plans.find(key);
+  if (it == c->plans.end()) {
+    std::vector<CopyTile> tiles;
+    uint64_t bytes = 0;
+    std::string err;
+    if (!build_copy_tiles(c->plan, c->ts, *L, &tiles, &bytes, &err)) {
+      fprintf(stderr, "liblam: lam_pull: %s\n", err.c_str());
+      return LAM_EINVAL;
+    }
+    PullPlan pp;
+    pp.n_tiles = (uint32_t)tiles.size();
+    pp.bytes = bytes;
+    CK(cudaMalloc(&pp.d_tiles, sizeof(CopyTile) * std::max<size_t>(tiles.size(), 1)));
+    if (!tiles.empty()) CK(cudaMemcpy(pp.d_tiles, tiles.data(), sizeof(CopyTile) * tiles.size(), cudaMemcpyHostToDevice));
+    it = c->plans.emplace(key, pp).first;
+    c->shm->stats.plan_cache_misses++;
+  } else {
+    c->shm->stats.plan_cache_hits++;
+  }
+  ShmNode& n = c->shm->node[ro.node];
+  const uint64_t u = n.latest;
+  if (u == 0) return LAM_ENOVERSION;
+  const int s = find_slot(n, c->S, u, S_COMPLETE);
+  if (s < 0) return LAM_ECUDA;  // invariant broken
+  n.slot[s].readers++;
+  auto rb = c->d_rank_base.find({ro.node * LAM_MAX_SLOTS + s, ro.device});
+  if (rb == c->d_rank_base.end()) return LAM_EINVAL;
+  cudaEvent_t t0 = prof_begin(c, ro.device, (cudaStream_t)stream);
+  int rc = launch_pull(it->second.d_tiles, it->second.n_tiles, rb->second, c->pull_ctas, stream);
+  if (rc) {
+    n.slot[s].readers--;
+    fprintf(stderr, "liblam: pull launch failed: %s\n", cudaGetErrorString((cudaError_t)rc));
+    return LAM_ECUDA;
+  }
+  prof_end(c, 2, ro.device, (cudaStream_t)stream, t0);
+  cudaEvent_t ev = get_event(c, ro.device);
+  CK(cudaEventRecord(ev, (cudaStream_t)stream));
+  c->pending.push_back({ev, ro.node, s, ro.device});
+  c->shm->stats.pulls++;
+  if (vout) *vout = u;
+  return LAM_OK;
+}
+
+extern "C" lam_status lam_latest(lam_ctx* c, int32_t node, uint64_t* vout) {
+  if (!c || !vout || node < 0 || node >= c->n_nodes) return LAM_EINVAL;
+  Lock l(c->shm);
+  *vout = c->shm->node[node].latest;
+  return *vout ? LAM_OK : LAM_ENOVERSION;
+}
+
+extern "C" lam_status lam_get_plan_info(lam_ctx* c, lam_plan_info* o) {
+  if (!c || !o) return LAM_EINVAL;
+  o->image_bytes = c->plan.C * c->plan.total_chunks;
+  o->chunk_bytes = c->plan.C;
+  o->total_chunks = c->plan.total_chunks;
+  o->snapshot_bytes = 2 * c->params;
+  o->params = c->params;
+  o->n_tensors = (int32_t)c->ts.size();
+  o->n_nodes = c->n_nodes;
+  return LAM_OK;
+}
+
+extern "C" lam_status lam_get_stats(lam_ctx* c, lam_stats* o) {
+  if (!c || !o) return LAM_EINVAL;
+  Lock l(c->shm);
+  *o = c->shm->stats;
+  return LAM_OK;
+}
+
+static lam_status locate(lam_ctx* c, int node, uint64_t v, int* slot) {
+  if (!c || node < 0 || node >= c->n_nodes) return LAM_EINVAL;
+  *slot = find_slot(c->shm->node[node], c->S, v, S_COMPLETE);
+  return *slot < 0 ? LAM_ENOVERSION : LAM_OK;
+}
+
+extern "C" lam_status lam_read_image(lam_ctx* c, int32_t node, uint64_t v, uint64_t off, uint64_t nbytes, void* host) {
+  if (!c || !host) return LAM_EINVAL;
+  Lock l(c->shm);
+  int s;
+  lam_status st = locate(c, node, v, &s);
+  if (st != LAM_OK) return st;
+  const uint64_t C = c->plan.C, end = off + nbytes;
+  if (end > C * c->plan.total_chunks) return LAM_EINVAL;
+  uint8_t* h = (uint8_t*)host;
+  while (off < end) {
+    uint64_t g = off / C;
+    int r = (int)c->plan.chunk_rank[g];
+    uint64_t rend = (c->plan.chunk_base[r] + c->plan.n_chunks[r]) * C;
+    uint64_t n = std::min(end, rend) - off;
+    const Part& p = c->parts[c->node_rank_part[node][r]];
+    const uint8_t* src = slot_data(p, s) + p.rank_off[r] + (off - c->plan.chunk_base[r] * C);
+    CK(cudaMemcpy(h, src, n, cudaMemcpyDefault));
+    h += n;
+    off += n;
+  }
+  return LAM_OK;
+}
+
+extern "C" lam_status lam_read_headers(lam_ctx* c, int32_t node, uint64_t v, lam_chunk_header* host,
+                                       uint64_t first, uint64_t count) {
+  if (!c || !host) return LAM_EINVAL;
+  Lock l(c->shm);
+  int s;
+  lam_status st = locate(c, node, v, &s);
+  if (st != LAM_OK) return st;
+  if (first + count > c->plan.total_chunks) return LAM_EINVAL;
+  for (uint64_t g = first; g < first + count; ++g) {
+    const Part& p = c->parts[c->node_rank_part[node][c->plan.chunk_rank[g]]];
+    ChunkMeta m = meta_of(c, p, s);
+    CK(cudaMemcpy(host + (g - first), m.hdr + g, sizeof(lam_chunk_header), cudaMemcpyDefault));
+  }
+  return LAM_OK;
+}
+
+extern "C" lam_status lam_set_profiling(lam_ctx* c, int32_t on) {
+  if (!c) return LAM_EINVAL;
+  Lock l(c->shm);
+  c->profiling = on != 0;
+  return LAM_OK;
+}
+
+extern "C" lam_status lam_kernel_times(lam_ctx* c, double ms[3], uint64_t cnt[3]) {
+  if (!c || !ms || !cnt) return LAM_EINVAL;
+  Lock l(c->shm);
+  for (int k = 0; k < 3; ++k) { ms[k] = 0; cnt[k] = 0; }
+  std::vector<lam_ctx::Timed> keep;
+  for (auto& t : c->timed) {
+    if (cudaEventQuery(t.b) != cudaSuccess) { cudaGetLastError(); keep.push_back(t); continue; }
+    float x = 0;
+    CK(cudaEventElapsedTime(&x, t.a, t.b));
+    ms[t.kind] += x;
+    cnt[t.kind]++;
+    c->tev_pool[t.dev].push_back(t.a);
+    c->tev_pool[t.dev].push_back(t.b);
+  }
+  c->timed.swap(keep);
+  return LAM_OK;
+}
+
+extern "C" lam_status lam_debug_region(lam_ctx* c, int32_t node, uint64_t v, int32_t rank, void** ptr) {
+  if (!c || !ptr || node < 0 || node >= c->n_nodes || rank < 0 || rank >= c->cfg.fsdp_size) return LAM_EINVAL;
+  Lock l(c->shm);
+  const ShmNode& n = c->shm->node[node];
+  int s = find_slot(n, c->S, v, S_COMPLETE);
+  if (s < 0) s = find_slot(n, c->S, v, S_FILLING);
+  if (s < 0) return LAM_ENOVERSION;
+  const Part& p = c->parts[c->node_rank_part[node][rank]];
+  if (!p.base) return LAM_EINVAL;
+  *ptr = slot_data(p, s) + p.rank_off[rank];
+  return LAM_OK;
+}
+
+extern "C" void lam_destroy(lam_ctx* c) {
+  if (!c) return;
+  for (Part& p : c->parts) {
+    if (p.local && p.base) {
+      cudaSetDevice(p.device);
+      cudaDeviceSynchronize();
+    }
+  }
+  for (auto& kv : c->dev) {
+    cudaSetDevice(kv.first);
+    cudaDeviceSynchronize();
+    if (kv.second.d_chunk_len) cudaFree(kv.second.d_chunk_len);
+    if (kv.second.side) cudaStreamDestroy(kv.second.side);
+  }
+  for (auto& kv : c->plans) {
+    cudaFree(kv.second.d_tiles);
+  }
+  for (auto& kv : c->d_rank_base) {
+    cudaSetDevice(kv.first.second);
+    cudaFree((void*)kv.second);
+  }
+  for (RankPub& rp : c->pubs) {
+    if (rp.d_units) cudaFree(rp.d_units);
+    if (rp.d_units_per_chunk) cudaFree(rp.d_units_per_chunk);
+    if (rp.d_ptrs) cudaFree((void*)rp.d_ptrs);
+    for (int s = 0; s < LAM_MAX_SLOTS; ++s)
+      if (rp.ev[s]) cudaEventDestroy(rp.ev[s]);
+  }
+  for (Part& p : c->parts) {
+    if (p.ipc_opened && p.base) cudaIpcCloseMemHandle(p.base);
+    if (!p.local) continue;
+    cudaSetDevice(p.device);
+    if (p.d_tiles) cudaFree(p.d_tiles);
+    if (p.d_tiles_per_chunk) cudaFree(p.d_tiles_per_chunk);
+    if (p.d_links) cudaFree(p.d_links);
+    if (p.base) cudaFree(p.base);
+    if (p.err_host) cudaFreeHost(p.err_host);
+    for (int s = 0; s < LAM_MAX_SLOTS; ++s)
+      if (p.done_ev[s]) cudaEventDestroy(p.done_ev[s]);
+    if (p.stream) cudaStreamDestroy(p.stream);
+  }
+  for (auto& pp : c->pending) cudaEventDestroy(pp.ev);
+  for (auto& kv : c->ev_pool)
+    for (cudaEvent_t e : kv.second) cudaEventDestroy(e);
+  for (auto& kv : c->tev_pool)
+    for (cudaEvent_t e : kv.second) cudaEventDestroy(e);
+  for (auto& t : c->timed) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }
+  if (c->shm) {
+    if (c->shm_mapped) {
+      munmap(c->shm, sizeof(Shm));
+      if (c->shm_owner) {
+        char name[80];
+        snprintf(name, sizeof name, "/%s", c->cfg.shm_name);
+        shm_unlink(name);
+      }
+    } else {
+      pthread_mutex_destroy(&c->shm->mu);
+      delete c->shm;
+    }
+  }
+  delete c;
+}

@@ -1,0 +1,390 @@
+"""Thin ctypes binding of liblam.so (include/lam.h): same names, argument marshalling only.
+
+Every step of the path runs in liblam's CUDA kernels; this module only converts Python values to
+the C structs.  There is no CPU fallback: `load()` raises if liblam.so is missing, and liblam
+returns LAM_ECUDA when no GPU is present.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "liblam.so")
+
+LAM_MAX_RANKS, LAM_MAX_NODES, LAM_MAX_ROLLOUTS, LAM_MAX_DEVICES, LAM_MAX_SLOTS = 64, 32, 64, 16, 4
+LAM_OK, LAM_ENOVERSION, LAM_IDLE = 0, 1, 2
+LAM_EINVAL, LAM_ESTALE, LAM_ECUDA, LAM_ECHECKSUM, LAM_ENOMEM = -1, -2, -3, -4, -5
+LAM_ESHUTDOWN, LAM_EBUSY, LAM_ETIMEOUT, LAM_EIPC = -6, -7, -8, -9
+LAM_FSDP2_DIM0, LAM_FSDP1_FLAT = 0, 1
+LAM_REPLICATE, LAM_SHARD_DIM0, LAM_SHARD_DIM1, LAM_VOCAB_DIM0 = 0, 1, 2, 3
+
+
+class lam_model_dims(C.Structure):
+    _fields_ = [(n, C.c_int64) for n in ("hidden", "intermediate", "layers", "heads", "kv_heads",
+                                          "head_dim", "vocab")]
+
+
+class lam_node_desc(C.Structure):
+    _fields_ = [("part_device", C.c_int32 * LAM_MAX_RANKS)]
+
+
+class lam_rollout_desc(C.Structure):
+    _fields_ = [("node", C.c_int32), ("device", C.c_int32)]
+
+
+class lam_config(C.Structure):
+    _fields_ = [("model", lam_model_dims), ("actor_layout", C.c_int32), ("fsdp_size", C.c_int32),
+                ("actor_device", C.c_int32 * LAM_MAX_RANKS), ("n_relays", C.c_int32),
+                ("relay", lam_node_desc * LAM_MAX_NODES), ("slots", C.c_int32), ("chunk_bytes", C.c_uint64),
+                ("t_start_s", C.c_double), ("t_byte_s", C.c_double), ("n_rollouts", C.c_int32),
+                ("rollout", lam_rollout_desc * LAM_MAX_ROLLOUTS), ("proc_rank", C.c_int32),
+                ("n_procs", C.c_int32), ("proc_of_device", C.c_int32 * LAM_MAX_DEVICES),
+                ("shm_name", C.c_char * 64), ("pack_ctas", C.c_int32), ("hop_ctas", C.c_int32),
+                ("pull_ctas", C.c_int32), ("spin_timeout_s", C.c_double)]
+
+
+class lam_shard(C.Structure):
+    _fields_ = [("tensor_id", C.c_uint32), ("_pad", C.c_uint32), ("elem_offset", C.c_uint64),
+                ("elem_count", C.c_uint64), ("ptr", C.c_void_p)]
+
+
+class lam_part(C.Structure):
+    _fields_ = [("tensor_id", C.c_uint32), ("rule", C.c_int32)]
+
+
+class lam_dst(C.Structure):
+    _fields_ = [("parts", C.POINTER(lam_part)), ("n_parts", C.c_int32), ("transpose", C.c_int32),
+                ("dst", C.c_void_p), ("dst_row_pitch_bytes", C.c_int64)]
+
+
+class lam_tp_layout(C.Structure):
+    _fields_ = [("tp_size", C.c_int32), ("tp_rank", C.c_int32), ("dsts", C.POINTER(lam_dst)),
+                ("n_dsts", C.c_int32)]
+
+
+class lam_chunk_header(C.Structure):
+    _fields_ = [(n, C.c_uint64) for n in ("version", "idx", "n", "bytes", "s1", "s2", "_p0", "_p1")]
+
+
+class lam_plan_info(C.Structure):
+    _fields_ = [("image_bytes", C.c_uint64), ("chunk_bytes", C.c_uint64), ("total_chunks", C.c_uint64),
+                ("snapshot_bytes", C.c_uint64), ("params", C.c_uint64), ("n_tensors", C.c_int32),
+                ("n_nodes", C.c_int32)]
+
+
+class lam_segment_info(C.Structure):
+    _fields_ = [("tensor_id", C.c_uint32), ("rank", C.c_uint32), ("elem0", C.c_uint64), ("count", C.c_uint64),
+                ("image_off", C.c_uint64)]
+
+
+class lam_copy_tile_info(C.Structure):
+    _fields_ = [("src_off", C.c_uint64), ("dst", C.c_uint64), ("src_pitch", C.c_uint32), ("dst_pitch", C.c_uint32),
+                ("rows", C.c_uint32), ("row_bytes", C.c_uint32), ("src_rank", C.c_uint32), ("align", C.c_uint32)]
+
+
+class lam_stats(C.Structure):
+    _fields_ = [(n, C.c_uint64) for n in ("publishes", "publish_busy", "hops_launched", "versions_skipped",
+                                          "pulls", "checksum_errors", "timeouts", "plan_cache_hits",
+                                          "plan_cache_misses")]
+
+
+_LIB = None
+
+
+def load() -> C.CDLL:
+    """Load liblam.so (fails loudly if it was not built — there is no fallback path)."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"{LIB_PATH} is missing: run __graft_entry__.build() (no CPU fallback exists)")
+    L = C.CDLL(LIB_PATH)
+    P, V = C.POINTER, C.c_void_p
+    sig = {
+        "lam_init": (C.c_int32, [P(lam_config), P(V)]),
+        "lam_export_ipc": (C.c_int32, [V, V, C.c_size_t, P(C.c_size_t)]),
+        "lam_import_ipc": (C.c_int32, [V, C.c_int32, V, C.c_size_t]),
+        "lam_connect": (C.c_int32, [V]),
+        "lam_destroy": (None, [V]),
+        "lam_strerror": (C.c_char_p, [C.c_int32]),
+        "lam_publish": (C.c_int32, [V, C.c_uint64, C.c_int32, P(lam_shard), C.c_int32, V, V]),
+        "lam_relay_step": (C.c_int32, [V, P(C.c_int32)]),
+        "lam_pull": (C.c_int32, [V, C.c_int32, P(lam_tp_layout), V, P(C.c_uint64)]),
+        "lam_latest": (C.c_int32, [V, C.c_int32, P(C.c_uint64)]),
+        "lam_get_plan_info": (C.c_int32, [V, P(lam_plan_info)]),
+        "lam_get_stats": (C.c_int32, [V, P(lam_stats)]),
+        "lam_read_image": (C.c_int32, [V, C.c_int32, C.c_uint64, C.c_uint64, C.c_uint64, V]),
+        "lam_read_headers": (C.c_int32, [V, C.c_int32, C.c_uint64, P(lam_chunk_header), C.c_uint64, C.c_uint64]),
+        "lam_set_profiling": (C.c_int32, [V, C.c_int32]),
+        "lam_kernel_times": (C.c_int32, [V, P(C.c_double), P(C.c_uint64)]),
+        "lam_debug_region": (C.c_int32, [V, C.c_int32, C.c_uint64, C.c_int32, P(V)]),
+        "lam_model_n_tensors": (C.c_int32, [P(lam_model_dims)]),
+        "lam_model_tensor": (C.c_int32, [P(lam_model_dims), C.c_int32, C.c_char_p, C.c_int32,
+                                         P(C.c_int64), P(C.c_int32)]),
+        "lam_vllm_layout": (C.c_int32, [P(lam_model_dims), C.c_int32, P(lam_dst), C.c_int32, P(lam_part),
+                                        C.c_int32, C.c_char_p, C.c_int32, P(C.c_int64), P(C.c_int64)]),
+        "lam_plan_segments": (C.c_int64, [P(lam_model_dims), C.c_int32, C.c_int32, C.c_uint64,
+                                          P(lam_segment_info), C.c_int64]),
+        "lam_plan_copy_tiles": (C.c_int64, [P(lam_model_dims), C.c_int32, C.c_int32, C.c_uint64, P(lam_tp_layout),
+                                            P(lam_copy_tile_info), C.c_int64]),
+        "lam_optimal_chunks": (C.c_int64, [C.c_int32, C.c_double, C.c_double, C.c_double, C.c_int64]),
+        "lam_chain_latency": (C.c_double, [C.c_int32, C.c_int64, C.c_double, C.c_double, C.c_double]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype, f.argtypes = res, args
+    _LIB = L
+    return L
+
+
+EXPORTED = ["lam_init", "lam_export_ipc", "lam_import_ipc", "lam_connect", "lam_destroy", "lam_strerror",
+            "lam_publish", "lam_relay_step", "lam_pull", "lam_latest", "lam_get_plan_info", "lam_get_stats",
+            "lam_read_image", "lam_read_headers", "lam_debug_region", "lam_set_profiling", "lam_kernel_times", "lam_model_n_tensors", "lam_model_tensor", "lam_vllm_layout",
+            "lam_plan_segments", "lam_plan_copy_tiles", "lam_optimal_chunks", "lam_chain_latency"]
+
+
+class LamError(RuntimeError):
+    def __init__(self, status: int, what: str):
+        self.status = status
+        super().__init__(f"{what}: {load().lam_strerror(status).decode()} ({status})")
+
+
+def _check(st: int, what: str, ok=(LAM_OK,)) -> int:
+    if st not in ok:
+        raise LamError(st, what)
+    return st
+
+
+# ------------------------------------------------------------------------------ model helpers
+def dims(H, I, L, nh, nkv, hd, V) -> lam_model_dims:
+    return lam_model_dims(H, I, L, nh, nkv, hd, V)
+
+
+def model_tensors(d: lam_model_dims) -> list[tuple[str, tuple[int, ...]]]:
+    L = load()
+    n = L.lam_model_n_tensors(C.byref(d))
+    _check(0 if n > 0 else LAM_EINVAL, "lam_model_n_tensors")
+    out, name, shape, nd = [], C.create_string_buffer(128), (C.c_int64 * 2)(), C.c_int32()
+    for i in range(n):
+        _check(L.lam_model_tensor(C.byref(d), i, name, 128, shape, C.byref(nd)), "lam_model_tensor")
+        out.append((name.value.decode(), (shape[0], shape[1]) if nd.value == 2 else (shape[0],)))
+    return out
+
+
+@dataclass
+class VllmDst:
+    name: str
+    rows: int
+    cols: int
+    parts: list[tuple[int, int]]          # (tensor_id, rule)
+
+
+def vllm_layout(d: lam_model_dims, tp: int) -> list[VllmDst]:
+    L = load()
+    n = L.lam_vllm_layout(C.byref(d), tp, None, 0, None, 0, None, 0, None, None)
+    _check(0 if n > 0 else LAM_EINVAL, f"lam_vllm_layout(tp={tp})")
+    dsts, parts = (lam_dst * n)(), (lam_part * (4 * n))()
+    names = C.create_string_buffer(128 * n)
+    rows, cols = (C.c_int64 * n)(), (C.c_int64 * n)()
+    got = L.lam_vllm_layout(C.byref(d), tp, dsts, n, parts, 4 * n, names, 128, rows, cols)
+    _check(0 if got == n else LAM_EINVAL, "lam_vllm_layout")
+    out = []
+    for i in range(n):
+        nm = C.string_at(C.addressof(names) + 128 * i).decode()
+        ps = [(dsts[i].parts[j].tensor_id, dsts[i].parts[j].rule) for j in range(dsts[i].n_parts)]
+        out.append(VllmDst(nm, rows[i], cols[i], ps))
+    return out
+
+
+class TPLayout:
+    """A rollout TP rank's destination buffers (keeps the ctypes arrays alive)."""
+
+    def __init__(self, tp_size: int, tp_rank: int, dsts: list[tuple[list[tuple[int, int]], int, int]]):
+        """dsts: list of (parts [(tensor_id, rule)], device pointer, row pitch bytes or 0)."""
+        self._parts = [(lam_part * len(p))(*[lam_part(t, r) for t, r in p]) for p, _, _ in dsts]
+        self._dsts = (lam_dst * max(1, len(dsts)))()
+        for i, (p, ptr, pitch) in enumerate(dsts):
+            self._dsts[i] = lam_dst(C.cast(self._parts[i], C.POINTER(lam_part)), len(p), 0, ptr, pitch)
+        self.c = lam_tp_layout(tp_size, tp_rank, C.cast(self._dsts, C.POINTER(lam_dst)), len(dsts))
+
+
+# ------------------------------------------------------------------------------------ context
+@dataclass
+class Config:
+    model: lam_model_dims
+    fsdp_size: int = 1
+    actor_devices: list[int] = field(default_factory=lambda: [0])
+    relays: list[list[int]] = field(default_factory=list)      # per relay node: device per actor rank
+    rollouts: list[tuple[int, int]] = field(default_factory=list)  # (node, device)
+    actor_layout: int = LAM_FSDP2_DIM0
+    slots: int = 2
+    chunk_bytes: int = 0
+    t_start_s: float = 0.0
+    t_byte_s: float = 0.0
+    proc_rank: int = 0
+    n_procs: int = 1
+    proc_of_device: dict[int, int] | None = None            # default: every used device -> proc 0
+    shm_name: str = ""
+    pack_ctas: int = 0
+    hop_ctas: int = 0
+    pull_ctas: int = 0
+    spin_timeout_s: float = 0.0
+
+    def to_c(self) -> lam_config:
+        c = lam_config()
+        c.model = self.model
+        c.actor_layout, c.fsdp_size, c.n_relays, c.slots = (self.actor_layout, self.fsdp_size,
+                                                            len(self.relays), self.slots)
+        for r, d in enumerate(self.actor_devices):
+            c.actor_device[r] = d
+        for i, node in enumerate(self.relays):
+            for r, d in enumerate(node):
+                c.relay[i].part_device[r] = d
+        c.chunk_bytes, c.t_start_s, c.t_byte_s = self.chunk_bytes, self.t_start_s, self.t_byte_s
+        c.n_rollouts = len(self.rollouts)
+        for i, (node, dev) in enumerate(self.rollouts):
+            c.rollout[i] = lam_rollout_desc(node, dev)
+        c.proc_rank, c.n_procs = self.proc_rank, self.n_procs
+        for d in range(LAM_MAX_DEVICES):
+            c.proc_of_device[d] = -1
+        pod = self.proc_of_device
+        if pod is None:
+            used = set(self.actor_devices) | {d for n in self.relays for d in n} | {d for _, d in self.rollouts}
+            pod = {d: 0 for d in used}
+        for d, p in pod.items():
+            c.proc_of_device[d] = p
+        c.shm_name = self.shm_name.encode()
+        c.pack_ctas, c.hop_ctas, c.pull_ctas, c.spin_timeout_s = (self.pack_ctas, self.hop_ctas, self.pull_ctas,
+                                                                  self.spin_timeout_s)
+        return c
+
+
+class Context:
+    def __init__(self, cfg: Config):
+        self.L = load()
+        self.cfg = cfg
+        self._c = cfg.to_c()
+        h = C.c_void_p()
+        _check(self.L.lam_init(C.byref(self._c), C.byref(h)), "lam_init")
+        self.h = h
+        self._keep = []
+
+    # -- multi-process plumbing (bytes move through torch.distributed in the caller)
+    def export_ipc(self) -> bytes:
+        n = C.c_size_t()
+        _check(self.L.lam_export_ipc(self.h, None, 0, C.byref(n)), "lam_export_ipc")
+        buf = C.create_string_buffer(n.value)
+        _check(self.L.lam_export_ipc(self.h, buf, n.value, C.byref(n)), "lam_export_ipc")
+        return buf.raw[:n.value]
+
+    def import_ipc(self, proc: int, blob: bytes) -> None:
+        _check(self.L.lam_import_ipc(self.h, proc, blob, len(blob)), "lam_import_ipc")
+
+    def connect(self) -> None:
+        _check(self.L.lam_connect(self.h), "lam_connect")
+
+    # -- the path
+    def publish(self, version: int, rank: int, shards: list[tuple[int, int, int, int]], actor_stream: int = 0,
+                reads_done: int | None = None) -> int:
+        """shards: (tensor_id, elem_offset, elem_count, device_ptr).  Returns LAM_OK or LAM_EBUSY."""
+        arr = (lam_shard * max(1, len(shards)))()
+        for i, (t, off, cnt, ptr) in enumerate(shards):
+            arr[i] = lam_shard(t, 0, off, cnt, ptr)
+        st = self.L.lam_publish(self.h, version, rank, arr, len(shards), actor_stream, reads_done)
+        return _check(st, "lam_publish", ok=(LAM_OK, LAM_EBUSY))
+
+    def relay_step(self) -> tuple[int, int]:
+        n = C.c_int32()
+        st = self.L.lam_relay_step(self.h, C.byref(n))
+        _check(st, "lam_relay_step", ok=(LAM_OK, LAM_IDLE))
+        return st, n.value
+
+    def pull(self, rollout: int, layout: TPLayout, stream: int = 0) -> int:
+        v = C.c_uint64()
+        st = self.L.lam_pull(self.h, rollout, C.byref(layout.c), stream, C.byref(v))
+        _check(st, "lam_pull", ok=(LAM_OK, LAM_ENOVERSION))
+        return v.value
+
+    def latest(self, node: int) -> int:
+        v = C.c_uint64()
+        _check(self.L.lam_latest(self.h, node, C.byref(v)), "lam_latest", ok=(LAM_OK, LAM_ENOVERSION))
+        return v.value
+
+    def plan_info(self) -> lam_plan_info:
+        p = lam_plan_info()
+        _check(self.L.lam_get_plan_info(self.h, C.byref(p)), "lam_get_plan_info")
+        return p
+
+    def stats(self) -> dict:
+        s = lam_stats()
+        _check(self.L.lam_get_stats(self.h, C.byref(s)), "lam_get_stats")
+        return {n: getattr(s, n) for n, _ in lam_stats._fields_}
+
+    def read_image(self, node: int, version: int, offset: int, nbytes: int) -> np.ndarray:
+        out = np.empty(nbytes, dtype=np.uint8)
+        _check(self.L.lam_read_image(self.h, node, version, offset, nbytes, out.ctypes.data), "lam_read_image")
+        return out
+
+    def read_headers(self, node: int, version: int, first: int = 0, count: int | None = None) -> list[dict]:
+        if count is None:
+            count = self.plan_info().total_chunks - first
+        arr = (lam_chunk_header * max(1, count))()
+        _check(self.L.lam_read_headers(self.h, node, version, arr, first, count), "lam_read_headers")
+        return [dict(version=h.version, idx=h.idx, n=h.n, bytes=h.bytes, s1=h.s1, s2=h.s2) for h in arr[:count]]
+
+    def set_profiling(self, on: bool) -> None:
+        _check(self.L.lam_set_profiling(self.h, int(on)), "lam_set_profiling")
+
+    def kernel_times(self) -> dict:
+        """{'pack'|'hop'|'pull': (total_ms, launches)} of completed launches since the last call."""
+        ms, n = (C.c_double * 3)(), (C.c_uint64 * 3)()
+        _check(self.L.lam_kernel_times(self.h, ms, n), "lam_kernel_times")
+        return {k: (ms[i], n[i]) for i, k in enumerate(("pack", "hop", "pull"))}
+
+    def debug_region(self, node: int, version: int, rank: int) -> int:
+        p = C.c_void_p()
+        _check(self.L.lam_debug_region(self.h, node, version, rank, C.byref(p)), "lam_debug_region")
+        return p.value
+
+    def close(self) -> None:
+        if self.h:
+            self.L.lam_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def plan_segments(d: lam_model_dims, layout: int, N: int, C_bytes: int) -> list[tuple[int, int, int, int, int]]:
+    """(tensor_id, rank, elem0, count, image_off) of the library's image plan (host-only)."""
+    L = load()
+    n = L.lam_plan_segments(C.byref(d), layout, N, C_bytes, None, 0)
+    _check(0 if n >= 0 else int(n), "lam_plan_segments")
+    arr = (lam_segment_info * max(1, n))()
+    L.lam_plan_segments(C.byref(d), layout, N, C_bytes, arr, n)
+    return [(a.tensor_id, a.rank, a.elem0, a.count, a.image_off) for a in arr[:n]]
+
+
+def plan_copy_tiles(d: lam_model_dims, layout: int, N: int, C_bytes: int, tp: TPLayout) -> list[lam_copy_tile_info]:
+    """The library's pull copy plan for a TP layout (host-only; dst pointers used as integers)."""
+    L = load()
+    n = L.lam_plan_copy_tiles(C.byref(d), layout, N, C_bytes, C.byref(tp.c), None, 0)
+    _check(0 if n >= 0 else int(n), "lam_plan_copy_tiles")
+    arr = (lam_copy_tile_info * max(1, n))()
+    L.lam_plan_copy_tiles(C.byref(d), layout, N, C_bytes, C.byref(tp.c), arr, n)
+    return list(arr[:n])
+
+
+def optimal_chunks(p: int, M: float, t_byte: float, t_start: float, k_cap: int = 1024) -> int:
+    return load().lam_optimal_chunks(p, M, t_byte, t_start, k_cap)
+
+
+def chain_latency(p: int, k: int, M: float, t_byte: float, t_start: float) -> float:
+    return load().lam_chain_latency(p, k, M, t_byte, t_start)

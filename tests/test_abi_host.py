@@ -1,0 +1,108 @@
+"""CPU tests of the C ABI library: it loads, exports every symbol include/lam.h declares, and its host
+planner (model table, vLLM layout, image plan, pull copy plan, Appendix D) agrees with the oracle.
+No compute call is made here: the copy plan is *executed* by a numpy loop in this test only to check
+the planner's arithmetic; the product executes it in k_pull on the GPU."""
+import os
+import re
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import relay as orelay
+from oracle.image import FSDP1_FLAT, FSDP2_DIM0, image_plan, publish
+from oracle.model import MODELS as OMODELS
+from oracle.model import tensors as otensors
+from oracle.tp import direct_pull, vllm_dsts
+from paper_2510_12633_b200 import lam
+from paper_2510_12633_b200.workload import MODELS
+from synth import SEED
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+LAYOUT = {FSDP2_DIM0: lam.LAM_FSDP2_DIM0, FSDP1_FLAT: lam.LAM_FSDP1_FLAT}
+
+
+def test_library_exports_every_declared_symbol():
+    hdr = open(os.path.join(ROOT, "include", "lam.h")).read()
+    declared = set(re.findall(r"\b(lam_[a-z_]+)\s*\(", hdr))
+    L = lam.load()
+    missing = [s for s in sorted(declared) if not hasattr(L, s)]
+    assert not missing, missing
+    assert declared >= set(lam.EXPORTED)
+
+
+def test_no_gpu_fails_loudly():
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(lam.LamError) as e:
+        lam.Context(lam.Config(model=MODELS["tiny"], rollouts=[(0, 0)]))
+    assert e.value.status == lam.LAM_ECUDA
+
+
+@pytest.mark.parametrize("name", ["tiny", "7b", "32b", "72b"])
+def test_model_table_matches_oracle(name):
+    assert lam.model_tensors(MODELS[name]) == otensors(OMODELS[name])
+
+
+@pytest.mark.parametrize("name,tp", [("tiny", 1), ("tiny", 4), ("7b", 2), ("72b", 8)])
+def test_vllm_layout_matches_oracle(name, tp):
+    ours = lam.vllm_layout(MODELS[name], tp)
+    ref = vllm_dsts(OMODELS[name], tp)
+    names = [n for n, _ in otensors(OMODELS[name])]
+    assert [d.name for d in ours] == [d.name for d in ref]
+    for a, b in zip(ours, ref):
+        assert (a.rows,) + ((a.cols,) if len(b.shape) == 2 else ()) == b.shape
+        assert [(names[t], r) for t, r in a.parts] == [(p.tensor, p.rule) for p in b.parts]
+
+
+def test_appendix_d_matches_oracle():
+    import random
+    rng = random.Random(1)
+    for _ in range(200):
+        p, k = rng.randint(2, 300), rng.randint(1, 2000)
+        M, tb, ts = rng.uniform(1e6, 2e11), 1 / rng.uniform(1e9, 1e12), rng.uniform(1e-7, 1e-3)
+        assert lam.chain_latency(p, k, M, tb, ts) == pytest.approx(orelay.chain_latency(p, k, M, tb, ts), rel=1e-12)
+        assert lam.optimal_chunks(p, M, tb, ts, 1024) == orelay.optimal_chunks(p, M, tb, ts, 1024)
+
+
+@pytest.mark.parametrize("name,layout,N,C", [("tiny", FSDP2_DIM0, 1, 1 << 20), ("tiny", FSDP1_FLAT, 3, 1 << 18),
+                                             ("7b", FSDP2_DIM0, 1, 96 << 20), ("32b", FSDP2_DIM0, 4, 64 << 20),
+                                             ("72b", FSDP2_DIM0, 8, 128 << 20), ("7b", FSDP1_FLAT, 8, 1 << 22)])
+def test_image_plan_matches_oracle(name, layout, N, C):
+    ours = lam.plan_segments(MODELS[name], LAYOUT[layout], N, C)
+    plan = image_plan([s for _, s in otensors(OMODELS[name])], N, C, layout)
+    ref = [(s.tensor_id, s.rank, s.elem0, s.count, plan.image_offset(s)) for s in plan.segments]
+    assert ours == ref
+
+
+def _execute_plan(tiles, img_rank_base, img, out_base, out):
+    """numpy executor of the library's copy plan (test-only: checks the plan's arithmetic)."""
+    for t in tiles:
+        for r in range(t.rows):
+            s = img_rank_base[t.src_rank] + t.src_off + r * t.src_pitch
+            d = t.dst - out_base + r * t.dst_pitch
+            out[d:d + t.row_bytes] = img[s:s + t.row_bytes]
+
+
+@pytest.mark.parametrize("layout,N,C,tp", [(FSDP2_DIM0, 1, 1 << 20, 1), (FSDP2_DIM0, 4, 1 << 18, 2),
+                                           (FSDP1_FLAT, 3, 1 << 18, 4), (FSDP2_DIM0, 8, 4096 * 5, 4),
+                                           (FSDP1_FLAT, 8, 4096, 8), (FSDP2_DIM0, 3, 4096 * 3, 2)])
+def test_copy_plan_reproduces_oracle_pull(layout, N, C, tp):
+    d = OMODELS["tiny"]
+    plan = image_plan([s for _, s in otensors(d)], N, C, layout)
+    img, _ = publish(plan, SEED, 4, specials=True)
+    rank_base = [plan.chunk_base[r] * C for r in range(N)]
+    for rank in range(tp):
+        want = direct_pull(d, tp, rank, SEED, 4, specials=True)
+        layout_c = lam.vllm_layout(MODELS["tiny"], tp)
+        base, offs, o = 1 << 40, {}, 0
+        for x in layout_c:
+            offs[x.name] = o
+            o += -(-x.rows * x.cols * 2 // 256) * 256
+        tpl = lam.TPLayout(tp, rank, [(x.parts, base + offs[x.name], 0) for x in layout_c])
+        tiles = lam.plan_copy_tiles(MODELS["tiny"], LAYOUT[layout], N, C, tpl)
+        out = np.full(o, 0xAB, dtype=np.uint8)
+        _execute_plan(tiles, rank_base, img, base, out)
+        for x in layout_c:
+            got = out[offs[x.name]:offs[x.name] + x.rows * x.cols * 2].view(np.uint16)
+            assert np.array_equal(got, want[x.name].ravel()), (x.name, rank)
