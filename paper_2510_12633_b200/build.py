@@ -45,7 +45,8 @@ def _run(cmd: list[str]) -> None:
 def build(verbose: bool = False, force: bool = False) -> list[str]:
     os.makedirs(BUILD, exist_ok=True)
     nvcc = _nvcc()
-    headers = [os.path.join(CSRC, "lam_internal.h"), os.path.join(ROOT, "include", "lam.h")]
+    headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
+    headers.append(os.path.join(ROOT, "include", "lam.h"))
     srcs = ["kernels.cu", "plan.cpp", "model.cpp", "runtime.cpp"]
     objs, jobs = [], []
     for s in srcs:

@@ -5,9 +5,9 @@
 //             checksum (S1, S2) by warp shuffles + one u64 atomic pair per unit; the CTA finishing a
 //             chunk publishes its header and flag (st.release.sys) so the next relay, on another
 //             GPU, can start pulling that chunk while later chunks are still being packed.
-//   k_hop   — chain-pipelined broadcast hop (A3/A4): receiver-driven.  For
-//             each chunk of its part, the node waits (ld.acquire.sys on the predecessor's flag,
-//             over NVLink), copies the chunk from the predecessor's slot with 16-B peer loads into
+//   k_hop   — chain-pipelined broadcast hop (A3/A4), hop.cuh: receiver-driven
+//             TMA bulk pipeline.  Per chunk, the node waits (ld.acquire.sys on the predecessor flag,
+//             over NVLink), bulk-copies the chunk from the predecessor slot through shared memory into
 //             local HBM, recomputes the checksum on the way, and releases its own flag only if it
 //             matches the predecessor's header.  Few CTAs (SM-light).
 //   k_pull  — pull-time TP reshard (A6): copy-plan driven 2-D block copy from
@@ -170,110 +170,7 @@ int launch_pack(const PackUnit* units, uint32_t n_units, const float* const* sha
   return (int)cudaGetLastError();
 }
 
-// ------------------------------------------------------------------------------------- k_hop
-constexpr int kHopThreads = 512;
-constexpr int kHopUnroll = 8;  // 8 x 16 B peer loads in flight per thread (64 KiB per CTA)
-
-enum : int { kHopOk = 0, kHopPoison = 1, kHopAbort = 2, kHopTimeout = 3 };
-
-__device__ void hop_fail(ChunkMeta meta, uint32_t* err_word, uint32_t chunk, uint64_t version, int why) {
-  atomicExch(meta.abort_flag, 1);
-  const uint32_t code = (why == kHopTimeout) ? (uint32_t)(-LAM_ETIMEOUT) : (uint32_t)(-LAM_ECHECKSUM);
-  atomicCAS(err_word, 0u, code);
-  st_release_sys(meta.flags + chunk, version | kPoison);  // tell our successor
-  __threadfence_system();
-}
-
-__global__ void __launch_bounds__(kHopThreads) k_hop(const HopTile* __restrict__ tiles, uint32_t n_tiles,
-                                                     const RankLink* __restrict__ links, ChunkMeta meta,
-                                                     const uint32_t* __restrict__ tiles_per_chunk,
-                                                     uint64_t version, uint32_t* err_word, uint64_t timeout_ns) {
-  __shared__ uint64_t red[2][kHopThreads / 32];
-  __shared__ uint32_t ready_chunk;
-  __shared__ int status;
-  if (threadIdx.x == 0) ready_chunk = 0xFFFFFFFFu;
-  __syncthreads();
-  const uint64_t deadline = globaltimer() + timeout_ns;
-  for (uint32_t ti = blockIdx.x; ti < n_tiles; ti += gridDim.x) {
-    const HopTile T = tiles[ti];
-    const RankLink L = links[T.rank];
-    if (T.chunk != ready_chunk) {
-      if (threadIdx.x == 0) {
-        int st = kHopOk;
-        for (uint32_t spin = 0;; ++spin) {
-          const uint64_t f = ld_acquire_sys(L.src_flags + T.chunk);
-          if (f == version) break;
-          if (f == (version | kPoison)) { st = kHopPoison; break; }
-          if (*(volatile int32_t*)meta.abort_flag) { st = kHopAbort; break; }
-          if ((spin & 63) == 63 && globaltimer() > deadline) { st = kHopTimeout; break; }
-          __nanosleep(spin < 64 ? 64 : 512);
-        }
-        status = st;
-        ready_chunk = T.chunk;
-        if (st != kHopOk) hop_fail(meta, err_word, T.chunk, version, st);
-      }
-      __syncthreads();
-      if (status != kHopOk) return;
-    }
-    const uint8_t* src = L.src + T.region_off;
-    uint8_t* dst = L.dst + T.region_off;
-    const uint32_t nvec = T.bytes >> 4;
-    uint64_t s1 = 0, s2 = 0;
-    for (uint32_t v0 = threadIdx.x; v0 < nvec; v0 += kHopThreads * kHopUnroll) {
-      uint4 w[kHopUnroll];
-#pragma unroll
-      for (int k = 0; k < kHopUnroll; ++k) {
-        const uint32_t v = v0 + k * kHopThreads;
-        if (v < nvec) w[k] = ld_stream_v4(src + 16 * (size_t)v);
-      }
-#pragma unroll
-      for (int k = 0; k < kHopUnroll; ++k) {
-        const uint32_t v = v0 + k * kHopThreads;
-        if (v < nvec) {
-          st_v4(dst + 16 * (size_t)v, w[k]);
-          cks4((uint64_t)T.word0 + 4ull * v, w[k], s1, s2);
-        }
-      }
-    }
-    __threadfence_system();
-    block_reduce2<kHopThreads>(s1, s2, red);
-    if (threadIdx.x == 0) {
-      lam_chunk_header* h = meta.hdr + T.chunk;
-      atomicAdd((unsigned long long*)&h->s1, (unsigned long long)s1);
-      atomicAdd((unsigned long long*)&h->s2, (unsigned long long)s2);
-      __threadfence_system();
-      const uint32_t prev = atomicAdd(meta.cnt + T.chunk, 1u);
-      if (prev + 1 == tiles_per_chunk[T.chunk]) {  // last tile: verify against the predecessor
-        __threadfence_system();
-        const uint64_t got1 = atomicAdd((unsigned long long*)&h->s1, 0ull);
-        const uint64_t got2 = atomicAdd((unsigned long long*)&h->s2, 0ull);
-        const lam_chunk_header* ph = L.src_hdr + T.chunk;
-        const uint64_t want1 = ld_relaxed_sys(&ph->s1), want2 = ld_relaxed_sys(&ph->s2);
-        if (got1 == want1 && got2 == want2) {
-          h->version = ld_relaxed_sys(&ph->version);
-          h->idx = ld_relaxed_sys(&ph->idx);
-          h->n = ld_relaxed_sys(&ph->n);
-          h->bytes = ld_relaxed_sys(&ph->bytes);
-          __threadfence_system();
-          st_release_sys(meta.flags + T.chunk, version);
-        } else {
-          hop_fail(meta, err_word, T.chunk, version, kHopPoison);
-        }
-      }
-    }
-    __syncthreads();
-  }
-}
-
-int launch_hop(const HopTile* tiles, uint32_t n_tiles, const RankLink* links, ChunkMeta meta,
-               const uint32_t* tiles_per_chunk, uint64_t version, uint32_t* err_word, uint64_t timeout_ns,
-               int ctas, void* stream) {
-  if (n_tiles == 0) return 0;
-  unsigned grid = (unsigned)(n_tiles < (uint32_t)ctas ? n_tiles : (uint32_t)ctas);
-  k_hop<<<grid, kHopThreads, 0, (cudaStream_t)stream>>>(tiles, n_tiles, links, meta, tiles_per_chunk, version,
-                                                        err_word, timeout_ns);
-  return (int)cudaGetLastError();
-}
+#include "hop.cuh"  // k_hop: TMA bulk pipeline
 
 // ------------------------------------------------------------------------------------ k_pull
 constexpr int kPullThreads = 512;

@@ -14,7 +14,7 @@ constexpr uint64_t kSegAlign = 256;      // segment start alignment in a rank re
 constexpr uint64_t kChunkAlign = 4096;   // chunk size granularity
 constexpr uint64_t kSlotAlign = 2u << 20;
 constexpr uint32_t kPackUnitElems = 32768;     // fp32 elements per pack work unit (128 KiB read)
-constexpr uint32_t kHopTileBytes = 256u << 10; // bytes per chain-hop tile
+constexpr uint32_t kHopTileBytes = 1u << 20;   // bytes per chain-hop tile
 constexpr uint32_t kPullTileBytes = 256u << 10;
 constexpr uint64_t kPoison = 1ull << 63;       // flag = version | kPoison marks a failed chunk
 

@@ -191,9 +191,10 @@ def test_version_rules_and_busy():
     # pin v5 with a pull whose stream is blocked, publish v6 (other slot), then v7 must be BUSY
     s = torch.cuda.Stream()
     with torch.cuda.stream(s):
-        torch.cuda._sleep(200_000_000)                   # keep the pull (and its pin) in flight
+        torch.cuda._sleep(3_000_000_000)                 # ~1.5 s: keeps the pull (and its pin) in flight
     assert ctx.pull(0, rb.tp, s.cuda_stream) == 5
-    publish_all(ctx, [shard], 6, False)
+    # no device-wide synchronize from here on: it would drain stream s and release the pin
+    assert ctx.publish(6, 0, shard.shards(), torch.cuda.current_stream().cuda_stream) == lam.LAM_OK
     until_busy = time.time()
     while ctx.latest(0) != 6 and time.time() - until_busy < 30:
         ctx.relay_step()
