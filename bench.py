@@ -38,6 +38,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="lam", choices=["lam", "reference"])
     ap.add_argument("--model", default="7b")
+    ap.add_argument("--config", default="chain", choices=["chain", "colocated", "relay-tp"],
+                    help="placement: chain (config 2), colocated (config 4), relay-tp (config 3)")
+    ap.add_argument("--tp", type=int, default=0, help="rollout TP size (colocated / relay-tp)")
     ap.add_argument("--chunk-mb", type=int, default=0, help="chunk size; 0 = Appendix D k*")
     ap.add_argument("--hop-ctas", type=int, default=0)
     ap.add_argument("--pack-ctas", type=int, default=0)
@@ -174,10 +177,43 @@ class Clocks:
 
 
 # -------------------------------------------------------------------------------- GPU leg
+def topology(config: str, N: int, tp_arg: int):
+    """Placement of actor ranks, relay nodes and rollouts on N GPUs (BASELINE.json configs)."""
+    if config == "chain" or N == 1:
+        # config 2: actor FSDP-1 on GPU 0 -> chain of relays on GPUs 1..N-1, one TP=1 rollout each
+        if N == 1:
+            return dict(fsdp=1, actors=[0], relays=[], rollouts=[(0, 0, 1, 0)],
+                        desc="actor FSDP-1 + master node + one TP=1 rollout on GPU0")
+        return dict(fsdp=1, actors=[0], relays=[[d] for d in range(1, N)],
+                    rollouts=[(i, i, 1, 0) for i in range(1, N)],
+                    desc=f"actor FSDP-1 on GPU0 -> chain of {N - 1} relays (GPUs 1..{N - 1}), one TP=1 rollout per relay")
+    if config == "colocated":
+        # config 4: actor FSDP-N colocated on all GPUs; node 0 (the N colocated bf16 shards) serves
+        # TP=tp rollouts that gather their slices over NVLink.  Replica k = GPUs {k + j*N/tp}.
+        tp = tp_arg or N
+        reps = N // tp
+        ro = [(0, k + j * reps, tp, j) for k in range(reps) for j in range(tp)]
+        return dict(fsdp=N, actors=list(range(N)), relays=[], rollouts=ro,
+                    desc=f"actor FSDP-{N} colocated on GPUs 0..{N - 1}; {reps} TP={tp} rollout(s) gather from the colocated shards")
+    if config == "relay-tp":
+        # config 3: actor FSDP-N/2 on GPUs 0..N/2-1 -> one relay node range-sharded over GPUs N/2..N-1
+        # (rank r's region on GPU N/2+r) -> TP=tp rollouts on the relay GPUs gather over NVLink
+        h = N // 2
+        tp = tp_arg or min(2, h)
+        ro = [(1, h + k * tp + j, tp, j) for k in range(h // tp) for j in range(tp)]
+        return dict(fsdp=h, actors=list(range(h)), relays=[[h + r for r in range(h)]], rollouts=ro,
+                    desc=f"actor FSDP-{h} on GPUs 0..{h - 1} -> relay range-sharded over GPUs {h}..{N - 1} -> "
+                         f"{h // tp} TP={tp} rollout(s) on the relay GPUs")
+    raise SystemExit(f"unknown --config {config}")
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if os.environ.get("LAM_BENCH_WATCHDOG"):      # debugging aid: dump every thread's stack, then exit
+        import faulthandler
+        faulthandler.dump_traceback_later(float(os.environ["LAM_BENCH_WATCHDOG"]), exit=True)
     import torch
     import torch.distributed as dist
 
@@ -201,13 +237,14 @@ def main():
             dist.barrier(group=gloo)
 
     model = MODELS[args.model]
-    relays = [[d] for d in range(1, N)]
-    rollouts = [(0, 0)] if N == 1 else [(i, i) for i in range(1, N)]
+    T = topology(args.config, N, args.tp)
+    rollouts = T["rollouts"]
     port = os.environ.get("MASTER_PORT", "0")
-    cfg = lam.Config(model=model, fsdp_size=1, actor_devices=[0], relays=relays, rollouts=rollouts,
-                     chunk_bytes=args.chunk_mb << 20, proc_rank=rank, n_procs=N,
-                     proc_of_device={d: d for d in range(N)}, shm_name=f"lam_bench_{port}_{os.getppid()}",
-                     hop_ctas=args.hop_ctas, pack_ctas=args.pack_ctas, pull_ctas=args.pull_ctas)
+    cfg = lam.Config(model=model, fsdp_size=T["fsdp"], actor_devices=T["actors"], relays=T["relays"],
+                     rollouts=[(n, d) for n, d, _, _ in rollouts], chunk_bytes=args.chunk_mb << 20,
+                     proc_rank=rank, n_procs=N, proc_of_device={d: d for d in range(N)},
+                     shm_name=f"lam_bench_{port}_{os.getppid()}", hop_ctas=args.hop_ctas,
+                     pack_ctas=args.pack_ctas, pull_ctas=args.pull_ctas)
     ctx = lam.Context(cfg)
     if N > 1:
         blobs = [None] * N
@@ -221,26 +258,26 @@ def main():
     M = info.snapshot_bytes
     params = info.params
 
-    shard = None
-    if rank == 0:
-        shard = ActorShard(model, 1, 0, 0)
-        shard.fill(SEED, 1)
-    mine = [rid for rid, (_, dev) in enumerate(rollouts) if dev == rank]
-    bufs = {rid: RolloutBuffers(model, 1, 0, rank) for rid in mine}
+    my_ranks = [r for r, d in enumerate(T["actors"]) if d == rank]
+    shards = {r: ActorShard(model, T["fsdp"], r, rank) for r in my_ranks}
+    for sh in shards.values():
+        sh.fill(SEED, 1)
+    mine = [rid for rid, (_, dev, _, _) in enumerate(rollouts) if dev == rank]
+    bufs = {rid: RolloutBuffers(model, rollouts[rid][2], rollouts[rid][3], rank) for rid in mine}
+    pull_bytes = {rid: ctx.pull_bytes(rid, bufs[rid].tp) for rid in mine}
     stream = torch.cuda.Stream()
-    actor_stream = torch.cuda.Stream() if rank == 0 else None
+    actor_stream = torch.cuda.Stream()
     torch.cuda.synchronize()
-
     state = {"v": 0}
 
     def step(h2d=None, d2h=None):
         state["v"] += 1
         v = state["v"]
-        if rank == 0:
+        for r in my_ranks:
             if h2d is not None:                        # e2e: the step's inputs arrive from host memory
                 with torch.cuda.stream(actor_stream):
-                    shard.buf.copy_(h2d, non_blocking=True)
-            while ctx.publish(v, 0, shard.shards(), actor_stream.cuda_stream) == lam.LAM_EBUSY:
+                    shards[r].buf.copy_(h2d[r], non_blocking=True)
+            while ctx.publish(v, r, shards[r].shards(), actor_stream.cuda_stream) == lam.LAM_EBUSY:
                 ctx.relay_step()
         pending = list(mine)
         while True:
@@ -252,9 +289,9 @@ def main():
                     if d2h is not None:
                         with torch.cuda.stream(stream):
                             for name, t in bufs[rid].bufs.items():
-                                d2h[name].copy_(t, non_blocking=True)
+                                d2h[rid][name].copy_(t, non_blocking=True)
                     pending.remove(rid)
-            if not pending and (rank != 0 or ctx.latest(0) >= v):
+            if not pending and (not my_ranks or ctx.latest(0) >= v):
                 break
         stream.synchronize()
         ctx.relay_step()
@@ -286,53 +323,66 @@ def main():
     st1 = ctx.stats()
     launches = sum(n for _, n in kt.values())
 
-    def allmax(x):
+    def allreduce(x, op):
         if gloo is None:
             return x
         t = torch.tensor([x], dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=gloo)
+        dist.all_reduce(t, op=op, group=gloo)
         return float(t.item())
 
-    def allsum(x):
-        if gloo is None:
-            return x
-        t = torch.tensor([x], dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=gloo)
-        return float(t.item())
-
+    allmax = lambda x: allreduce(x, dist.ReduceOp.MAX if gloo is not None else None)
+    allsum = lambda x: allreduce(x, dist.ReduceOp.SUM if gloo is not None else None)
     ms_max = allmax(ms)
     launches_all = int(allsum(launches))
-    pack_ms = allmax(kt["pack"][0] / max(1, kt["pack"][1]) if kt["pack"][1] else 0.0)
-    hop_ms = allmax(kt["hop"][0] / max(1, kt["hop"][1]) if kt["hop"][1] else 0.0)
-    pull_ms = allmax(kt["pull"][0] / max(1, kt["pull"][1]) if kt["pull"][1] else 0.0)
+    avg = {k: (v / n if n else None) for k, (v, n) in kt.items()}
+    # per-rank roofline candidates of this rank's dominant kernel work
+    cand = []
+    if avg["pack"]:
+        b = 6.0 * sum(sh.numel for sh in shards.values())
+        cand.append(dict(kernel="k_pack", ms=avg["pack"], bound="hbm", bytes=b))
+    if avg["hop"]:
+        part_bytes = sum(info.snapshot_bytes for _ in [0]) if args.config == "chain" else M / max(1, T["fsdp"])
+        cand.append(dict(kernel="k_hop", ms=avg["hop"], bound="nvlink", bytes=float(part_bytes)))
+    if avg["pull"] and mine:
+        loc, rem = pull_bytes[mine[0]]
+        if rem > 0:
+            cand.append(dict(kernel="k_pull", ms=avg["pull"], bound="nvlink", bytes=float(rem), local=loc, remote=rem))
+        else:
+            cand.append(dict(kernel="k_pull", ms=avg["pull"], bound="hbm", bytes=2.0 * loc, local=loc, remote=rem))
+    per_rank = [None] * N
+    mine_info = dict(rank=rank, ms=round(ms, 3), **{k: (round(v, 3) if v else None) for k, v in avg.items()},
+                     cand=cand)
+    if gloo is not None:
+        dist.all_gather_object(per_rank, mine_info, group=gloo)
+    else:
+        per_rank = [mine_info]
 
-    # e2e through the public API with host buffers: H2D of the masters, publish, relay, pull, D2H
+    kmax = {k: allmax(v or 0.0) for k, v in avg.items()}   # collective: every rank, outside rank-0 code
     e2e = None
     if not args.quick and not args.no_e2e:
-        e2e = run_e2e(args, rank, N, shard, bufs, mine, step, barrier, allmax, torch)
+        e2e = run_e2e(args, N, shards, bufs, mine, step, barrier, allmax, torch)
 
     if rank == 0:
-        import json as _json
         peaks = {}
         try:
-            peaks = _json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+            peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
         except Exception:
             pass
         hbm_peak = peaks.get("hbm_gbs", 6650.0)
+        nvl_peak = 770.0
         sec = ms_max / 1e3 / args.steps
-        if N == 1:
-            pack_gbs = 6.0 * params / (pack_ms / 1e3) / 1e9 if pack_ms else None
-            roof = dict(bound="hbm", kernel="k_pack", achieved=pack_gbs, peak=hbm_peak, unit="GB/s",
-                        frac=(pack_gbs / hbm_peak) if pack_gbs else None, traffic=None,
-                        algorithmic_bytes_per_launch=6 * params,
-                        peak_source="MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6.65 TB/s")
-        else:
-            nvl_peak = 770.0
-            hop_gbs = 2.0 * params / (hop_ms / 1e3) / 1e9 if hop_ms else None
-            roof = dict(bound="nvlink", kernel="k_hop", achieved=hop_gbs, peak=nvl_peak, unit="GB/s",
-                        frac=(hop_gbs / nvl_peak) if hop_gbs else None, traffic=None,
-                        algorithmic_bytes_per_launch=2 * params,
-                        peak_source="B200_PROFILING.md measured peer copy 770 GB/s/dir (nominal 900)")
+        allc = [c for pr in per_rank for c in pr["cand"]]
+        dom = max(allc, key=lambda c: c["ms"]) if allc else None
+        roof = None
+        if dom:
+            peak = hbm_peak if dom["bound"] == "hbm" else nvl_peak
+            ach = dom["bytes"] / (dom["ms"] / 1e3) / 1e9
+            roof = dict(bound=dom["bound"], kernel=dom["kernel"], achieved=ach, peak=peak, unit="GB/s",
+                        frac=ach / peak, traffic=traffic_of(dom["kernel"], args.model, N, args.config),
+                        algorithmic_bytes_per_launch=dom["bytes"], launch_ms=dom["ms"],
+                        peak_source=("MEASURED_PEAKS.json hbm_gbs (burst copy)" if dom["bound"] == "hbm" and "hbm_gbs" in peaks
+                                     else "fallback 6.65 TB/s" if dom["bound"] == "hbm"
+                                     else "B200_PROFILING.md measured peer copy 770 GB/s/dir (nominal 900)"))
         cpu = None
         if N == 1 and not args.quick and not args.no_cpu_baseline:
             _, cpu = oracle_sample(args.model, args.cpu_seconds)
@@ -341,14 +391,12 @@ def main():
             metric=METRIC, value=sec, unit=UNIT, n_gpus=N, steps=args.steps, warmup=args.warmup,
             ms_per_step=sec * 1e3, higher_is_better=False, scaling="weak", vs_baseline=None, dtype="bf16",
             data="synthetic",
-            config=dict(workload=(f"{args.model}: actor FSDP-1 on GPU0, " +
-                                  ("master node + 1 TP=1 rollout on GPU0" if N == 1 else
-                                   f"chain of {N - 1} relays on GPUs 1..{N - 1}, one TP=1 rollout per relay")),
+            config=dict(workload=f"{args.model} [{args.config}]: " + T["desc"],
                         model=f"Qwen2.5-{args.model.upper()}-shaped", params=params, snapshot_bytes=M,
                         chunk_bytes=info.chunk_bytes, chunks=info.total_chunks, global_batch=None, seq_len=None,
-                        parallelism=f"relay-chain p={N}", l2="inputs (fp32 masters, slots) >> 126 MB L2"),
+                        parallelism=f"{args.config} N={N}", l2="inputs (fp32 masters, slots) >> 126 MB L2"),
             roofline=roof,
-            kernels_ms=dict(pack=pack_ms, hop=hop_ms, pull=pull_ms),
+            kernels_ms=kmax, per_rank=per_rank,
             host_latency_ms=dict(p50=lat[len(lat) // 2] * 1e3, max=lat[-1] * 1e3),
             paper_context="actor stall 0.64 s (32B) / 1.40 s (72B); 72B to 127 relays < 1.6 s on 128x8 H800 + RDMA",
             cpu_baseline=cpu, e2e=e2e, gpu_launches=launches_all,
@@ -363,6 +411,15 @@ def main():
     return 0
 
 
+def traffic_of(kernel, model, N, config):
+    """dram read+write bytes per launch from the committed ncu --set full capture, if one matches."""
+    try:
+        t = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+        return t.get(f"{kernel}:{model}:{config}:{N}")
+    except Exception:
+        return None
+
+
 class _Null:
     def __enter__(self):
         return self
@@ -371,17 +428,16 @@ class _Null:
         return False
 
 
-def run_e2e(args, rank, N, shard, bufs, mine, step, barrier, allmax, torch):
+def run_e2e(args, N, shards, bufs, mine, step, barrier, allmax, torch):
     import psutil
-    need = (shard.buf.numel() * 4 if shard is not None else 0) + sum(b.bytes for b in bufs.values())
-    ok = psutil.virtual_memory().available > 2 * need + (8 << 30)
-    okall = allmax(0.0 if ok else 1.0) == 0.0
-    if not okall:
+    need = sum(sh.buf.numel() * 4 for sh in shards.values()) + sum(b.bytes for b in bufs.values())
+    need_all = allsum_host(need, torch)          # every rank pins its share of the same host RAM
+    ok = psutil.virtual_memory().available > 1.5 * need_all + (16 << 30)
+    if allmax(0.0 if ok else 1.0) != 0.0:
         return dict(value=None, unit=UNIT, reason="not enough host RAM for pinned buffers")
-    h2d = shard.buf.to("cpu").pin_memory() if shard is not None else None
-    d2h = None
-    if mine:
-        d2h = {n: torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for n, t in bufs[mine[0]].bufs.items()}
+    h2d = {r: sh.buf.to("cpu").pin_memory() for r, sh in shards.items()}
+    d2h = {rid: {n: torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for n, t in bufs[rid].bufs.items()}
+           for rid in mine}
     step(h2d, d2h)  # warm-up with host buffers
     torch.cuda.synchronize()
     barrier()
@@ -394,11 +450,31 @@ def run_e2e(args, rank, N, shard, bufs, mine, step, barrier, allmax, torch):
     e.record(st)
     e.synchronize()
     ms = allmax(s.elapsed_time(e))
-    hb = int(allmax(float(shard.buf.numel() * 4) if shard is not None else 0.0))
-    db = int(allmax(float(sum(b.bytes for b in bufs.values()))))
-    return dict(value=ms / 1e3 / args.e2e_steps, unit=UNIT, h2d_bytes_per_step=hb,
-                d2h_bytes_per_step=db * max(1, N - 1), steps=args.e2e_steps,
+    hb = allsum_host(sum(sh.buf.numel() * 4 for sh in shards.values()), torch)
+    db = allsum_host(sum(b.bytes for b in bufs.values()), torch)
+    return dict(value=ms / 1e3 / args.e2e_steps, unit=UNIT, h2d_bytes_per_step=int(hb), d2h_bytes_per_step=int(db),
+                steps=args.e2e_steps,
                 note="pinned host fp32 masters -> H2D -> lam_publish -> relay -> lam_pull -> D2H of every rollout")
+
+
+def allsum_host(x, torch):
+    import torch.distributed as dist
+    if not dist.is_initialized():
+        return x
+    t = torch.tensor([float(x)], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=_gloo_group())
+    return float(t.item())
+
+
+_GLOO = None
+
+
+def _gloo_group():
+    global _GLOO
+    import torch.distributed as dist
+    if _GLOO is None:
+        _GLOO = dist.new_group(backend="gloo")
+    return _GLOO
 
 
 if __name__ == "__main__":

@@ -220,6 +220,11 @@ lam_status lam_read_headers(lam_ctx*, int32_t node, uint64_t version, lam_chunk_
 lam_status lam_set_profiling(lam_ctx*, int32_t on);
 lam_status lam_kernel_times(lam_ctx*, double ms_out[3], uint64_t count_out[3]);
 
+/* Bytes a pull of `layout` at rollout `rollout_id` reads from the rollout's own GPU (local) and from
+ * other GPUs over NVLink (remote); builds/caches the copy plan.  For roofline accounting. */
+lam_status lam_pull_bytes(lam_ctx*, int32_t rollout_id, const lam_tp_layout* layout, uint64_t* local_bytes,
+                          uint64_t* remote_bytes);
+
 /* Test hook: device pointer (valid in this process) of actor rank `rank`'s region of the slot
  * holding `version` (FILLING or COMPLETE) at `node`.  Used by fault-injection tests only. */
 lam_status lam_debug_region(lam_ctx*, int32_t node, uint64_t version, int32_t rank, void** dev_ptr);

@@ -95,7 +95,7 @@ struct RankPub {   // per local actor rank (node 0)
 struct PullPlan {
   CopyTile* d_tiles = nullptr;
   uint32_t n_tiles = 0;
-  uint64_t bytes = 0;
+  uint64_t bytes = 0, local_bytes = 0, remote_bytes = 0;
 };
 
 struct PendingPull {
@@ -634,6 +634,38 @@ lam_status step_locked(lam_ctx* c, int* transitions, bool* busy) {
   return first_err;
 }
 
+std::string layout_key(int node, const lam_tp_layout& L);
+
+// Cached copy plan of (node, layout); build on miss (caller holds the lock, device = rollout's).
+lam_status get_plan(lam_ctx* c, const lam_rollout_desc& ro, const lam_tp_layout& L, const std::string& key,
+                    PullPlan** out) {
+  auto it = c->plans.find(key);
+  if (it != c->plans.end()) {
+    c->shm->stats.plan_cache_hits++;
+    *out = &it->second;
+    return LAM_OK;
+  }
+  std::vector<CopyTile> tiles;
+  uint64_t bytes = 0;
+  std::string err;
+  if (!build_copy_tiles(c->plan, c->ts, L, &tiles, &bytes, &err)) {
+    fprintf(stderr, "liblam: lam_pull: %s\n", err.c_str());
+    return LAM_EINVAL;
+  }
+  PullPlan pp;
+  pp.n_tiles = (uint32_t)tiles.size();
+  pp.bytes = bytes;
+  for (const CopyTile& t : tiles) {
+    const Part& q = c->parts[c->node_rank_part[ro.node][t.src_rank]];
+    (q.device == ro.device ? pp.local_bytes : pp.remote_bytes) += (uint64_t)t.rows * t.row_bytes;
+  }
+  CK(cudaMalloc(&pp.d_tiles, sizeof(CopyTile) * std::max<size_t>(tiles.size(), 1)));
+  if (!tiles.empty()) CK(cudaMemcpy(pp.d_tiles, tiles.data(), sizeof(CopyTile) * tiles.size(), cudaMemcpyHostToDevice));
+  *out = &c->plans.emplace(key, pp).first->second;
+  c->shm->stats.plan_cache_misses++;
+  return LAM_OK;
+}
+
 std::string layout_key(int node, const lam_tp_layout& L) {
   std::string k = std::to_string(node) + ":" + std::to_string(L.tp_size) + ":" + std::to_string(L.tp_rank);
   for (int i = 0; i < L.n_dsts; ++i) {
@@ -906,25 +938,9 @@ extern "C" lam_status lam_pull(lam_ctx* c, int32_t rid, const lam_tp_layout* L, 
   CK(cudaSetDevice(ro.device));
   std::string key = layout_key(ro.node, *L);
   Lock l(c->shm);
-  auto it = c->plans.find(key);
-  if (it == c->plans.end()) {
-    std::vector<CopyTile> tiles;
-    uint64_t bytes = 0;
-    std::string err;
-    if (!build_copy_tiles(c->plan, c->ts, *L, &tiles, &bytes, &err)) {
-      fprintf(stderr, "liblam: lam_pull: %s\n", err.c_str());
-      return LAM_EINVAL;
-    }
-    PullPlan pp;
-    pp.n_tiles = (uint32_t)tiles.size();
-    pp.bytes = bytes;
-    CK(cudaMalloc(&pp.d_tiles, sizeof(CopyTile) * std::max<size_t>(tiles.size(), 1)));
-    if (!tiles.empty()) CK(cudaMemcpy(pp.d_tiles, tiles.data(), sizeof(CopyTile) * tiles.size(), cudaMemcpyHostToDevice));
-    it = c->plans.emplace(key, pp).first;
-    c->shm->stats.plan_cache_misses++;
-  } else {
-    c->shm->stats.plan_cache_hits++;
-  }
+  PullPlan* pp = nullptr;
+  lam_status pst = get_plan(c, ro, *L, key, &pp);
+  if (pst != LAM_OK) return pst;
   ShmNode& n = c->shm->node[ro.node];
   const uint64_t u = n.latest;
   if (u == 0) return LAM_ENOVERSION;
@@ -934,7 +950,7 @@ extern "C" lam_status lam_pull(lam_ctx* c, int32_t rid, const lam_tp_layout* L, 
   auto rb = c->d_rank_base.find({ro.node * LAM_MAX_SLOTS + s, ro.device});
   if (rb == c->d_rank_base.end()) return LAM_EINVAL;
   cudaEvent_t t0 = prof_begin(c, ro.device, (cudaStream_t)stream);
-  int rc = launch_pull(it->second.d_tiles, it->second.n_tiles, rb->second, c->pull_ctas, stream);
+  int rc = launch_pull(pp->d_tiles, pp->n_tiles, rb->second, c->pull_ctas, stream);
   if (rc) {
     n.slot[s].readers--;
     fprintf(stderr, "liblam: pull launch failed: %s\n", cudaGetErrorString((cudaError_t)rc));
@@ -1017,6 +1033,21 @@ extern "C" lam_status lam_read_headers(lam_ctx* c, int32_t node, uint64_t v, lam
     ChunkMeta m = meta_of(c, p, s);
     CK(cudaMemcpy(host + (g - first), m.hdr + g, sizeof(lam_chunk_header), cudaMemcpyDefault));
   }
+  return LAM_OK;
+}
+
+extern "C" lam_status lam_pull_bytes(lam_ctx* c, int32_t rid, const lam_tp_layout* L, uint64_t* local,
+                                     uint64_t* remote) {
+  if (!c || !c->connected || !L || rid < 0 || rid >= c->cfg.n_rollouts || !local || !remote) return LAM_EINVAL;
+  const lam_rollout_desc ro = c->cfg.rollout[rid];
+  if (!owns(c, ro.device)) return LAM_EINVAL;
+  CK(cudaSetDevice(ro.device));
+  Lock l(c->shm);
+  PullPlan* pp = nullptr;
+  lam_status st = get_plan(c, ro, *L, layout_key(ro.node, *L), &pp);
+  if (st != LAM_OK) return st;
+  *local = pp->local_bytes;
+  *remote = pp->remote_bytes;
   return LAM_OK;
 }
 

@@ -119,6 +119,7 @@ def load() -> C.CDLL:
         "lam_get_stats": (C.c_int32, [V, P(lam_stats)]),
         "lam_read_image": (C.c_int32, [V, C.c_int32, C.c_uint64, C.c_uint64, C.c_uint64, V]),
         "lam_read_headers": (C.c_int32, [V, C.c_int32, C.c_uint64, P(lam_chunk_header), C.c_uint64, C.c_uint64]),
+        "lam_pull_bytes": (C.c_int32, [V, C.c_int32, P(lam_tp_layout), P(C.c_uint64), P(C.c_uint64)]),
         "lam_set_profiling": (C.c_int32, [V, C.c_int32]),
         "lam_kernel_times": (C.c_int32, [V, P(C.c_double), P(C.c_uint64)]),
         "lam_debug_region": (C.c_int32, [V, C.c_int32, C.c_uint64, C.c_int32, P(V)]),
@@ -143,7 +144,7 @@ def load() -> C.CDLL:
 
 EXPORTED = ["lam_init", "lam_export_ipc", "lam_import_ipc", "lam_connect", "lam_destroy", "lam_strerror",
             "lam_publish", "lam_relay_step", "lam_pull", "lam_latest", "lam_get_plan_info", "lam_get_stats",
-            "lam_read_image", "lam_read_headers", "lam_debug_region", "lam_set_profiling", "lam_kernel_times", "lam_model_n_tensors", "lam_model_tensor", "lam_vllm_layout",
+            "lam_read_image", "lam_read_headers", "lam_debug_region", "lam_set_profiling", "lam_kernel_times", "lam_pull_bytes", "lam_model_n_tensors", "lam_model_tensor", "lam_vllm_layout",
             "lam_plan_segments", "lam_plan_copy_tiles", "lam_optimal_chunks", "lam_chain_latency"]
 
 
@@ -335,6 +336,12 @@ class Context:
         arr = (lam_chunk_header * max(1, count))()
         _check(self.L.lam_read_headers(self.h, node, version, arr, first, count), "lam_read_headers")
         return [dict(version=h.version, idx=h.idx, n=h.n, bytes=h.bytes, s1=h.s1, s2=h.s2) for h in arr[:count]]
+
+    def pull_bytes(self, rollout: int, layout: TPLayout) -> tuple[int, int]:
+        """(local, remote) bytes a pull of `layout` reads (remote = over NVLink)."""
+        a, b = C.c_uint64(), C.c_uint64()
+        _check(self.L.lam_pull_bytes(self.h, rollout, C.byref(layout.c), C.byref(a), C.byref(b)), "lam_pull_bytes")
+        return a.value, b.value
 
     def set_profiling(self, on: bool) -> None:
         _check(self.L.lam_set_profiling(self.h, int(on)), "lam_set_profiling")

@@ -9,6 +9,7 @@
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
+#include <vector>
 
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("%s: %s\n", #x, cudaGetErrorString(e)); exit(1); } } while (0)
 
@@ -77,43 +78,76 @@ __global__ void __launch_bounds__(128) k_tma(const char* __restrict__ src, char*
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// TMA push: local global -> smem -> peer global
+template <int STAGES, int SB>
+__global__ void __launch_bounds__(128) k_tma_push(const char* __restrict__ src, char* __restrict__ dst, size_t bytes) {
+  k_tma<STAGES, SB>(src, dst, bytes);
+}
+
+struct Bufs { char* a[8]; };
+
 int main(int argc, char** argv) {
-  int a = 0, b = 1;
-  size_t bytes = (size_t)2 << 30;
   int ndev = 0;
   CK(cudaGetDeviceCount(&ndev));
   if (ndev < 2) { printf("need 2 GPUs\n"); return 0; }
-  char *pa, *pb, *pb2;
-  CK(cudaSetDevice(a)); CK(cudaMalloc(&pa, bytes)); CK(cudaMemset(pa, 1, bytes)); CK(cudaDeviceEnablePeerAccess(b, 0));
-  CK(cudaSetDevice(b)); CK(cudaMalloc(&pb, bytes)); CK(cudaMalloc(&pb2, bytes)); CK(cudaDeviceEnablePeerAccess(a, 0));
-  auto timeit = [&](int dev, auto fn) {
-    CK(cudaSetDevice(dev));
-    cudaEvent_t e0, e1; CK(cudaEventCreate(&e0)); CK(cudaEventCreate(&e1));
-    fn(); CK(cudaDeviceSynchronize());
-    float best = 1e9;
-    for (int r = 0; r < 5; ++r) {
-      CK(cudaEventRecord(e0)); fn(); CK(cudaEventRecord(e1)); CK(cudaEventSynchronize(e1));
-      float ms; CK(cudaEventElapsedTime(&ms, e0, e1)); if (ms < best) best = ms;
-    }
-    CK(cudaGetLastError());
-    return bytes / (best / 1e3) / 1e9;
-  };
-  size_t n = bytes / 16;
-  int ctas[] = {16, 32, 48, 64, 96, 148, 296};
-  printf("mode      ctas  unroll  GB/s\n");
-  for (int c : ctas) {
-    printf("pull  %6d  %6d  %7.1f\n", c, 8, timeit(b, [&] { k_copy<8><<<c, 512>>>((const uint4*)pa, (uint4*)pb, n); }));
-    printf("pull  %6d  %6d  %7.1f\n", c, 16, timeit(b, [&] { k_copy<16><<<c, 512>>>((const uint4*)pa, (uint4*)pb, n); }));
-    printf("push  %6d  %6d  %7.1f\n", c, 4, timeit(a, [&] { k_copy<4><<<c, 512>>>((const uint4*)pa, (uint4*)pb, n); }));
-    printf("push  %6d  %6d  %7.1f\n", c, 8, timeit(a, [&] { k_copy<8><<<c, 512>>>((const uint4*)pa, (uint4*)pb, n); }));
+  const size_t bytes = (size_t)2 << 30;
+  // per GPU: src buffer (own data) and dst buffer (received data)
+  char *src[8], *dst[8];
+  for (int d = 0; d < ndev; ++d) {
+    CK(cudaSetDevice(d)); CK(cudaMalloc(&src[d], bytes)); CK(cudaMalloc(&dst[d], bytes)); CK(cudaMemset(src[d], d + 1, bytes));
+    for (int e = 0; e < ndev; ++e) if (e != d) { cudaError_t r = cudaDeviceEnablePeerAccess(e, 0); if (r != cudaSuccess) cudaGetLastError(); }
   }
-  CK(cudaSetDevice(b));
   constexpr int ST = 6, SB = 32768;
-  CK(cudaFuncSetAttribute(k_tma<ST, SB>, cudaFuncAttributeMaxDynamicSharedMemorySize, ST * SB));
-  for (int c : ctas)
-    printf("tma   %6d  %6d  %7.1f\n", c, ST, timeit(b, [&] { k_tma<ST, SB><<<c, 128, ST * SB>>>(pa, pb, bytes); }));
-  printf("ce (memcpyPeer)      %7.1f\n", timeit(b, [&] { CK(cudaMemcpyPeerAsync(pb, b, pa, a, bytes, 0)); }));
-  printf("local copy (HBM r+w) %7.1f (x2 for r+w)\n", timeit(b, [&] { k_copy<8><<<148 * 4, 512>>>((const uint4*)pb2, (uint4*)pb, n); }));
-  // bidirectional: a pulls from b while b pulls from a (chain middle node sees both directions)
+  for (int d = 0; d < ndev; ++d) { CK(cudaSetDevice(d)); CK(cudaFuncSetAttribute(k_tma<ST, SB>, cudaFuncAttributeMaxDynamicSharedMemorySize, ST * SB)); }
+  cudaStream_t st[8]; cudaEvent_t e0[8], e1[8];
+  for (int d = 0; d < ndev; ++d) { CK(cudaSetDevice(d)); CK(cudaStreamCreate(&st[d])); CK(cudaEventCreate(&e0[d])); CK(cudaEventCreate(&e1[d])); }
+  // run a set of concurrent copies; each copy = (device running it, src ptr, dst ptr, kind)
+  struct Copy { int dev; const char* s; char* d; int kind; };  // kind 0 = TMA kernel, 1 = copy engine, 2 = 16-B push
+  auto run = [&](const char* name, std::vector<Copy> cs, int ctas) {
+    float best = 1e9;
+    for (int rep = 0; rep < 4; ++rep) {
+      for (int d = 0; d < ndev; ++d) { CK(cudaSetDevice(d)); CK(cudaDeviceSynchronize()); }
+      for (auto& c : cs) { CK(cudaSetDevice(c.dev)); CK(cudaEventRecord(e0[c.dev], st[c.dev])); }
+      for (auto& c : cs) {
+        CK(cudaSetDevice(c.dev));
+        if (c.kind == 0) k_tma<ST, SB><<<ctas, 128, ST * SB, st[c.dev]>>>(c.s, c.d, bytes);
+        else if (c.kind == 1) CK(cudaMemcpyAsync(c.d, c.s, bytes, cudaMemcpyDefault, st[c.dev]));
+        else k_copy<8><<<ctas, 512, 0, st[c.dev]>>>((const uint4*)c.s, (uint4*)c.d, bytes / 16);
+      }
+      float worst = 0;
+      for (auto& c : cs) { CK(cudaSetDevice(c.dev)); CK(cudaEventRecord(e1[c.dev], st[c.dev])); }
+      for (auto& c : cs) { CK(cudaSetDevice(c.dev)); CK(cudaEventSynchronize(e1[c.dev])); float ms; CK(cudaEventElapsedTime(&ms, e0[c.dev], e1[c.dev])); if (ms > worst) worst = ms; }
+      CK(cudaGetLastError());
+      if (worst < best) best = worst;
+    }
+    printf("%-44s ctas=%3d  per-copy %6.1f GB/s\n", name, ctas, bytes / (best / 1e3) / 1e9);
+  };
+  auto run_tma = [&](const char* name, std::vector<Copy> cs, int ctas, auto kern, int smem) {
+    for (int d = 0; d < ndev; ++d) { CK(cudaSetDevice(d)); CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)); }
+    float best = 1e9;
+    for (int rep = 0; rep < 4; ++rep) {
+      for (int d = 0; d < ndev; ++d) { CK(cudaSetDevice(d)); CK(cudaDeviceSynchronize()); }
+      for (auto& c : cs) { CK(cudaSetDevice(c.dev)); CK(cudaEventRecord(e0[c.dev], st[c.dev])); }
+      for (auto& c : cs) { CK(cudaSetDevice(c.dev)); kern<<<ctas, 128, smem, st[c.dev]>>>(c.s, c.d, bytes); }
+      float worst = 0;
+      for (auto& c : cs) { CK(cudaSetDevice(c.dev)); CK(cudaEventRecord(e1[c.dev], st[c.dev])); }
+      for (auto& c : cs) { CK(cudaSetDevice(c.dev)); CK(cudaEventSynchronize(e1[c.dev])); float ms; CK(cudaEventElapsedTime(&ms, e0[c.dev], e1[c.dev])); if (ms > worst) worst = ms; }
+      CK(cudaGetLastError());
+      if (worst < best) best = worst;
+    }
+    printf("%-44s ctas=%3d  per-copy %6.1f GB/s\n", name, ctas, bytes / (best / 1e3) / 1e9);
+  };
+  std::vector<Copy> chain3 = {{1, src[0], dst[1], 0}, {2, src[1], dst[2], 0}, {3, src[2], dst[3], 0}};
+  std::vector<Copy> push3 = {{0, src[0], dst[1], 0}, {1, src[1], dst[2], 0}, {2, src[2], dst[3], 0}};
+  for (int ctas : {16, 24, 32, 48}) {
+    run_tma("chain3 pull SB=16K x12", chain3, ctas, k_tma<12, 16384>, 12 * 16384);
+    run_tma("chain3 pull SB=32K x6", chain3, ctas, k_tma<6, 32768>, 6 * 32768);
+    run_tma("chain3 pull SB=64K x3", chain3, ctas, k_tma<3, 65536>, 3 * 65536);
+    run_tma("chain3 pull SB=96K x2", chain3, ctas, k_tma<2, 98304>, 2 * 98304);
+    run_tma("chain3 push SB=32K x6", push3, ctas, k_tma<6, 32768>, 6 * 32768);
+    run_tma("chain3 push SB=64K x3", push3, ctas, k_tma<3, 65536>, 3 * 65536);
+  }
+  run("CE 1<-0", {{1, src[0], dst[1], 1}}, 0);
+  if (ndev >= 4) run("CE chain 1<-0, 2<-1, 3<-2", {{1, src[0], dst[1], 1}, {2, src[1], dst[2], 1}, {3, src[2], dst[3], 1}}, 0);
   return 0;
 }
