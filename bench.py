@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--tp", type=int, default=0, help="rollout TP size (colocated / relay-tp)")
     ap.add_argument("--chunk-mb", type=int, default=0, help="chunk size; 0 = Appendix D k*")
     ap.add_argument("--hop-ctas", type=int, default=0)
+    ap.add_argument("--hop-mode", default="kernel", choices=["kernel", "ce"],
+                    help="relay hop: TMA kernel or copy engines + k_verify")
     ap.add_argument("--pack-ctas", type=int, default=0)
     ap.add_argument("--pull-ctas", type=int, default=0)
     ap.add_argument("--e2e-steps", type=int, default=2)
@@ -244,7 +246,8 @@ def main():
                      rollouts=[(n, d) for n, d, _, _ in rollouts], chunk_bytes=args.chunk_mb << 20,
                      proc_rank=rank, n_procs=N, proc_of_device={d: d for d in range(N)},
                      shm_name=f"lam_bench_{port}_{os.getppid()}", hop_ctas=args.hop_ctas,
-                     pack_ctas=args.pack_ctas, pull_ctas=args.pull_ctas)
+                     pack_ctas=args.pack_ctas, pull_ctas=args.pull_ctas,
+                     hop_mode=lam.LAM_HOP_COPY_ENGINE if args.hop_mode == "ce" else lam.LAM_HOP_KERNEL)
     ctx = lam.Context(cfg)
     if N > 1:
         blobs = [None] * N

@@ -110,7 +110,15 @@ typedef struct {
   /* tuning (0 => default) */
   int32_t pack_ctas, hop_ctas, pull_ctas;
   double spin_timeout_s;                   /* chain-hop wait limit (default 60 s) */
+  int32_t hop_mode;                        /* LAM_HOP_KERNEL (default) | LAM_HOP_COPY_ENGINE */
 } lam_config;
+
+/* How a relay moves a chunk from its predecessor (both receiver-driven, chunk-pipelined, verified):
+ *  LAM_HOP_KERNEL       k_hop: TMA bulk copies through shared memory by ~32 SMs, checksum on the fly
+ *  LAM_HOP_COPY_ENGINE  copy engines (zero SMs for the transfer): per chunk the relay's stream waits
+ *                       for the predecessor's flag (stream memory op), cudaMemcpyAsync pulls the chunk
+ *                       over NVLink, then k_verify checksums it in local HBM and releases the flag. */
+enum { LAM_HOP_KERNEL = 0, LAM_HOP_COPY_ENGINE = 1 };
 
 /* One fp32 master shard piece owned by the caller: elements [elem_offset, elem_offset+elem_count)
  * of the flattened tensor `tensor_id`, at `ptr` (device memory of the actor rank's GPU). */

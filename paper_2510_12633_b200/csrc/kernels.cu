@@ -14,6 +14,8 @@
 //             the pinned relay slot (local HBM or peer GPU) into the rollout's TP buffers.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "lam_internal.h"
 
 namespace lam {
@@ -241,6 +243,83 @@ int launch_pull(const CopyTile* tiles, uint32_t n_tiles, const uint8_t* const* r
   if (n_tiles == 0) return 0;
   unsigned grid = (unsigned)(n_tiles < (uint32_t)ctas ? n_tiles : (uint32_t)ctas);
   k_pull<<<grid, kPullThreads, 0, (cudaStream_t)stream>>>(tiles, n_tiles, rank_base);
+  return (int)cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------- k_verify
+// Copy-engine hop, receiver side: the chunk was copied by a copy engine; recompute its
+// checksum from local HBM, compare with the predecessor's header, and release (or poison) the flag.
+constexpr int kVerifyThreads = 512;
+
+__global__ void __launch_bounds__(kVerifyThreads) k_verify(const uint8_t* __restrict__ data, uint32_t chunk,
+                                                           uint64_t len, uint64_t* pred_flags,
+                                                           const lam_chunk_header* pred_hdr, ChunkMeta meta,
+                                                           uint64_t version, uint32_t* err_word,
+                                                           const uint32_t* __restrict__ my_chunks, uint32_t pos,
+                                                           uint32_t n_my) {
+  __shared__ uint64_t red[2][kVerifyThreads / 32];
+  const uint64_t nvec = len / 16;
+  const uint64_t per = (nvec + gridDim.x - 1) / gridDim.x;
+  const uint64_t v0 = per * blockIdx.x, v1 = min(nvec, v0 + per);
+  uint64_t s1 = 0, s2 = 0;
+  for (uint64_t v = v0 + threadIdx.x; v < v1; v += 4 * kVerifyThreads) {
+    uint4 w[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (v + k * kVerifyThreads < v1) w[k] = ld_stream_v4(data + 16 * (v + k * kVerifyThreads));
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (v + k * kVerifyThreads < v1) cks4(4 * (v + k * kVerifyThreads), w[k], s1, s2);
+  }
+  block_reduce2<kVerifyThreads>(s1, s2, red);
+  if (threadIdx.x != 0) return;
+  lam_chunk_header* h = meta.hdr + chunk;
+  atomicAdd((unsigned long long*)&h->s1, (unsigned long long)s1);
+  atomicAdd((unsigned long long*)&h->s2, (unsigned long long)s2);
+  __threadfence();
+  if (atomicAdd(meta.cnt + chunk, 1u) + 1 != gridDim.x) return;
+  __threadfence();
+  const uint64_t got1 = atomicAdd((unsigned long long*)&h->s1, 0ull);
+  const uint64_t got2 = atomicAdd((unsigned long long*)&h->s2, 0ull);
+  const lam_chunk_header* ph = pred_hdr + chunk;
+  const bool ok = ld_acquire_sys(pred_flags + chunk) == version && got1 == ld_relaxed_sys(&ph->s1) &&
+                  got2 == ld_relaxed_sys(&ph->s2);
+  if (ok) {
+    h->version = ld_relaxed_sys(&ph->version);
+    h->idx = ld_relaxed_sys(&ph->idx);
+    h->n = ld_relaxed_sys(&ph->n);
+    h->bytes = ld_relaxed_sys(&ph->bytes);
+    __threadfence_system();
+    st_release_sys(meta.flags + chunk, version);
+  } else {
+    atomicCAS(err_word, 0u, (uint32_t)(-LAM_ECHECKSUM));
+    st_release_sys(meta.flags + chunk, version | kPoison);
+    for (uint32_t j = pos + 1; j < n_my; ++j) st_release_sys(pred_flags + my_chunks[j], version | kPoison);
+    __threadfence_system();
+  }
+}
+
+__global__ void k_wait_flag(const uint64_t* flag, uint64_t v, uint64_t timeout_ns) {
+  const uint64_t deadline = globaltimer() + timeout_ns;
+  for (uint32_t spin = 0;; ++spin) {
+    if ((int64_t)(ld_acquire_sys(flag) - v) >= 0) return;
+    if ((spin & 63) == 63 && globaltimer() > deadline) return;  // k_verify then reports the failure
+    __nanosleep(200);
+  }
+}
+
+int launch_wait_flag(const uint64_t* flag, uint64_t v, uint64_t timeout_ns, void* stream) {
+  k_wait_flag<<<1, 1, 0, (cudaStream_t)stream>>>(flag, v, timeout_ns);
+  return (int)cudaGetLastError();
+}
+
+int launch_verify(const uint8_t* data, uint32_t chunk, uint64_t len, uint64_t* pred_flags,
+                  const lam_chunk_header* pred_hdr, ChunkMeta meta, uint64_t version, uint32_t* err_word,
+                  const uint32_t* my_chunks, uint32_t pos, uint32_t n_my, int ctas, void* stream) {
+  uint64_t nvec = len / 16;
+  unsigned grid = (unsigned)std::min<uint64_t>((uint64_t)ctas, std::max<uint64_t>(1, nvec / 2048));
+  k_verify<<<grid, kVerifyThreads, 0, (cudaStream_t)stream>>>(data, chunk, len, pred_flags, pred_hdr, meta, version,
+                                                             err_word, my_chunks, pos, n_my);
   return (int)cudaGetLastError();
 }
 

@@ -16,7 +16,9 @@ constexpr uint64_t kSlotAlign = 2u << 20;
 constexpr uint32_t kPackUnitElems = 32768;     // fp32 elements per pack work unit (128 KiB read)
 constexpr uint32_t kHopTileBytes = 1u << 20;   // bytes per chain-hop tile
 constexpr uint32_t kPullTileBytes = 256u << 10;
-constexpr uint64_t kPoison = 1ull << 63;       // flag = version | kPoison marks a failed chunk
+// flag = version | kPoison marks a failed chunk.  Bit 62 (not 63) so that a stream memory op waiting
+// for "(int64)(flag - version) >= 0" is released by a poisoned flag as well.
+constexpr uint64_t kPoison = 1ull << 62;
 
 inline uint64_t cdiv(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
 inline uint64_t align_up(uint64_t a, uint64_t b) { return cdiv(a, b) * b; }
@@ -118,5 +120,14 @@ int launch_hop(const HopTile* tiles, uint32_t n_tiles, const RankLink* links, Ch
                uint64_t timeout_ns, int ctas, void* stream);
 int launch_pull(const CopyTile* tiles, uint32_t n_tiles, const uint8_t* const* rank_base, int ctas,
                 void* stream);
+// One-thread kernel: spin until (int64)(*flag - v) >= 0 or timeout (fallback for stream memory ops).
+int launch_wait_flag(const uint64_t* flag, uint64_t v, uint64_t timeout_ns, void* stream);
+// Copy-engine hop: verify chunk `chunk` (len bytes at `data`, already copied from the predecessor)
+// against the predecessor's header; publish the header and flag — or poison it and also poison the
+// predecessor flags of this part's later chunks (my_chunks[pos+1 .. n_my)) so that the stream's
+// remaining flag waits fall through and the hop terminates.
+int launch_verify(const uint8_t* data, uint32_t chunk, uint64_t len, uint64_t* pred_flags,
+                  const lam_chunk_header* pred_hdr, ChunkMeta meta, uint64_t version, uint32_t* err_word,
+                  const uint32_t* my_chunks, uint32_t pos, uint32_t n_my, int ctas, void* stream);
 
 }  // namespace lam

@@ -78,6 +78,15 @@ struct Part {
   uint32_t n_tiles = 0;
   uint32_t* d_tiles_per_chunk = nullptr;
   RankLink* d_links = nullptr;       // [S][S][N] (my slot, pred slot, rank)
+  // copy-engine hop mode
+  cudaStream_t vstream = nullptr;    // verify stream
+  std::vector<uint32_t> my_chunks;   // this part's chunks in processing order
+  uint32_t* d_my_chunks = nullptr;
+  std::vector<cudaEvent_t> chunk_ev; // [n_my + 1]: per-chunk copy done, last = verify stream done
+  uint32_t ce_next = 0;              // next chunk to enqueue (bounded window, see ce_topup)
+  int ce_slot = -1, ce_ps = -1;
+  uint64_t ce_version = 0;           // non-zero while chunks remain to be enqueued
+  cudaEvent_t ce_t0 = nullptr;
 };
 
 struct RankPub {   // per local actor rank (node 0)
@@ -257,6 +266,7 @@ lam_status validate(const lam_config& c, std::string* why) {
     if (c.rollout[i].node < 0 || c.rollout[i].node > c.n_relays || !dev_ok(c.rollout[i].device))
       return bad("rollout " + std::to_string(i));
   if (c.n_procs > 1 && c.shm_name[0] == 0) return bad("shm_name required with n_procs > 1");
+  if (c.hop_mode != LAM_HOP_KERNEL && c.hop_mode != LAM_HOP_COPY_ENGINE) return bad("hop_mode");
   return LAM_OK;
 }
 
@@ -383,6 +393,17 @@ lam_status alloc_parts(lam_ctx* c) {
       if (!tiles.empty()) CK(cudaMemcpy(p.d_tiles, tiles.data(), sizeof(HopTile) * tiles.size(), cudaMemcpyHostToDevice));
       CK(cudaMalloc(&p.d_tiles_per_chunk, 4 * std::max<uint64_t>(total, 1)));
       if (total) CK(cudaMemcpy(p.d_tiles_per_chunk, tpc.data(), 4 * total, cudaMemcpyHostToDevice));
+      // copy-engine mode: chunk order, verify stream, per-chunk events
+      for (const HopTile& t : tiles)
+        if (p.my_chunks.empty() || p.my_chunks.back() != t.chunk) p.my_chunks.push_back(t.chunk);
+      CK(cudaMalloc(&p.d_my_chunks, 4 * std::max<size_t>(p.my_chunks.size(), 1)));
+      if (!p.my_chunks.empty())
+        CK(cudaMemcpy(p.d_my_chunks, p.my_chunks.data(), 4 * p.my_chunks.size(), cudaMemcpyHostToDevice));
+      if (c->cfg.hop_mode == LAM_HOP_COPY_ENGINE) {
+        CK(cudaStreamCreateWithPriority(&p.vstream, cudaStreamNonBlocking, lo));
+        p.chunk_ev.resize(p.my_chunks.size() + 1);
+        for (auto& e : p.chunk_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      }
     }
   }
   return LAM_OK;
@@ -453,6 +474,80 @@ lam_status connect_links(lam_ctx* c) {
   return LAM_OK;
 }
 
+// ------------------------------------------------------------------------ copy-engine hop mode
+// cuStreamWaitValue64 through the runtime's driver entry point (no link dependency on libcuda).
+typedef int (*WaitValue64Fn)(void* stream, unsigned long long addr, unsigned long long value, unsigned int flags);
+
+WaitValue64Fn wait_value_fn() {
+  static WaitValue64Fn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue64", (void**)&fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    cudaGetLastError();
+  }
+  return fn;
+}
+
+// Stream waits until (int64)(*flag - v) >= 0 (flag == v, or v | kPoison): a front-end stream memory
+// operation when the driver supports it, else a one-thread polling kernel.
+lam_status stream_wait_flag(lam_ctx* c, cudaStream_t st, const uint64_t* flag, uint64_t v) {
+  // Stream memory ops on CUDA-IPC-mapped peer memory never released in multi-process runs on
+  // B200 / driver 580 (observed hang); there, poll with a one-thread kernel instead.
+  WaitValue64Fn fn = c->cfg.n_procs == 1 ? wait_value_fn() : nullptr;
+  if (fn && fn((void*)st, (unsigned long long)(uintptr_t)flag, v, 0x0 /*CU_STREAM_WAIT_VALUE_GEQ*/) == 0)
+    return LAM_OK;
+  if (launch_wait_flag(flag, v, c->timeout_ns, st)) return LAM_ECUDA;
+  return LAM_OK;
+}
+
+// Enqueue the next chunks of the part's copy-engine hop, at most kCeWindow ahead of the copies
+// that completed: enqueueing hundreds of flag waits at once can block the host thread (full push
+// buffer) while it holds the cross-process lock — the predecessor's process could then never
+// launch the work those waits need.  lam_relay_step tops the window up.
+constexpr uint32_t kCeWindow = 8;
+
+lam_status ce_topup(lam_ctx* c, Part& p) {
+  if (!p.ce_version) return LAM_OK;
+  const int s = p.ce_slot, ps = p.ce_ps;
+  const uint64_t u = p.ce_version;
+  ChunkMeta m = meta_of(c, p, s);
+  const uint32_t n = (uint32_t)p.my_chunks.size();
+  CK(cudaSetDevice(p.device));
+  for (uint32_t i = p.ce_next; i < n; i = ++p.ce_next) {
+    if (i >= kCeWindow) {
+      cudaError_t q = cudaEventQuery(p.chunk_ev[i - kCeWindow]);
+      if (q == cudaErrorNotReady) return LAM_OK;
+      if (q != cudaSuccess) return LAM_ECUDA;
+    }
+    const uint32_t g = p.my_chunks[i];
+    const int r = (int)c->plan.chunk_rank[g];
+    const Part& q = c->parts[c->node_rank_part[p.node - 1][r]];
+    ChunkMeta qm = meta_of(c, q, ps);
+    const uint64_t off = (g - c->plan.chunk_base[r]) * c->plan.C, len = c->plan.chunk_len(g);
+    const uint8_t* src = slot_data(q, ps) + q.rank_off[r] + off;
+    uint8_t* dst = slot_data(p, s) + p.rank_off[r] + off;
+    lam_status st = stream_wait_flag(c, p.stream, qm.flags + g, u);
+    if (st != LAM_OK) return st;
+    CK(cudaMemcpyAsync(dst, src, len, cudaMemcpyDeviceToDevice, p.stream));
+    CK(cudaEventRecord(p.chunk_ev[i], p.stream));
+    CK(cudaStreamWaitEvent(p.vstream, p.chunk_ev[i], 0));
+    if (launch_verify(dst, g, len, qm.flags, qm.hdr, m, u, p.err_dev + s, p.d_my_chunks, i, n, 32, p.vstream))
+      return LAM_ECUDA;
+  }
+  // all chunks enqueued: join the verify stream, close the timing bracket, arm completion polling
+  CK(cudaEventRecord(p.chunk_ev.back(), p.vstream));
+  CK(cudaStreamWaitEvent(p.stream, p.chunk_ev.back(), 0));
+  prof_end(c, 1, p.device, p.stream, p.ce_t0);
+  CK(cudaEventRecord(p.done_ev[s], p.stream));
+  p.inflight_version[s] = u;
+  p.ce_version = 0;
+  return LAM_OK;
+}
+
 // ----------------------------------------------------------------------------- progress engine
 // Launch the hop kernel of local part p (node >= 1) for FILLING slot s.  Returns true if launched.
 lam_status launch_hop_part(lam_ctx* c, Part& p, int s, bool* launched) {
@@ -485,13 +580,25 @@ lam_status launch_hop_part(lam_ctx* c, Part& p, int s, bool* launched) {
   ChunkMeta m = meta_of(c, p, s);
   CK(cudaMemsetAsync((uint8_t*)m.hdr, 0, c->sm.abort + 64 - c->sm.hdr, p.stream));  // hdr, cnt, abort
   p.err_host[s] = 0;
-  const RankLink* links = p.d_links + (size_t)(s * c->S + ps) * c->cfg.fsdp_size;
   cudaEvent_t t0 = prof_begin(c, p.device, p.stream);
-  int rc = launch_hop(p.d_tiles, p.n_tiles, links, m, p.d_tiles_per_chunk, u, p.err_dev + s, c->timeout_ns,
-                      c->hop_ctas, p.stream);
-  if (rc) {
-    fprintf(stderr, "liblam: hop launch failed: %s\n", cudaGetErrorString((cudaError_t)rc));
-    return LAM_ECUDA;
+  if (c->cfg.hop_mode == LAM_HOP_COPY_ENGINE) {
+    p.ce_slot = s;
+    p.ce_ps = ps;
+    p.ce_next = 0;
+    p.ce_version = u;
+    p.ce_t0 = t0;
+    sl.launched_mask |= 1ull << p.pos;
+    c->shm->stats.hops_launched++;
+    *launched = true;
+    return ce_topup(c, p);
+  } else {
+    const RankLink* links = p.d_links + (size_t)(s * c->S + ps) * c->cfg.fsdp_size;
+    int rc = launch_hop(p.d_tiles, p.n_tiles, links, m, p.d_tiles_per_chunk, u, p.err_dev + s, c->timeout_ns,
+                        c->hop_ctas, p.stream);
+    if (rc) {
+      fprintf(stderr, "liblam: hop launch failed: %s\n", cudaGetErrorString((cudaError_t)rc));
+      return LAM_ECUDA;
+    }
   }
   prof_end(c, 1, p.device, p.stream, t0);
   CK(cudaEventRecord(p.done_ev[s], p.stream));
@@ -528,9 +635,14 @@ lam_status step_locked(lam_ctx* c, int* transitions, bool* busy) {
       rp.inflight_version[s] = 0;
     }
   }
-  // (2) completions of local hop kernels
+  // (2) copy-engine hops: top up the enqueue window; completions of local hops
   for (Part& p : c->parts) {
     if (!p.local || p.node == 0) continue;
+    if (p.ce_version) {
+      *busy = true;
+      lam_status st = ce_topup(c, p);
+      if (st != LAM_OK) return st;
+    }
     for (int s = 0; s < S; ++s) {
       if (!p.inflight_version[s]) continue;
       cudaError_t q = cudaEventQuery(p.done_ev[s]);
@@ -1124,6 +1236,9 @@ extern "C" void lam_destroy(lam_ctx* c) {
     if (p.d_tiles) cudaFree(p.d_tiles);
     if (p.d_tiles_per_chunk) cudaFree(p.d_tiles_per_chunk);
     if (p.d_links) cudaFree(p.d_links);
+    if (p.d_my_chunks) cudaFree(p.d_my_chunks);
+    for (cudaEvent_t e : p.chunk_ev) cudaEventDestroy(e);
+    if (p.vstream) cudaStreamDestroy(p.vstream);
     if (p.base) cudaFree(p.base);
     if (p.err_host) cudaFreeHost(p.err_host);
     for (int s = 0; s < LAM_MAX_SLOTS; ++s)

@@ -21,6 +21,7 @@ LAM_EINVAL, LAM_ESTALE, LAM_ECUDA, LAM_ECHECKSUM, LAM_ENOMEM = -1, -2, -3, -4, -
 LAM_ESHUTDOWN, LAM_EBUSY, LAM_ETIMEOUT, LAM_EIPC = -6, -7, -8, -9
 LAM_FSDP2_DIM0, LAM_FSDP1_FLAT = 0, 1
 LAM_REPLICATE, LAM_SHARD_DIM0, LAM_SHARD_DIM1, LAM_VOCAB_DIM0 = 0, 1, 2, 3
+LAM_HOP_KERNEL, LAM_HOP_COPY_ENGINE = 0, 1
 
 
 class lam_model_dims(C.Structure):
@@ -44,7 +45,7 @@ class lam_config(C.Structure):
                 ("rollout", lam_rollout_desc * LAM_MAX_ROLLOUTS), ("proc_rank", C.c_int32),
                 ("n_procs", C.c_int32), ("proc_of_device", C.c_int32 * LAM_MAX_DEVICES),
                 ("shm_name", C.c_char * 64), ("pack_ctas", C.c_int32), ("hop_ctas", C.c_int32),
-                ("pull_ctas", C.c_int32), ("spin_timeout_s", C.c_double)]
+                ("pull_ctas", C.c_int32), ("spin_timeout_s", C.c_double), ("hop_mode", C.c_int32)]
 
 
 class lam_shard(C.Structure):
@@ -234,6 +235,7 @@ class Config:
     hop_ctas: int = 0
     pull_ctas: int = 0
     spin_timeout_s: float = 0.0
+    hop_mode: int = LAM_HOP_KERNEL
 
     def to_c(self) -> lam_config:
         c = lam_config()
@@ -261,6 +263,7 @@ class Config:
         c.shm_name = self.shm_name.encode()
         c.pack_ctas, c.hop_ctas, c.pull_ctas, c.spin_timeout_s = (self.pack_ctas, self.hop_ctas, self.pull_ctas,
                                                                   self.spin_timeout_s)
+        c.hop_mode = self.hop_mode
         return c
 
 

@@ -37,7 +37,10 @@ def main():
     ap.add_argument("--tp", type=int, default=0)
     ap.add_argument("--versions", type=int, default=2)
     ap.add_argument("--chunk-kb", type=int, default=64)
+    ap.add_argument("--hop-mode", type=int, default=0)
     a = ap.parse_args()
+    import faulthandler
+    faulthandler.dump_traceback_later(float(os.environ.get("LAM_MP_WATCHDOG", "500")), exit=True)
     rank, N = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     torch.cuda.set_device(rank)
     dist.init_process_group("gloo")
@@ -47,7 +50,8 @@ def main():
     cfg = lam.Config(model=MODELS[a.model], fsdp_size=T["fsdp"], actor_devices=T["actors"], relays=T["relays"],
                      rollouts=[(n, d) for n, d, _, _ in ro], chunk_bytes=a.chunk_kb << 10, proc_rank=rank,
                      n_procs=N, proc_of_device={d: d for d in range(N)},
-                     shm_name=f"lam_mp_{os.environ.get('MASTER_PORT', '0')}_{os.getppid()}", spin_timeout_s=60)
+                     shm_name=f"lam_mp_{os.environ.get('MASTER_PORT', '0')}_{os.getppid()}", spin_timeout_s=60,
+                     hop_mode=a.hop_mode)
     ctx = lam.Context(cfg)
     blobs = [None] * N
     dist.all_gather_object(blobs, ctx.export_ipc())

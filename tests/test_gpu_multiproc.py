@@ -33,6 +33,8 @@ CASES = [  # (min GPUs, args)
     (4, ["--config", "colocated", "--model", "tiny", "--tp", "2"]),
     (4, ["--config", "relay-tp", "--model", "tiny", "--tp", "2"]),
     (2, ["--config", "chain", "--model", "7b", "--chunk-kb", str(128 << 10)]),
+    (4, ["--config", "chain", "--model", "tiny", "--versions", "3", "--chunk-kb", "16", "--hop-mode", "1"]),
+    (4, ["--config", "relay-tp", "--model", "tiny", "--tp", "2", "--hop-mode", "1"]),
 ]
 
 

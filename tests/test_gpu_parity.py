@@ -115,11 +115,15 @@ def test_tiny_publish_pull_single_gpu(layout, N, C, tp):
     ctx.close()
 
 
-def test_tiny_three_versions_chain_on_one_gpu():
+HOP_MODES = [lam.LAM_HOP_KERNEL, lam.LAM_HOP_COPY_ENGINE]
+
+
+@pytest.mark.parametrize("hop_mode", HOP_MODES)
+def test_tiny_three_versions_chain_on_one_gpu(hop_mode):
     """Config 1: 1 actor, 2 relays, 2 rollouts TP=1, 3 versions — all on GPU 0 (stream-ordered hops)."""
     od = OMODELS["tiny"]
     C = 64 * 4096
-    ctx = make_ctx("tiny", 1, [0], [[0], [0]], [(1, 0), (2, 0)], C=C)
+    ctx = make_ctx("tiny", 1, [0], [[0], [0]], [(1, 0), (2, 0)], C=C, hop_mode=hop_mode)
     shard = ActorShard(MODELS["tiny"], 1, 0, 0)
     plan = image_plan([s for _, s in otensors(od)], 1, C)
     for v in (1, 2, 3):
@@ -136,14 +140,15 @@ def test_tiny_three_versions_chain_on_one_gpu():
     ctx.close()
 
 
-def test_tiny_chain_across_gpus():
+@pytest.mark.parametrize("hop_mode", HOP_MODES)
+def test_tiny_chain_across_gpus(hop_mode):
     n = ngpu()
     if n < 2:
         pytest.skip("needs >= 2 GPUs")
     od = OMODELS["tiny"]
     C = 16 * 4096
     relays = [[d] for d in range(1, n)]
-    ctx = make_ctx("tiny", 1, [0], relays, [(i + 1, i + 1) for i in range(n - 1)], C=C)
+    ctx = make_ctx("tiny", 1, [0], relays, [(i + 1, i + 1) for i in range(n - 1)], C=C, hop_mode=hop_mode)
     shard = ActorShard(MODELS["tiny"], 1, 0, 0)
     plan = image_plan([s for _, s in otensors(od)], 1, C)
     for v in (1, 2):
@@ -208,11 +213,12 @@ def test_version_rules_and_busy():
     ctx.close()
 
 
-def test_corrupt_chunk_is_never_committed():
+@pytest.mark.parametrize("hop_mode", HOP_MODES)
+def test_corrupt_chunk_is_never_committed(hop_mode):
     """A byte flipped in the master's slot after packing: the relay's checksum rejects the version,
     the relay keeps serving the previous one."""
     C = 16 * 4096
-    ctx = make_ctx("tiny", 1, [0], [[0]], [(1, 0)], C=C)
+    ctx = make_ctx("tiny", 1, [0], [[0]], [(1, 0)], C=C, hop_mode=hop_mode)
     shard = ActorShard(MODELS["tiny"], 1, 0, 0)
     publish_all(ctx, [shard], 1, False)
     until_idle(ctx)
