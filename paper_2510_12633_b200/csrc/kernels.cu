@@ -27,8 +27,10 @@ __device__ __forceinline__ uint4 ld_stream_v4(const void* p) {
                : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
   return v;
 }
+// streaming store (evict-first): every output of this path is written once and is far larger than
+// L2 (tools/hbm_bench.cu: +5-7 % on the pack's 2:1 read:write stream)
 __device__ __forceinline__ void st_v4(void* p, uint4 v) {
-  asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+  asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
                : "memory");
 }
 __device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
@@ -82,8 +84,40 @@ __device__ __forceinline__ void block_reduce2(uint64_t& a, uint64_t& b, uint64_t
   }
 }
 
+// Persistent grids: exactly one wave of resident CTAs (SMs x CTAs/SM the occupancy calculator
+// allows for this kernel's registers) — a partial second wave made k_pack 20 % slower.
+template <typename K>
+int resident_ctas(K kernel, int threads, size_t smem = 0) {
+  int dev = 0, sms = 148, per = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, threads, smem);
+  return sms * (per > 0 ? per : 1);
+}
+
 // ------------------------------------------------------------------------------------ k_pack
 constexpr int kPackThreads = 256;
+constexpr int kPackGroups = 4;
+
+// Add a CTA's share of chunk `g` (n units, checksum partial sums) into the header; the CTA that
+// completes the chunk publishes the header fields and releases the flag for the next relay.
+__device__ void pack_flush(ChunkMeta meta, const uint32_t* units_per_chunk, const uint64_t* chunk_len, uint32_t g,
+                           uint64_t s1, uint64_t s2, uint32_t n, uint64_t version, uint64_t n_total) {
+  lam_chunk_header* h = meta.hdr + g;
+  atomicAdd((unsigned long long*)&h->s1, (unsigned long long)s1);
+  atomicAdd((unsigned long long*)&h->s2, (unsigned long long)s2);
+  __threadfence_system();
+  const uint32_t prev = atomicAdd(meta.cnt + g, n);
+  if (prev + n == units_per_chunk[g]) {
+    __threadfence_system();
+    h->version = version;
+    h->idx = g;
+    h->n = n_total;
+    h->bytes = chunk_len[g];
+    __threadfence_system();
+    st_release_sys(meta.flags + g, version);
+  }
+}
 
 __global__ void __launch_bounds__(kPackThreads) k_pack(const PackUnit* __restrict__ units, uint32_t n_units,
                                                        const float* const* __restrict__ shard_ptrs,
@@ -92,24 +126,45 @@ __global__ void __launch_bounds__(kPackThreads) k_pack(const PackUnit* __restric
                                                        uint64_t version, uint64_t n_total,
                                                        const uint64_t* __restrict__ chunk_len) {
   __shared__ uint64_t red[2][kPackThreads / 32];
+  // Per-CTA accumulation: the CTA's checksum and unit count for its current chunk are flushed once
+  // when it moves on to another chunk (units are chunk-ordered), not per unit — the per-unit atomics
+  // on a handful of hot header addresses serialised in L2.
+  uint32_t cur = 0xFFFFFFFFu, acc_n = 0;
+  uint64_t acc1 = 0, acc2 = 0;
   for (uint32_t ui = blockIdx.x; ui < n_units; ui += gridDim.x) {
     const PackUnit u = units[ui];
+    if (u.chunk != cur) {                                   // uniform: every thread read the same unit
+      if (cur != 0xFFFFFFFFu) {
+        __threadfence_system();                             // this thread's stores of the finished chunk
+        __syncthreads();
+        if (threadIdx.x == 0) pack_flush(meta, units_per_chunk, chunk_len, cur, acc1, acc2, acc_n, version, n_total);
+      }
+      cur = u.chunk;
+      acc1 = acc2 = 0;
+      acc_n = 0;
+    }
     const float* src = shard_ptrs[u.shard] + u.src_elem;
     uint8_t* out = dst + u.dst_off;
     uint64_t s1 = 0, s2 = 0;
     const uint32_t nvec = u.n >> 3;  // groups of 8 elements = 32 B in, 16 B out
     if ((((uintptr_t)src) & 15) == 0) {
       uint32_t v = threadIdx.x;
-      for (; v + kPackThreads < nvec; v += 2 * kPackThreads) {  // 2 groups in flight per thread
-        const uint4 a0 = ld_stream_v4(src + 8 * (size_t)v), b0 = ld_stream_v4(src + 8 * (size_t)v + 4);
-        const uint32_t v1 = v + kPackThreads;
-        const uint4 a1 = ld_stream_v4(src + 8 * (size_t)v1), b1 = ld_stream_v4(src + 8 * (size_t)v1 + 4);
-        const uint4 w0 = make_uint4(pack2(a0.x, a0.y), pack2(a0.z, a0.w), pack2(b0.x, b0.y), pack2(b0.z, b0.w));
-        const uint4 w1 = make_uint4(pack2(a1.x, a1.y), pack2(a1.z, a1.w), pack2(b1.x, b1.y), pack2(b1.z, b1.w));
-        st_v4(out + 16 * (size_t)v, w0);
-        st_v4(out + 16 * (size_t)v1, w1);
-        cks4((uint64_t)u.word0 + 4ull * v, w0, s1, s2);
-        cks4((uint64_t)u.word0 + 4ull * v1, w1, s1, s2);
+      constexpr int G = kPackGroups;  // groups of 8 elements in flight per thread (G x 32 B of loads)
+      for (; v + (G - 1) * kPackThreads < nvec; v += G * kPackThreads) {
+        uint4 a[G], b[G];
+#pragma unroll
+        for (int k = 0; k < G; ++k) {
+          a[k] = ld_stream_v4(src + 8 * (size_t)(v + k * kPackThreads));
+          b[k] = ld_stream_v4(src + 8 * (size_t)(v + k * kPackThreads) + 4);
+        }
+#pragma unroll
+        for (int k = 0; k < G; ++k) {
+          const uint32_t vk = v + k * kPackThreads;
+          const uint4 w = make_uint4(pack2(a[k].x, a[k].y), pack2(a[k].z, a[k].w), pack2(b[k].x, b[k].y),
+                                     pack2(b[k].z, b[k].w));
+          st_v4(out + 16 * (size_t)vk, w);
+          cks4((uint64_t)u.word0 + 4ull * vk, w, s1, s2);
+        }
       }
       for (; v < nvec; v += kPackThreads) {
         const uint4 a = ld_stream_v4(src + 8 * (size_t)v), b = ld_stream_v4(src + 8 * (size_t)v + 4);
@@ -140,25 +195,14 @@ __global__ void __launch_bounds__(kPackThreads) k_pack(const PackUnit* __restric
         s2 += ((uint64_t)u.word0 + e / 2 + 1) * w;
       }
     }
-    __threadfence_system();  // this thread's image stores before the chunk's completion count
     block_reduce2<kPackThreads>(s1, s2, red);
-    if (threadIdx.x == 0) {
-      lam_chunk_header* h = meta.hdr + u.chunk;
-      atomicAdd((unsigned long long*)&h->s1, (unsigned long long)s1);
-      atomicAdd((unsigned long long*)&h->s2, (unsigned long long)s2);
-      __threadfence_system();
-      const uint32_t prev = atomicAdd(meta.cnt + u.chunk, 1u);
-      if (prev + 1 == units_per_chunk[u.chunk]) {  // last unit of the chunk: publish it
-        __threadfence_system();
-        h->version = version;
-        h->idx = u.chunk;
-        h->n = n_total;
-        h->bytes = chunk_len[u.chunk];
-        __threadfence_system();
-        st_release_sys(meta.flags + u.chunk, version);
-      }
-    }
+    if (threadIdx.x == 0) { acc1 += s1; acc2 += s2; ++acc_n; }
     __syncthreads();  // red[] reuse
+  }
+  if (cur != 0xFFFFFFFFu) {
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) pack_flush(meta, units_per_chunk, chunk_len, cur, acc1, acc2, acc_n, version, n_total);
   }
 }
 
@@ -166,6 +210,7 @@ int launch_pack(const PackUnit* units, uint32_t n_units, const float* const* sha
                 ChunkMeta meta, const uint32_t* units_per_chunk, uint64_t version, uint64_t n_total,
                 const uint64_t* chunk_len, int ctas, void* stream) {
   if (n_units == 0) return 0;
+  if (ctas <= 0) ctas = resident_ctas(k_pack, kPackThreads);
   unsigned grid = (unsigned)(n_units < (uint32_t)ctas ? n_units : (uint32_t)ctas);
   k_pack<<<grid, kPackThreads, 0, (cudaStream_t)stream>>>(units, n_units, shard_ptrs, dst, meta,
                                                           units_per_chunk, version, n_total, chunk_len);
@@ -241,6 +286,7 @@ __global__ void __launch_bounds__(kPullThreads) k_pull(const CopyTile* __restric
 
 int launch_pull(const CopyTile* tiles, uint32_t n_tiles, const uint8_t* const* rank_base, int ctas, void* stream) {
   if (n_tiles == 0) return 0;
+  if (ctas <= 0) ctas = resident_ctas(k_pull, kPullThreads);
   unsigned grid = (unsigned)(n_tiles < (uint32_t)ctas ? n_tiles : (uint32_t)ctas);
   k_pull<<<grid, kPullThreads, 0, (cudaStream_t)stream>>>(tiles, n_tiles, rank_base);
   return (int)cudaGetLastError();

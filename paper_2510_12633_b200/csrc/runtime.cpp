@@ -845,9 +845,9 @@ extern "C" lam_status lam_init(const lam_config* cfg, lam_ctx** out) {
   if (!build_image_plan(c->ts, cfg->fsdp_size, cfg->actor_layout, C, &c->plan)) return LAM_EINVAL;
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  c->pack_ctas = cfg->pack_ctas > 0 ? cfg->pack_ctas : sms * 6;
+  c->pack_ctas = cfg->pack_ctas > 0 ? cfg->pack_ctas : 0;  // 0: one resident wave (occupancy API)
   c->hop_ctas = cfg->hop_ctas > 0 ? cfg->hop_ctas : 32;  // TMA hop: ~785 GB/s at 32 CTAs
-  c->pull_ctas = cfg->pull_ctas > 0 ? cfg->pull_ctas : sms * 4;
+  c->pull_ctas = cfg->pull_ctas > 0 ? cfg->pull_ctas : 0;
   if (cfg->spin_timeout_s > 0) c->timeout_ns = (uint64_t)(cfg->spin_timeout_s * 1e9);
   c->pubs.resize(cfg->fsdp_size);
   st = setup_shm(c.get());
