@@ -267,6 +267,25 @@ typedef struct {
 int64_t lam_plan_copy_tiles(const lam_model_dims*, int32_t actor_layout, int32_t fsdp_size, uint64_t chunk_bytes,
                             const lam_tp_layout*, lam_copy_tile_info* out, int64_t cap);
 
+/* ---- control plane (host-only; no GPU) ------------------------------------------------- */
+/* The version-table state machine the runtime runs under its cross-process lock, exposed so the
+ * CPU test-suite can drive it from several processes.  `name` = POSIX shm name ("" = private heap
+ * block); create = 1 for the creating process.  States: 0 FREE, 1 FILLING, 2 COMPLETE.
+ * Semantics: PAPER L548-550, L652-670; SPEC L546-547, L633, L638, L643, L661 (see control.h). */
+typedef struct lam_ctl lam_ctl;
+lam_ctl* lam_ctl_open(const char* name, int32_t create, int32_t n_nodes, int32_t slots, int32_t fsdp_size);
+void lam_ctl_close(lam_ctl*);
+lam_status lam_ctl_publish(lam_ctl*, uint64_t version, int32_t rank, int32_t* slot);  /* ESTALE, EBUSY */
+int32_t lam_ctl_pack_done(lam_ctl*, int32_t slot, uint64_t version);                  /* 1 = changed */
+int32_t lam_ctl_start(lam_ctl*, int32_t node, uint64_t* version, int32_t* started);   /* FILLING slot / -1 */
+int32_t lam_ctl_part_done(lam_ctl*, int32_t node, int32_t slot, uint64_t version, int32_t n_parts,
+                          lam_status err);
+uint64_t lam_ctl_pin(lam_ctl*, int32_t node, int32_t* slot);                           /* 0 = none */
+void lam_ctl_unpin(lam_ctl*, int32_t node, int32_t slot);
+uint64_t lam_ctl_latest(lam_ctl*, int32_t node);
+int32_t lam_ctl_busy(lam_ctl*);
+lam_status lam_ctl_slot(lam_ctl*, int32_t node, int32_t slot, uint64_t* version, int32_t* state, int32_t* readers);
+
 /* Appendix D: chunk count k = clamp(round(sqrt((p-2) M T_byte / T_start)),
  * 1, k_cap); and T(p, k) = (p + k - 2)(M/k T_byte + T_start). */
 int64_t lam_optimal_chunks(int32_t p, double M, double t_byte, double t_start, int64_t k_cap);

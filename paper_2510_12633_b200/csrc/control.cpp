@@ -1,0 +1,345 @@
+// Control plane of the relay tier (see control.h): version table state machine + shared memory.
+// Host-only C++ — no CUDA — so that the CPU test-suite can drive it from several processes.
+#include "control.h"
+
+#include <errno.h>
+#include <fcntl.h>
+#include <stdio.h>
+#include <string.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <new>
+
+namespace lam {
+
+ShmLock::ShmLock(Shm* s) : m(&s->mu) {
+  int rc = pthread_mutex_lock(m);
+  if (rc == EOWNERDEAD) pthread_mutex_consistent(m);  // a rank died holding it: state is per-field valid
+}
+ShmLock::~ShmLock() { pthread_mutex_unlock(m); }
+
+static void init_mutex(Shm* s, bool shared) {
+  pthread_mutexattr_t a;
+  pthread_mutexattr_init(&a);
+  pthread_mutexattr_settype(&a, PTHREAD_MUTEX_RECURSIVE);
+  if (shared) {
+    pthread_mutexattr_setpshared(&a, PTHREAD_PROCESS_SHARED);
+    pthread_mutexattr_setrobust(&a, PTHREAD_MUTEX_ROBUST);
+  }
+  pthread_mutex_init(&s->mu, &a);
+  pthread_mutexattr_destroy(&a);
+}
+
+Shm* shm_heap() {
+  Shm* s = new (std::nothrow) Shm();
+  if (!s) return nullptr;
+  memset(s, 0, sizeof(Shm));
+  init_mutex(s, false);
+  s->magic = kMagic;
+  return s;
+}
+
+Shm* shm_create(const char* name) {
+  char path[96];
+  snprintf(path, sizeof path, "/%s", name);
+  shm_unlink(path);
+  int fd = shm_open(path, O_CREAT | O_EXCL | O_RDWR, 0600);
+  if (fd < 0) return nullptr;
+  if (ftruncate(fd, sizeof(Shm)) != 0) {
+    close(fd);
+    return nullptr;
+  }
+  void* p = mmap(nullptr, sizeof(Shm), PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+  close(fd);
+  if (p == MAP_FAILED) return nullptr;
+  Shm* s = reinterpret_cast<Shm*>(p);
+  init_mutex(s, true);
+  __atomic_store_n(&s->magic, kMagic, __ATOMIC_RELEASE);  // attachers wait for this
+  return s;
+}
+
+Shm* shm_attach(const char* name) {
+  char path[96];
+  snprintf(path, sizeof path, "/%s", name);
+  int fd = -1;
+  for (int i = 0; i < 6000 && fd < 0; ++i) {
+    fd = shm_open(path, O_RDWR, 0600);
+    if (fd < 0) usleep(10000);
+  }
+  if (fd < 0) return nullptr;
+  struct stat st;
+  for (int i = 0; i < 6000; ++i) {
+    if (fstat(fd, &st) == 0 && (size_t)st.st_size >= sizeof(Shm)) break;
+    usleep(10000);
+  }
+  void* p = mmap(nullptr, sizeof(Shm), PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+  close(fd);
+  if (p == MAP_FAILED) return nullptr;
+  Shm* s = reinterpret_cast<Shm*>(p);
+  for (int i = 0; i < 6000 && __atomic_load_n(&s->magic, __ATOMIC_ACQUIRE) != kMagic; ++i) usleep(10000);
+  if (__atomic_load_n(&s->magic, __ATOMIC_ACQUIRE) != kMagic) {
+    munmap(p, sizeof(Shm));
+    return nullptr;
+  }
+  return s;
+}
+
+void shm_release(Shm* s, const char* name, bool mapped, bool owner) {
+  if (!s) return;
+  if (mapped) {
+    munmap(s, sizeof(Shm));
+    if (owner) {
+      char path[96];
+      snprintf(path, sizeof path, "/%s", name);
+      shm_unlink(path);
+    }
+  } else {
+    pthread_mutex_destroy(&s->mu);
+    delete s;
+  }
+}
+
+namespace ctl {
+
+int find_slot(const ShmNode& n, int S, uint64_t v, int32_t state) {
+  for (int i = 0; i < S; ++i)
+    if (n.slot[i].version == v && n.slot[i].state == state) return i;
+  return -1;
+}
+
+int acquire_slot(const ShmNode& n, int S) {
+  for (int i = 0; i < S; ++i)
+    if (n.slot[i].state == S_FREE && n.slot[i].readers == 0) return i;
+  for (int i = 0; i < S; ++i)
+    if (n.slot[i].state == S_COMPLETE && n.slot[i].readers == 0 && n.slot[i].version != n.latest) return i;
+  return -1;
+}
+
+uint64_t newest_held(const ShmNode& n, int S, int* slot) {
+  uint64_t best = 0;
+  *slot = -1;
+  for (int i = 0; i < S; ++i)
+    if ((n.slot[i].state == S_FILLING || n.slot[i].state == S_COMPLETE) && n.slot[i].version > best) {
+      best = n.slot[i].version;
+      *slot = i;
+    }
+  return best;
+}
+
+static void open_slot(ShmSlot& sl, uint64_t v, int src_slot) {
+  sl.version = v;
+  sl.state = S_FILLING;
+  sl.readers = 0;
+  sl.parts_done = sl.parts_finished = 0;
+  sl.err = 0;
+  sl.src_slot = src_slot;
+  sl.launched_mask = 0;
+}
+
+lam_status publish(Shm* sh, int S, int fsdp, uint64_t v, int rank, int* slot) {
+  ShmNode& n0 = sh->node[0];
+  if (v == 0 || v < sh->last_published) return LAM_ESTALE;
+  int s;
+  if (v == sh->last_published) {             // another rank already opened v: join it
+    s = find_slot(n0, S, v, S_FILLING);
+    if (s < 0 || (n0.slot[s].launched_mask >> rank & 1ull)) return LAM_ESTALE;
+  } else {
+    const uint64_t all = fsdp == 64 ? ~0ull : ((1ull << fsdp) - 1);
+    for (int i = 0; i < S; ++i)                // the previous version still waits for some ranks
+      if (n0.slot[i].state == S_FILLING && n0.slot[i].launched_mask != all) return LAM_EBUSY;
+    s = acquire_slot(n0, S);
+    if (s < 0) {
+      sh->stats.publish_busy++;
+      return LAM_EBUSY;
+    }
+    open_slot(n0.slot[s], v, -1);
+    sh->last_published = v;
+    n0.started = v;
+    sh->stats.publishes++;
+  }
+  n0.slot[s].launched_mask |= 1ull << rank;
+  *slot = s;
+  return LAM_OK;
+}
+
+bool pack_done(Shm* sh, int fsdp, int slot, uint64_t v) {
+  ShmSlot& sl = sh->node[0].slot[slot];
+  if (sl.version != v || sl.state != S_FILLING) return false;
+  if (++sl.parts_done == fsdp) {
+    sl.state = S_COMPLETE;
+    if (v > sh->node[0].latest) sh->node[0].latest = v;
+  }
+  return true;
+}
+
+int start(Shm* sh, int S, int node, bool* started) {
+  *started = false;
+  ShmNode& n = sh->node[node];
+  ShmNode& pred = sh->node[node - 1];
+  for (int s = 0; s < S; ++s)
+    if (n.slot[s].state == S_FILLING) return s;
+  int ps = -1;
+  const uint64_t u = newest_held(pred, S, &ps);
+  if (u <= n.started) return -1;
+  const int s = acquire_slot(n, S);
+  if (s < 0) return -1;
+  if (n.started && u > n.started + 1) {
+    n.skipped += u - n.started - 1;
+    sh->stats.versions_skipped += u - n.started - 1;
+  }
+  open_slot(n.slot[s], u, ps);
+  pred.slot[ps].readers++;
+  n.started = u;
+  *started = true;
+  return s;
+}
+
+bool part_done(Shm* sh, int node, int slot, uint64_t v, int n_parts, lam_status err) {
+  ShmNode& n = sh->node[node];
+  ShmSlot& sl = n.slot[slot];
+  if (sl.version != v || sl.state != S_FILLING) return false;
+  sl.parts_finished++;
+  if (err != LAM_OK) {
+    if (!sl.err) sl.err = err;
+    if (err == LAM_ETIMEOUT) sh->stats.timeouts++; else sh->stats.checksum_errors++;
+  } else {
+    sl.parts_done++;
+  }
+  if (sl.parts_finished == n_parts) {
+    if (sl.src_slot >= 0) {
+      ShmSlot& src = sh->node[node - 1].slot[sl.src_slot];
+      if (src.readers > 0) src.readers--;
+    }
+    if (sl.err == 0) {
+      sl.state = S_COMPLETE;
+      if (v > n.latest) n.latest = v;
+    } else {
+      sl.state = S_FREE;                       // never committed: keep serving the previous version
+      sl.version = 0;
+    }
+    sl.src_slot = -1;
+  }
+  return true;
+}
+
+uint64_t pin_latest(Shm* sh, int S, int node, int* slot) {
+  ShmNode& n = sh->node[node];
+  *slot = -1;
+  if (n.latest == 0) return 0;
+  const int s = find_slot(n, S, n.latest, S_COMPLETE);
+  if (s < 0) return 0;
+  n.slot[s].readers++;
+  *slot = s;
+  return n.latest;
+}
+
+void unpin(Shm* sh, int node, int slot) {
+  ShmSlot& sl = sh->node[node].slot[slot];
+  if (sl.readers > 0) sl.readers--;
+}
+
+bool busy(Shm* sh, int S, int n_nodes) {
+  for (int node = 0; node < n_nodes; ++node) {
+    for (int s = 0; s < S; ++s)
+      if (sh->node[node].slot[s].state == S_FILLING) return true;
+    int ps;
+    if (node > 0 && newest_held(sh->node[node - 1], S, &ps) > sh->node[node].started) return true;
+  }
+  return false;
+}
+
+}  // namespace ctl
+}  // namespace lam
+
+// ------------------------------------------------------------------ C entry points (CPU tests)
+using namespace lam;
+
+struct lam_ctl {
+  Shm* sh;
+  int S, fsdp, n_nodes;
+  bool mapped, owner;
+  char name[64];
+};
+
+extern "C" lam_ctl* lam_ctl_open(const char* name, int32_t create, int32_t n_nodes, int32_t slots, int32_t fsdp) {
+  if (n_nodes < 1 || n_nodes > LAM_MAX_NODES + 1 || slots < 2 || slots > LAM_MAX_SLOTS || fsdp < 1 ||
+      fsdp > LAM_MAX_RANKS)
+    return nullptr;
+  lam_ctl* c = new (std::nothrow) lam_ctl();
+  if (!c) return nullptr;
+  c->S = slots;
+  c->fsdp = fsdp;
+  c->n_nodes = n_nodes;
+  snprintf(c->name, sizeof c->name, "%s", name ? name : "");
+  c->mapped = name && name[0];
+  c->owner = create != 0;
+  c->sh = !c->mapped ? shm_heap() : (create ? shm_create(name) : shm_attach(name));
+  if (!c->sh) {
+    delete c;
+    return nullptr;
+  }
+  return c;
+}
+
+extern "C" void lam_ctl_close(lam_ctl* c) {
+  if (!c) return;
+  shm_release(c->sh, c->name, c->mapped, c->owner);
+  delete c;
+}
+
+extern "C" lam_status lam_ctl_publish(lam_ctl* c, uint64_t v, int32_t rank, int32_t* slot) {
+  ShmLock l(c->sh);
+  return ctl::publish(c->sh, c->S, c->fsdp, v, rank, slot);
+}
+
+extern "C" int32_t lam_ctl_pack_done(lam_ctl* c, int32_t slot, uint64_t v) {
+  ShmLock l(c->sh);
+  return ctl::pack_done(c->sh, c->fsdp, slot, v);
+}
+
+extern "C" int32_t lam_ctl_start(lam_ctl* c, int32_t node, uint64_t* version, int32_t* started) {
+  ShmLock l(c->sh);
+  bool st = false;
+  int s = ctl::start(c->sh, c->S, node, &st);
+  *version = s >= 0 ? c->sh->node[node].slot[s].version : 0;
+  *started = st;
+  return s;
+}
+
+extern "C" int32_t lam_ctl_part_done(lam_ctl* c, int32_t node, int32_t slot, uint64_t v, int32_t n_parts,
+                                     lam_status err) {
+  ShmLock l(c->sh);
+  return ctl::part_done(c->sh, node, slot, v, n_parts, err);
+}
+
+extern "C" uint64_t lam_ctl_pin(lam_ctl* c, int32_t node, int32_t* slot) {
+  ShmLock l(c->sh);
+  return ctl::pin_latest(c->sh, c->S, node, slot);
+}
+
+extern "C" void lam_ctl_unpin(lam_ctl* c, int32_t node, int32_t slot) {
+  ShmLock l(c->sh);
+  ctl::unpin(c->sh, node, slot);
+}
+
+extern "C" uint64_t lam_ctl_latest(lam_ctl* c, int32_t node) {
+  ShmLock l(c->sh);
+  return c->sh->node[node].latest;
+}
+
+extern "C" int32_t lam_ctl_busy(lam_ctl* c) {
+  ShmLock l(c->sh);
+  return ctl::busy(c->sh, c->S, c->n_nodes);
+}
+
+extern "C" lam_status lam_ctl_slot(lam_ctl* c, int32_t node, int32_t slot, uint64_t* version, int32_t* state,
+                                   int32_t* readers) {
+  ShmLock l(c->sh);
+  const ShmSlot& s = c->sh->node[node].slot[slot];
+  *version = s.version;
+  *state = s.state;
+  *readers = s.readers;
+  return LAM_OK;
+}

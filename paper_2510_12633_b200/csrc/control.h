@@ -1,0 +1,78 @@
+// Control plane of the relay tier: the version table and its state machine, with no CUDA in it.
+//
+// PAPER L548-550 (steps 5-7), L652-670 (§4.2); SPEC L527-663 (relay semantics):
+//   * every node has S ring slots, FREE -> FILLING(v) -> COMPLETE(v);
+//   * node 0 is the master (the actor's publish slots); a version is COMPLETE there when all FSDP
+//     ranks packed it;
+//   * a relay starts receiving the NEWEST version its predecessor holds (FILLING or COMPLETE; this is
+//     what pipelines the chain) into a FREE slot or a COMPLETE slot with no readers that is not its
+//     latest (latest-wins: versions may be skipped, never reordered), pinning the predecessor's slot;
+//   * `latest` only moves up, and only to COMPLETE versions (SPEC L633 complete-only, L638 monotone);
+//   * a corrupt chunk frees the slot without committing it.
+// The block lives in POSIX shared memory when there is one process per GPU, behind a robust
+// process-shared mutex.  The runtime (runtime.cpp) calls these functions under that mutex; the
+// lam_ctl_* C entry points expose them to the CPU test-suite (multi-process, gloo).
+#pragma once
+#include <pthread.h>
+#include <stdint.h>
+
+#include "../../include/lam.h"
+
+namespace lam {
+
+enum : int32_t { S_FREE = 0, S_FILLING = 1, S_COMPLETE = 2 };
+
+struct ShmSlot {
+  uint64_t version;
+  int32_t state, readers;
+  int32_t parts_done, parts_finished;  // node 0: ranks packed; relays: parts completed ok / at all
+  int32_t err, src_slot;               // first error; predecessor slot pinned while FILLING
+  uint64_t launched_mask;              // node 0: ranks published; relays: parts launched
+};
+struct ShmNode {
+  ShmSlot slot[LAM_MAX_SLOTS];
+  uint64_t latest, started, skipped;
+};
+struct Shm {
+  uint64_t magic;
+  pthread_mutex_t mu;
+  uint64_t last_published;
+  int32_t ready_procs;
+  lam_stats stats;
+  ShmNode node[LAM_MAX_NODES + 1];
+};
+constexpr uint64_t kMagic = 0x4c414d5f53484d32ull;  // "LAM_SHM2"
+
+struct ShmLock {
+  pthread_mutex_t* m;
+  explicit ShmLock(Shm* s);
+  ~ShmLock();
+};
+
+// Shared-memory block: create (owner), attach (waits up to ~60 s), or heap (single process).
+Shm* shm_create(const char* name);
+Shm* shm_attach(const char* name);
+Shm* shm_heap();
+void shm_release(Shm* s, const char* name, bool mapped, bool owner);
+
+namespace ctl {
+int find_slot(const ShmNode& n, int S, uint64_t v, int32_t state);
+int acquire_slot(const ShmNode& n, int S);
+uint64_t newest_held(const ShmNode& n, int S, int* slot);
+// Actor rank `rank` publishes v at node 0 (joins v if another rank opened it).  *slot = its slot.
+lam_status publish(Shm* sh, int S, int fsdp, uint64_t v, int rank, int* slot);
+// One rank's pack of v in `slot` finished; returns true on a state change.
+bool pack_done(Shm* sh, int fsdp, int slot, uint64_t v);
+// Node `node` (>= 1): begin the newest version its predecessor holds if possible.  Returns the
+// FILLING slot (new or already open) or -1; *started = true if this call opened it.
+int start(Shm* sh, int S, int node, bool* started);
+// One part of `node` finished v in `slot` (err = 0 or a LAM_E* code); returns true on a change.
+bool part_done(Shm* sh, int node, int slot, uint64_t v, int n_parts, lam_status err);
+// Pull side: pin the latest COMPLETE slot (0 if none) / release it.
+uint64_t pin_latest(Shm* sh, int S, int node, int* slot);
+void unpin(Shm* sh, int node, int slot);
+// Anything FILLING, or a node behind its predecessor?
+bool busy(Shm* sh, int S, int n_nodes);
+}  // namespace ctl
+
+}  // namespace lam

@@ -29,32 +29,14 @@
 #include <string>
 #include <vector>
 
+#include "control.h"
 #include "lam_internal.h"
 
 namespace lam {
 
-enum : int32_t { S_FREE = 0, S_FILLING = 1, S_COMPLETE = 2 };
-
-struct ShmSlot {
-  uint64_t version;
-  int32_t state, readers;
-  int32_t parts_done, parts_finished;  // node 0: ranks packed; relays: parts completed ok / at all
-  int32_t err, src_slot;               // first error; predecessor slot pinned while FILLING
-  uint64_t launched_mask;              // node 0: ranks published; relays: parts launched
-};
-struct ShmNode {
-  ShmSlot slot[LAM_MAX_SLOTS];
-  uint64_t latest, started, skipped;
-};
-struct Shm {
-  uint64_t magic;
-  pthread_mutex_t mu;
-  uint64_t last_published;
-  int32_t ready_procs;
-  lam_stats stats;
-  ShmNode node[LAM_MAX_NODES + 1];
-};
-constexpr uint64_t kMagic = 0x4c414d5f53484d31ull;  // "LAM_SHM1"
+using ctl::acquire_slot;
+using ctl::find_slot;
+using ctl::newest_held;
 
 struct SlotMeta {   // byte offsets inside a slot's metadata block
   uint64_t flags, hdr, cnt, abort, bytes;
@@ -152,14 +134,7 @@ struct lam_ctx {
 
 namespace {
 
-struct Lock {
-  pthread_mutex_t* m;
-  explicit Lock(Shm* s) : m(&s->mu) {
-    int rc = pthread_mutex_lock(m);
-    if (rc == EOWNERDEAD) pthread_mutex_consistent(m);
-  }
-  ~Lock() { pthread_mutex_unlock(m); }
-};
+using Lock = ShmLock;
 
 bool owns(const lam_ctx* c, int device) {
   return device >= 0 && device < LAM_MAX_DEVICES && c->cfg.proc_of_device[device] == c->cfg.proc_rank;
@@ -221,31 +196,6 @@ ChunkMeta meta_of(const lam_ctx* c, const Part& p, int slot) {
 
 uint8_t* slot_data(const Part& p, int slot) { return p.base + (uint64_t)slot * p.slot_stride; }
 
-int find_slot(const ShmNode& n, int S, uint64_t v, int32_t state) {
-  for (int i = 0; i < S; ++i)
-    if (n.slot[i].version == v && n.slot[i].state == state) return i;
-  return -1;
-}
-
-int acquire_slot(const ShmNode& n, int S) {
-  for (int i = 0; i < S; ++i)
-    if (n.slot[i].state == S_FREE && n.slot[i].readers == 0) return i;
-  for (int i = 0; i < S; ++i)
-    if (n.slot[i].state == S_COMPLETE && n.slot[i].readers == 0 && n.slot[i].version != n.latest) return i;
-  return -1;
-}
-
-uint64_t newest_held(const ShmNode& n, int S, int* slot) {
-  uint64_t best = 0;
-  *slot = -1;
-  for (int i = 0; i < S; ++i)
-    if ((n.slot[i].state == S_FILLING || n.slot[i].state == S_COMPLETE) && n.slot[i].version > best) {
-      best = n.slot[i].version;
-      *slot = i;
-    }
-  return best;
-}
-
 lam_status validate(const lam_config& c, std::string* why) {
   auto bad = [&](const std::string& s) { *why = s; return LAM_EINVAL; };
   if (!model_valid(c.model)) return bad("model dims");
@@ -272,53 +222,13 @@ lam_status validate(const lam_config& c, std::string* why) {
 
 lam_status setup_shm(lam_ctx* c) {
   if (c->cfg.n_procs == 1) {
-    c->shm = new Shm();
-    memset(c->shm, 0, sizeof(Shm));
-    pthread_mutexattr_t a;
-    pthread_mutexattr_init(&a);
-    pthread_mutexattr_settype(&a, PTHREAD_MUTEX_RECURSIVE);
-    pthread_mutex_init(&c->shm->mu, &a);
-    c->shm->magic = kMagic;
-    return LAM_OK;
+    c->shm = shm_heap();
+    return c->shm ? LAM_OK : LAM_ENOMEM;
   }
-  char name[80];
-  snprintf(name, sizeof name, "/%s", c->cfg.shm_name);
-  int fd = -1;
-  if (c->cfg.proc_rank == 0) {
-    shm_unlink(name);
-    fd = shm_open(name, O_CREAT | O_EXCL | O_RDWR, 0600);
-    if (fd < 0 || ftruncate(fd, sizeof(Shm)) != 0) return LAM_EIPC;
-    c->shm_owner = true;
-  } else {
-    for (int i = 0; i < 6000 && fd < 0; ++i) {
-      fd = shm_open(name, O_RDWR, 0600);
-      if (fd < 0) usleep(10000);
-    }
-    if (fd < 0) return LAM_EIPC;
-    struct stat st;
-    for (int i = 0; i < 6000; ++i) {
-      if (fstat(fd, &st) == 0 && (size_t)st.st_size >= sizeof(Shm)) break;
-      usleep(10000);
-    }
-  }
-  void* p = mmap(nullptr, sizeof(Shm), PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
-  close(fd);
-  if (p == MAP_FAILED) return LAM_EIPC;
-  c->shm = reinterpret_cast<Shm*>(p);
-  c->shm_mapped = true;
-  if (c->cfg.proc_rank == 0) {
-    pthread_mutexattr_t a;
-    pthread_mutexattr_init(&a);
-    pthread_mutexattr_setpshared(&a, PTHREAD_PROCESS_SHARED);
-    pthread_mutexattr_setrobust(&a, PTHREAD_MUTEX_ROBUST);
-    pthread_mutexattr_settype(&a, PTHREAD_MUTEX_RECURSIVE);
-    pthread_mutex_init(&c->shm->mu, &a);
-    __atomic_store_n(&c->shm->magic, kMagic, __ATOMIC_RELEASE);
-  } else {
-    for (int i = 0; i < 6000 && __atomic_load_n(&c->shm->magic, __ATOMIC_ACQUIRE) != kMagic; ++i) usleep(10000);
-    if (__atomic_load_n(&c->shm->magic, __ATOMIC_ACQUIRE) != kMagic) return LAM_EIPC;
-  }
-  return LAM_OK;
+  c->shm_owner = c->cfg.proc_rank == 0;
+  c->shm = c->shm_owner ? shm_create(c->cfg.shm_name) : shm_attach(c->cfg.shm_name);
+  c->shm_mapped = c->shm != nullptr;
+  return c->shm ? LAM_OK : LAM_EIPC;
 }
 
 lam_status alloc_parts(lam_ctx* c) {
@@ -623,15 +533,7 @@ lam_status step_locked(lam_ctx* c, int* transitions, bool* busy) {
       cudaError_t q = cudaEventQuery(rp.ev[s]);
       if (q == cudaErrorNotReady) { *busy = true; continue; }
       if (q != cudaSuccess) return LAM_ECUDA;
-      ShmSlot& sl = sh->node[0].slot[s];
-      if (sl.version == rp.inflight_version[s] && sl.state == S_FILLING) {
-        sl.parts_done++;
-        if (sl.parts_done == c->cfg.fsdp_size) {
-          sl.state = S_COMPLETE;
-          if (sl.version > sh->node[0].latest) sh->node[0].latest = sl.version;
-        }
-        (*transitions)++;
-      }
+      if (ctl::pack_done(sh, c->cfg.fsdp_size, s, rp.inflight_version[s])) (*transitions)++;
       rp.inflight_version[s] = 0;
     }
   }
@@ -648,33 +550,10 @@ lam_status step_locked(lam_ctx* c, int* transitions, bool* busy) {
       cudaError_t q = cudaEventQuery(p.done_ev[s]);
       if (q == cudaErrorNotReady) { *busy = true; continue; }
       if (q != cudaSuccess) return LAM_ECUDA;
-      ShmNode& n = sh->node[p.node];
-      ShmSlot& sl = n.slot[s];
-      uint32_t err = p.err_host[s];
-      if (sl.version == p.inflight_version[s] && sl.state == S_FILLING) {
-        sl.parts_finished++;
-        if (err) {
-          lam_status e = -(lam_status)err;
-          if (!sl.err) sl.err = e;
-          if (e == LAM_ETIMEOUT) sh->stats.timeouts++; else sh->stats.checksum_errors++;
-          if (first_err == LAM_OK) first_err = e;
-        } else {
-          sl.parts_done++;
-        }
-        const int np = (int)c->node_parts[p.node].size();
-        if (sl.parts_finished == np) {
-          ShmSlot& src = sh->node[p.node - 1].slot[sl.src_slot];
-          if (src.readers > 0) src.readers--;
-          if (sl.err == 0) {
-            sl.state = S_COMPLETE;
-            if (sl.version > n.latest) n.latest = sl.version;
-          } else {
-            sl.state = S_FREE;  // never committed: keep serving the previous version
-            sl.version = 0;
-          }
-          sl.src_slot = -1;
-        }
+      const lam_status e = p.err_host[s] ? -(lam_status)p.err_host[s] : LAM_OK;
+      if (ctl::part_done(sh, p.node, s, p.inflight_version[s], (int)c->node_parts[p.node].size(), e)) {
         (*transitions)++;
+        if (e != LAM_OK && first_err == LAM_OK) first_err = e;
       }
       p.inflight_version[s] = 0;
     }
@@ -684,8 +563,7 @@ lam_status step_locked(lam_ctx* c, int* transitions, bool* busy) {
     cudaError_t q = cudaEventQuery(c->pending[i].ev);
     if (q == cudaErrorNotReady) { *busy = true; ++i; continue; }
     if (q != cudaSuccess) return LAM_ECUDA;
-    ShmSlot& sl = sh->node[c->pending[i].node].slot[c->pending[i].slot];
-    if (sl.readers > 0) sl.readers--;
+    ctl::unpin(sh, c->pending[i].node, c->pending[i].slot);
     c->ev_pool[c->pending[i].device].push_back(c->pending[i].ev);
     c->pending[i] = c->pending.back();
     c->pending.pop_back();
@@ -694,35 +572,9 @@ lam_status step_locked(lam_ctx* c, int* transitions, bool* busy) {
   // (4) start new versions (latest-wins) and launch local parts
   for (int node = 1; node < c->n_nodes; ++node) {
     ShmNode& n = sh->node[node];
-    ShmNode& pred = sh->node[node - 1];
-    int fill = -1;
-    for (int s = 0; s < S; ++s)
-      if (n.slot[s].state == S_FILLING) fill = s;
-    if (fill < 0) {
-      int ps = -1;
-      uint64_t u = newest_held(pred, S, &ps);
-      if (u > n.started) {
-        int s = acquire_slot(n, S);
-        if (s >= 0) {
-          if (n.started && u > n.started + 1) {
-            n.skipped += u - n.started - 1;
-            sh->stats.versions_skipped += u - n.started - 1;
-          }
-          ShmSlot& sl = n.slot[s];
-          sl.version = u;
-          sl.state = S_FILLING;
-          sl.readers = 0;
-          sl.parts_done = sl.parts_finished = 0;
-          sl.err = 0;
-          sl.src_slot = ps;
-          sl.launched_mask = 0;
-          pred.slot[ps].readers++;
-          n.started = u;
-          fill = s;
-          (*transitions)++;
-        }
-      }
-    }
+    bool opened = false;
+    const int fill = ctl::start(sh, S, node, &opened);
+    if (opened) (*transitions)++;
     if (fill >= 0) {
       for (int pi : c->node_parts[node]) {
         Part& p = c->parts[pi];
@@ -735,14 +587,7 @@ lam_status step_locked(lam_ctx* c, int* transitions, bool* busy) {
     }
   }
   // (5) anything still moving anywhere?
-  for (int node = 0; node < c->n_nodes && !*busy; ++node) {
-    for (int s = 0; s < S; ++s)
-      if (sh->node[node].slot[s].state == S_FILLING) *busy = true;
-    if (node > 0) {
-      int ps;
-      if (newest_held(sh->node[node - 1], S, &ps) > sh->node[node].started) *busy = true;
-    }
-  }
+  if (!*busy) *busy = ctl::busy(sh, S, c->n_nodes);
   return first_err;
 }
 
@@ -976,35 +821,9 @@ extern "C" lam_status lam_publish(lam_ctx* c, uint64_t v, int32_t rank, const la
   }
   Lock l(c->shm);
   Shm* sh = c->shm;
-  ShmNode& n0 = sh->node[0];
   int s = -1;
-  if (v < sh->last_published) return LAM_ESTALE;
-  if (v == sh->last_published) {
-    s = find_slot(n0, c->S, v, S_FILLING);
-    if (s < 0 || (n0.slot[s].launched_mask >> rank & 1ull)) return LAM_ESTALE;
-  } else {
-    for (int i = 0; i < c->S; ++i)  // previous version still waiting for some ranks: refuse
-      if (n0.slot[i].state == S_FILLING &&
-          n0.slot[i].launched_mask != ((c->cfg.fsdp_size == 64) ? ~0ull : ((1ull << c->cfg.fsdp_size) - 1)))
-        return LAM_EBUSY;
-    s = acquire_slot(n0, c->S);
-    if (s < 0) {
-      sh->stats.publish_busy++;
-      return LAM_EBUSY;
-    }
-    ShmSlot& sl = n0.slot[s];
-    sl.version = v;
-    sl.state = S_FILLING;
-    sl.readers = 0;
-    sl.parts_done = sl.parts_finished = 0;
-    sl.err = 0;
-    sl.src_slot = -1;
-    sl.launched_mask = 0;
-    sh->last_published = v;
-    n0.started = v;
-    sh->stats.publishes++;
-  }
-  n0.slot[s].launched_mask |= 1ull << rank;
+  lam_status pst = ctl::publish(sh, c->S, c->cfg.fsdp_size, v, rank, &s);
+  if (pst != LAM_OK) return pst;
   // enqueue: side stream waits for the work already on the actor stream, then packs
   cudaStream_t side = c->dev[dev].side;
   cudaEvent_t fork = get_event(c, dev);
@@ -1053,18 +872,18 @@ extern "C" lam_status lam_pull(lam_ctx* c, int32_t rid, const lam_tp_layout* L, 
   PullPlan* pp = nullptr;
   lam_status pst = get_plan(c, ro, *L, key, &pp);
   if (pst != LAM_OK) return pst;
-  ShmNode& n = c->shm->node[ro.node];
-  const uint64_t u = n.latest;
+  int s = -1;
+  const uint64_t u = ctl::pin_latest(c->shm, c->S, ro.node, &s);
   if (u == 0) return LAM_ENOVERSION;
-  const int s = find_slot(n, c->S, u, S_COMPLETE);
-  if (s < 0) return LAM_ECUDA;  // invariant broken
-  n.slot[s].readers++;
   auto rb = c->d_rank_base.find({ro.node * LAM_MAX_SLOTS + s, ro.device});
-  if (rb == c->d_rank_base.end()) return LAM_EINVAL;
+  if (rb == c->d_rank_base.end()) {
+    ctl::unpin(c->shm, ro.node, s);
+    return LAM_EINVAL;
+  }
   cudaEvent_t t0 = prof_begin(c, ro.device, (cudaStream_t)stream);
   int rc = launch_pull(pp->d_tiles, pp->n_tiles, rb->second, c->pull_ctas, stream);
   if (rc) {
-    n.slot[s].readers--;
+    ctl::unpin(c->shm, ro.node, s);
     fprintf(stderr, "liblam: pull launch failed: %s\n", cudaGetErrorString((cudaError_t)rc));
     return LAM_ECUDA;
   }
@@ -1251,18 +1070,6 @@ extern "C" void lam_destroy(lam_ctx* c) {
   for (auto& kv : c->tev_pool)
     for (cudaEvent_t e : kv.second) cudaEventDestroy(e);
   for (auto& t : c->timed) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }
-  if (c->shm) {
-    if (c->shm_mapped) {
-      munmap(c->shm, sizeof(Shm));
-      if (c->shm_owner) {
-        char name[80];
-        snprintf(name, sizeof name, "/%s", c->cfg.shm_name);
-        shm_unlink(name);
-      }
-    } else {
-      pthread_mutex_destroy(&c->shm->mu);
-      delete c->shm;
-    }
-  }
+  shm_release(c->shm, c->cfg.shm_name, c->shm_mapped, c->shm_owner);
   delete c;
 }

@@ -398,3 +398,64 @@ def optimal_chunks(p: int, M: float, t_byte: float, t_start: float, k_cap: int =
 
 def chain_latency(p: int, k: int, M: float, t_byte: float, t_start: float) -> float:
     return load().lam_chain_latency(p, k, M, t_byte, t_start)
+
+
+class Ctl:
+    """The control plane alone (lam_ctl_*; host-only, no GPU): the version-table state machine the
+    runtime uses, on a POSIX shared-memory block shared by several processes (name != "")."""
+
+    def __init__(self, name: str, create: bool, n_nodes: int, slots: int = 2, fsdp: int = 1):
+        L = self.L = load()
+        P, V, I32, U64 = C.POINTER, C.c_void_p, C.c_int32, C.c_uint64
+        for fn, res, args in [("lam_ctl_open", V, [C.c_char_p, I32, I32, I32, I32]), ("lam_ctl_close", None, [V]),
+                              ("lam_ctl_publish", I32, [V, U64, I32, P(I32)]), ("lam_ctl_pack_done", I32, [V, I32, U64]),
+                              ("lam_ctl_start", I32, [V, I32, P(U64), P(I32)]),
+                              ("lam_ctl_part_done", I32, [V, I32, I32, U64, I32, I32]),
+                              ("lam_ctl_pin", U64, [V, I32, P(I32)]), ("lam_ctl_unpin", None, [V, I32, I32]),
+                              ("lam_ctl_latest", U64, [V, I32]), ("lam_ctl_busy", I32, [V]),
+                              ("lam_ctl_slot", I32, [V, I32, I32, P(U64), P(I32), P(I32)])]:
+            f = getattr(L, fn)
+            f.restype, f.argtypes = res, args
+        self.h = L.lam_ctl_open(name.encode(), int(create), n_nodes, slots, fsdp)
+        if not self.h:
+            raise LamError(LAM_EIPC, "lam_ctl_open")
+
+    def publish(self, v: int, rank: int = 0):
+        s = C.c_int32(-1)
+        st = self.L.lam_ctl_publish(self.h, v, rank, C.byref(s))
+        return st, s.value
+
+    def pack_done(self, slot: int, v: int) -> bool:
+        return bool(self.L.lam_ctl_pack_done(self.h, slot, v))
+
+    def start(self, node: int):
+        v, st = C.c_uint64(), C.c_int32()
+        s = self.L.lam_ctl_start(self.h, node, C.byref(v), C.byref(st))
+        return s, v.value, bool(st.value)
+
+    def part_done(self, node: int, slot: int, v: int, n_parts: int = 1, err: int = LAM_OK) -> bool:
+        return bool(self.L.lam_ctl_part_done(self.h, node, slot, v, n_parts, err))
+
+    def pin(self, node: int):
+        s = C.c_int32(-1)
+        v = self.L.lam_ctl_pin(self.h, node, C.byref(s))
+        return v, s.value
+
+    def unpin(self, node: int, slot: int) -> None:
+        self.L.lam_ctl_unpin(self.h, node, slot)
+
+    def latest(self, node: int) -> int:
+        return self.L.lam_ctl_latest(self.h, node)
+
+    def busy(self) -> bool:
+        return bool(self.L.lam_ctl_busy(self.h))
+
+    def slot(self, node: int, slot: int):
+        v, st, rd = C.c_uint64(), C.c_int32(), C.c_int32()
+        self.L.lam_ctl_slot(self.h, node, slot, C.byref(v), C.byref(st), C.byref(rd))
+        return v.value, st.value, rd.value
+
+    def close(self) -> None:
+        if self.h:
+            self.L.lam_ctl_close(self.h)
+            self.h = None

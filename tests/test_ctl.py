@@ -1,0 +1,178 @@
+"""CPU tests of the relay control plane (liblam's lam_ctl_*: the version table the runtime drives).
+
+* Differential: seeded random publish / relay-round / pin / unpin interleavings give the same
+  per-node latest versions, skip counts and publish outcomes as the oracle's RelayChain model
+  (oracle/relay.py, PAPER L661-665 with one chunk per version: a hop completes within its round).
+* Multi-process (world_size 2, gloo): an actor process publishes while a relay process runs the
+  chain and pins/unpins, on one POSIX shared-memory block — the N>1 host path of the library.
+"""
+import os
+import random
+
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle.relay import RelayChain
+from paper_2510_12633_b200 import lam
+
+FREE, FILLING, COMPLETE = 0, 1, 2
+
+
+def _round(ctl: lam.Ctl, p: int):
+    """One oracle round with k = 1: hops in tail-to-head order, each starts and completes a version."""
+    for node in range(p - 1, 0, -1):
+        s, v, opened = ctl.start(node)
+        if s >= 0:
+            assert ctl.part_done(node, s, v, 1, lam.LAM_OK)
+
+
+def test_publish_rules():
+    c = lam.Ctl("", True, n_nodes=2, slots=2)
+    assert c.publish(0)[0] == lam.LAM_ESTALE
+    st, s = c.publish(3)
+    assert st == lam.LAM_OK
+    assert c.publish(3)[0] == lam.LAM_ESTALE and c.publish(2)[0] == lam.LAM_ESTALE
+    assert c.latest(0) == 0 and c.pin(0) == (0, -1)          # FILLING is never served
+    assert c.pack_done(s, 3) and c.latest(0) == 3
+    v, ps = c.pin(0)
+    assert v == 3
+    st4, s4 = c.publish(4)
+    assert st4 == lam.LAM_OK and s4 != ps
+    c.pack_done(s4, 4)
+    assert c.publish(5)[0] == lam.LAM_EBUSY                  # 3 pinned, 4 latest
+    c.unpin(0, ps)
+    assert c.publish(5)[0] == lam.LAM_OK
+    c.close()
+
+
+def test_fsdp_ranks_join_one_version():
+    c = lam.Ctl("", True, n_nodes=1, slots=2, fsdp=3)
+    st, s = c.publish(1, rank=2)
+    assert st == lam.LAM_OK
+    assert c.publish(1, rank=2)[0] == lam.LAM_ESTALE          # same rank twice
+    assert c.publish(2, rank=0)[0] == lam.LAM_EBUSY           # v1 still waits for ranks 0, 1
+    for r in (0, 1):
+        assert c.publish(1, rank=r) == (lam.LAM_OK, s)
+    for _ in range(2):
+        c.pack_done(s, 1)
+        assert c.latest(0) == 0
+    c.pack_done(s, 1)
+    assert c.latest(0) == 1
+    c.close()
+
+
+def test_corrupt_version_is_not_committed():
+    c = lam.Ctl("", True, n_nodes=2, slots=2)
+    for v in (1, 2):
+        st, s = c.publish(v)
+        c.pack_done(s, v)
+        s1, u, _ = c.start(1)
+        c.part_done(1, s1, u, 2, lam.LAM_OK if v == 1 else lam.LAM_ECHECKSUM)
+        c.part_done(1, s1, u, 2, lam.LAM_OK)
+    assert c.latest(1) == 1 and c.latest(0) == 2
+    assert not c.busy()                                      # node 1 does not retry the bad version
+    c.close()
+
+
+@pytest.mark.parametrize("seed", range(25))
+def test_matches_oracle_relay_model(seed):
+    rng = random.Random(seed)
+    p, S = rng.randint(2, 5), rng.choice([2, 3])
+    c = lam.Ctl("", True, n_nodes=p, slots=S)
+    o = RelayChain(p, 1, slots=S)
+    v, pins = 0, []
+    for _ in range(300):
+        a = rng.random()
+        if a < 0.2:
+            v += 1
+            st, s = c.publish(v)
+            want = o.publish(v)
+            assert {"ok": lam.LAM_OK, "busy": lam.LAM_EBUSY, "stale": lam.LAM_ESTALE}[want] == st
+            if st == lam.LAM_OK:
+                c.pack_done(s, v)
+        elif a < 0.4:
+            node = rng.randrange(p)
+            got, slot = c.pin(node)
+            want, oslot = o.pin_latest(node)
+            assert got == want
+            if got:
+                pins.append((node, slot, oslot))
+        elif a < 0.55 and pins:
+            node, slot, oslot = pins.pop(rng.randrange(len(pins)))
+            c.unpin(node, slot)
+            o.unpin(node, oslot)
+        else:
+            _round(c, p)
+            o.step()
+        assert [c.latest(n) for n in range(p)] == [n.latest for n in o.nodes]
+    c.close()
+
+
+# ------------------------------------------------------------------------------ two processes
+def _worker(rank, world, port, name, versions, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    errors = []
+    try:
+        c = lam.Ctl(name, rank == 0, n_nodes=3, slots=2)
+        dist.barrier()
+        rng = random.Random(rank)
+        if rank == 0:                                        # the actor: publish as fast as it can
+            published = []
+            v = 0
+            while v < versions:
+                st, s = c.publish(v + 1)
+                if st == lam.LAM_OK:
+                    v += 1
+                    c.pack_done(s, v)
+                    published.append(v)
+            q.put(("published", published))
+        else:                                                # the relays + a rollout pulling
+            seen = {1: 0, 2: 0}
+            for _ in range(200000):
+                for node in (1, 2):
+                    s, u, opened = c.start(node)
+                    if s >= 0 and rng.random() < 0.7:
+                        c.part_done(node, s, u, 1, lam.LAM_OK)
+                    lt = c.latest(node)
+                    if lt < seen[node]:
+                        errors.append(f"node {node} latest went back {seen[node]} -> {lt}")
+                    seen[node] = lt
+                node = rng.choice((1, 2))
+                got, slot = c.pin(node)
+                if got:
+                    pv, pst, prd = c.slot(node, slot)
+                    if (pv, pst) != (got, COMPLETE) or prd < 1:
+                        errors.append(f"pinned slot not COMPLETE({got}): {(pv, pst, prd)}")
+                    c.unpin(node, slot)
+                if c.latest(2) == versions:
+                    break
+        dist.barrier()
+        if rank == 1:
+            final = [c.latest(n) for n in range(3)]
+            if final != [versions] * 3:
+                errors.append(f"not quiescent at the newest version: {final}")
+        dist.barrier()
+        c.close()
+    except Exception as e:  # pragma: no cover - reported to the parent
+        errors.append(repr(e))
+    q.put((rank, errors))
+    dist.destroy_process_group()
+
+
+def test_two_processes_share_the_version_table():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    name = f"lam_ctl_test_{os.getpid()}"
+    versions = 60
+    procs = [ctx.Process(target=_worker, args=(r, 2, 29500 + os.getpid() % 1000, name, versions, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    results = [q.get(timeout=120) for _ in range(3)]
+    for pr in procs:
+        pr.join(timeout=60)
+    errs = [e for r in results if r[0] in (0, 1) for e in r[1]]
+    assert errs == [], errs
+    published = next(r[1] for r in results if r[0] == "published")
+    assert published == list(range(1, versions + 1))
