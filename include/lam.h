@@ -111,6 +111,8 @@ typedef struct {
   int32_t pack_ctas, hop_ctas, pull_ctas;
   double spin_timeout_s;                   /* chain-hop wait limit (default 60 s) */
   int32_t hop_mode;                        /* LAM_HOP_KERNEL (default) | LAM_HOP_COPY_ENGINE */
+  double heartbeat_timeout_s;              /* n_procs > 1: a process silent this long is declared
+                                              failed and its relay nodes leave the chain (0 = off) */
 } lam_config;
 
 /* How a relay moves a chunk from its predecessor (both receiver-driven, chunk-pipelined, verified):
@@ -167,6 +169,9 @@ typedef struct {
 typedef struct {
   uint64_t publishes, publish_busy, hops_launched, versions_skipped, pulls, checksum_errors,
       timeouts, plan_cache_hits, plan_cache_misses;
+  uint64_t chain_rebuilds;   /* relay failures handled (lam_fail_node or heartbeat timeout) */
+  uint64_t chain_resumes;    /* hops restarted from a new predecessor, from the lowest missing chunk */
+  uint64_t last_repair_ns;   /* failure declared -> successor's resumed hop launched (steady clock) */
 } lam_stats;
 
 /* ---- lifecycle ------------------------------------------------------------------------- */
@@ -210,6 +215,16 @@ lam_status lam_pull(lam_ctx*, int32_t rollout_id, const lam_tp_layout* layout, v
 
 /* Newest COMPLETE version at a node (0 if none; node 0 = master). */
 lam_status lam_latest(lam_ctx*, int32_t node, uint64_t* version_out);
+
+/* Fault-tolerant broadcast (§4.3, "the scheduler … immediately reconstructs the
+ * broadcast chain among the remaining rollout machines … a constant-time (O(1)) operation"):
+ * declare relay `node` failed (as the rollout manager's heartbeat monitor would; with n_procs > 1
+ * lam_relay_step also detects silent processes by itself, see heartbeat_timeout_s).  Its successor
+ * is linked to its predecessor; a successor that was receiving from it resumes the same version
+ * from the new predecessor, keeping every chunk it already verified.  Node 0 (the actor's slots)
+ * cannot be failed: that is a trainer failure (checkpoint recovery, out of scope).  Pulls at a
+ * failed node return LAM_ENOVERSION. */
+lam_status lam_fail_node(lam_ctx*, int32_t node);
 
 /* ---- introspection / helpers ----------------------------------------------------------- */
 lam_status lam_get_plan_info(lam_ctx*, lam_plan_info* out);
@@ -280,6 +295,8 @@ int32_t lam_ctl_pack_done(lam_ctl*, int32_t slot, uint64_t version);            
 int32_t lam_ctl_start(lam_ctl*, int32_t node, uint64_t* version, int32_t* started);   /* FILLING slot / -1 */
 int32_t lam_ctl_part_done(lam_ctl*, int32_t node, int32_t slot, uint64_t version, int32_t n_parts,
                           lam_status err);
+int32_t lam_ctl_fail(lam_ctl*, int32_t node);                                          /* 1 = rebuilt */
+int32_t lam_ctl_pred(lam_ctl*, int32_t node);                                          /* -1 = dead */
 uint64_t lam_ctl_pin(lam_ctl*, int32_t node, int32_t* slot);                           /* 0 = none */
 void lam_ctl_unpin(lam_ctl*, int32_t node, int32_t slot);
 uint64_t lam_ctl_latest(lam_ctl*, int32_t node);

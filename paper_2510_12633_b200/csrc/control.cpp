@@ -136,6 +136,60 @@ static void open_slot(ShmSlot& sl, uint64_t v, int src_slot) {
   sl.err = 0;
   sl.src_slot = src_slot;
   sl.launched_mask = 0;
+  sl.epoch++;
+}
+
+void init(Shm* sh, int n_nodes) {
+  sh->n_nodes = n_nodes;
+  for (int i = 0; i <= LAM_MAX_NODES; ++i) {
+    sh->node[i].dead = 0;
+    sh->node[i].pred = i - 1;
+  }
+}
+
+bool fail_node(Shm* sh, int S, int node, uint64_t now_ns) {
+  if (node <= 0 || node >= sh->n_nodes || sh->node[node].dead) return false;
+  ShmNode& d = sh->node[node];
+  d.dead = 1;
+  sh->fail_ns[node] = now_ns;
+  sh->last_fail_ns = now_ns;
+  sh->chain_epoch++;
+  // the dead node's own fill no longer pins its predecessor
+  for (int s = 0; s < S; ++s) {
+    ShmSlot& sl = d.slot[s];
+    if (sl.state == S_FILLING) {
+      if (sl.src_slot >= 0 && sh->node[d.pred].slot[sl.src_slot].readers > 0) sh->node[d.pred].slot[sl.src_slot].readers--;
+      sl.state = S_FREE;
+      sl.version = 0;
+      sl.src_slot = -1;
+    }
+  }
+  // O(1) rebuild: the (single) successor links to the failed node's predecessor
+  for (int j = node + 1; j < sh->n_nodes; ++j) {
+    ShmNode& n = sh->node[j];
+    if (n.dead || n.pred != node) continue;
+    n.pred = d.pred;
+    ShmNode& np = sh->node[n.pred];
+    for (int s = 0; s < S; ++s) {
+      ShmSlot& sl = n.slot[s];
+      if (sl.state != S_FILLING) continue;
+      const int ps = find_slot(np, S, sl.version, S_COMPLETE) >= 0 ? find_slot(np, S, sl.version, S_COMPLETE)
+                                                                 : find_slot(np, S, sl.version, S_FILLING);
+      if (ps >= 0) {                       // resume the same version from the new predecessor
+        np.slot[ps].readers++;
+        sl.src_slot = ps;
+        sl.launched_mask = 0;
+        sl.parts_done = sl.parts_finished = 0;
+        sl.epoch++;
+      } else {                             // abandon: start over with what the new predecessor has
+        sl.state = S_FREE;
+        sl.version = 0;
+        sl.src_slot = -1;
+        n.started = n.latest;
+      }
+    }
+  }
+  return true;
 }
 
 lam_status publish(Shm* sh, int S, int fsdp, uint64_t v, int rank, int* slot) {
@@ -177,7 +231,8 @@ bool pack_done(Shm* sh, int fsdp, int slot, uint64_t v) {
 int start(Shm* sh, int S, int node, bool* started) {
   *started = false;
   ShmNode& n = sh->node[node];
-  ShmNode& pred = sh->node[node - 1];
+  if (n.dead) return -1;
+  ShmNode& pred = sh->node[n.pred];
   for (int s = 0; s < S; ++s)
     if (n.slot[s].state == S_FILLING) return s;
   int ps = -1;
@@ -196,10 +251,10 @@ int start(Shm* sh, int S, int node, bool* started) {
   return s;
 }
 
-bool part_done(Shm* sh, int node, int slot, uint64_t v, int n_parts, lam_status err) {
+bool part_done(Shm* sh, int node, int slot, uint64_t v, int n_parts, lam_status err, uint32_t epoch) {
   ShmNode& n = sh->node[node];
   ShmSlot& sl = n.slot[slot];
-  if (sl.version != v || sl.state != S_FILLING) return false;
+  if (sl.version != v || sl.state != S_FILLING || sl.epoch != epoch || n.dead) return false;
   sl.parts_finished++;
   if (err != LAM_OK) {
     if (!sl.err) sl.err = err;
@@ -209,7 +264,7 @@ bool part_done(Shm* sh, int node, int slot, uint64_t v, int n_parts, lam_status 
   }
   if (sl.parts_finished == n_parts) {
     if (sl.src_slot >= 0) {
-      ShmSlot& src = sh->node[node - 1].slot[sl.src_slot];
+      ShmSlot& src = sh->node[n.pred].slot[sl.src_slot];
       if (src.readers > 0) src.readers--;
     }
     if (sl.err == 0) {
@@ -227,7 +282,7 @@ bool part_done(Shm* sh, int node, int slot, uint64_t v, int n_parts, lam_status 
 uint64_t pin_latest(Shm* sh, int S, int node, int* slot) {
   ShmNode& n = sh->node[node];
   *slot = -1;
-  if (n.latest == 0) return 0;
+  if (n.latest == 0 || n.dead) return 0;
   const int s = find_slot(n, S, n.latest, S_COMPLETE);
   if (s < 0) return 0;
   n.slot[s].readers++;
@@ -242,10 +297,12 @@ void unpin(Shm* sh, int node, int slot) {
 
 bool busy(Shm* sh, int S, int n_nodes) {
   for (int node = 0; node < n_nodes; ++node) {
+    const ShmNode& n = sh->node[node];
+    if (n.dead) continue;
     for (int s = 0; s < S; ++s)
-      if (sh->node[node].slot[s].state == S_FILLING) return true;
+      if (n.slot[s].state == S_FILLING) return true;
     int ps;
-    if (node > 0 && newest_held(sh->node[node - 1], S, &ps) > sh->node[node].started) return true;
+    if (node > 0 && newest_held(sh->node[n.pred], S, &ps) > n.started) return true;
   }
   return false;
 }
@@ -280,6 +337,7 @@ extern "C" lam_ctl* lam_ctl_open(const char* name, int32_t create, int32_t n_nod
     delete c;
     return nullptr;
   }
+  if (create || !c->mapped) ctl::init(c->sh, n_nodes);
   return c;
 }
 
@@ -311,7 +369,17 @@ extern "C" int32_t lam_ctl_start(lam_ctl* c, int32_t node, uint64_t* version, in
 extern "C" int32_t lam_ctl_part_done(lam_ctl* c, int32_t node, int32_t slot, uint64_t v, int32_t n_parts,
                                      lam_status err) {
   ShmLock l(c->sh);
-  return ctl::part_done(c->sh, node, slot, v, n_parts, err);
+  return ctl::part_done(c->sh, node, slot, v, n_parts, err, c->sh->node[node].slot[slot].epoch);
+}
+
+extern "C" int32_t lam_ctl_fail(lam_ctl* c, int32_t node) {
+  ShmLock l(c->sh);
+  return ctl::fail_node(c->sh, c->S, node, 0);
+}
+
+extern "C" int32_t lam_ctl_pred(lam_ctl* c, int32_t node) {
+  ShmLock l(c->sh);
+  return c->sh->node[node].dead ? -1 : c->sh->node[node].pred;
 }
 
 extern "C" uint64_t lam_ctl_pin(lam_ctl* c, int32_t node, int32_t* slot) {

@@ -28,20 +28,28 @@ struct ShmSlot {
   int32_t parts_done, parts_finished;  // node 0: ranks packed; relays: parts completed ok / at all
   int32_t err, src_slot;               // first error; predecessor slot pinned while FILLING
   uint64_t launched_mask;              // node 0: ranks published; relays: parts launched
+  uint32_t epoch, _pad;                // bumped when the fill restarts from a new predecessor
 };
 struct ShmNode {
   ShmSlot slot[LAM_MAX_SLOTS];
   uint64_t latest, started, skipped;
+  int32_t dead;                        // relay failed (heartbeat timeout or lam_fail_node)
+  int32_t pred;                        // current predecessor in the chain (rebuilt on failures)
 };
 struct Shm {
   uint64_t magic;
   pthread_mutex_t mu;
   uint64_t last_published;
-  int32_t ready_procs;
+  int32_t n_nodes, ready_procs;
   lam_stats stats;
+  uint64_t chain_epoch;                // chain rebuilds so far
+  uint64_t fail_ns[LAM_MAX_NODES + 1]; // steady-clock time each node was declared failed
+  uint64_t hb_ns[LAM_MAX_DEVICES];     // per process heartbeat (steady clock, ns)
+  uint64_t dead_procs;                 // bit mask
+  uint64_t last_fail_ns;               // most recent failure (repair-time accounting)
   ShmNode node[LAM_MAX_NODES + 1];
 };
-constexpr uint64_t kMagic = 0x4c414d5f53484d32ull;  // "LAM_SHM2"
+constexpr uint64_t kMagic = 0x4c414d5f53484d33ull;  // "LAM_SHM3"
 
 struct ShmLock {
   pthread_mutex_t* m;
@@ -67,12 +75,23 @@ bool pack_done(Shm* sh, int fsdp, int slot, uint64_t v);
 // FILLING slot (new or already open) or -1; *started = true if this call opened it.
 int start(Shm* sh, int S, int node, bool* started);
 // One part of `node` finished v in `slot` (err = 0 or a LAM_E* code); returns true on a change.
-bool part_done(Shm* sh, int node, int slot, uint64_t v, int n_parts, lam_status err);
+// `epoch` = the slot epoch the finished kernel was launched for; results of superseded launches
+// (the fill restarted after a chain rebuild) are ignored.
+bool part_done(Shm* sh, int node, int slot, uint64_t v, int n_parts, lam_status err, uint32_t epoch);
 // Pull side: pin the latest COMPLETE slot (0 if none) / release it.
 uint64_t pin_latest(Shm* sh, int S, int node, int* slot);
 void unpin(Shm* sh, int node, int slot);
 // Anything FILLING, or a node behind its predecessor?
 bool busy(Shm* sh, int S, int n_nodes);
+// Chain of n_nodes (called once by the creator): every node alive, pred = node - 1.
+void init(Shm* sh, int n_nodes);
+// Relay failure: mark `node` dead and rebuild the chain in O(1): its successor is
+// linked to its (live) predecessor.  A successor that was filling from it re-pins the same version
+// at the new predecessor and restarts (slot epoch++, launch mask cleared: the runtime resumes from
+// the lowest chunk it lacks); if the new predecessor does not hold that version the fill is
+// abandoned and the successor starts over with the newest the new predecessor holds.
+// Returns false if the node is node 0 (the actor's slots: trainer failure, out of scope) or dead.
+bool fail_node(Shm* sh, int S, int node, uint64_t now_ns);
 }  // namespace ctl
 
 }  // namespace lam

@@ -221,7 +221,10 @@ __global__ void __launch_bounds__(kHopThreads, 1)
         mbar_wait(&bar[st], (phases >> st) & 1u);
         phases ^= 1u << st;
       }
-      hop_fail(meta, err_word, s_fail_chunk, version, s_status == kHopTimeout ? kHopTimeout : kHopPoison);
+      // abort flag 2 = superseded by a chain rebuild (runtime restarts the fill): exit quietly,
+      // keep the verified chunks and do not poison the successor
+      if (!(s_status == kHopAbort && *(volatile int32_t*)meta.abort_flag == 2))
+        hop_fail(meta, err_word, s_fail_chunk, version, s_status == kHopTimeout ? kHopTimeout : kHopPoison);
     }
   }
 }

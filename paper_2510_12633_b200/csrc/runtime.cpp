@@ -69,6 +69,12 @@ struct Part {
   int ce_slot = -1, ce_ps = -1;
   uint64_t ce_version = 0;           // non-zero while chunks remain to be enqueued
   cudaEvent_t ce_t0 = nullptr;
+  // chain repair (NEXT-1): what this part last launched into each slot, resume tables
+  uint64_t launched_version[LAM_MAX_SLOTS] = {};
+  uint32_t launched_epoch[LAM_MAX_SLOTS] = {};
+  std::vector<HopTile> h_tiles;      // host copy of the full tile list
+  HopTile* d_resume = nullptr;       // tiles of the chunks still missing after a rebuild
+  RankLink* d_links_dyn = nullptr;   // links to a predecessor other than node - 1
 };
 
 struct RankPub {   // per local actor rank (node 0)
@@ -301,6 +307,9 @@ lam_status alloc_parts(lam_ctx* c) {
       p.n_tiles = (uint32_t)tiles.size();
       CK(cudaMalloc(&p.d_tiles, sizeof(HopTile) * std::max<size_t>(tiles.size(), 1)));
       if (!tiles.empty()) CK(cudaMemcpy(p.d_tiles, tiles.data(), sizeof(HopTile) * tiles.size(), cudaMemcpyHostToDevice));
+      CK(cudaMalloc(&p.d_resume, sizeof(HopTile) * std::max<size_t>(tiles.size(), 1)));
+      CK(cudaMalloc(&p.d_links_dyn, sizeof(RankLink) * N));
+      p.h_tiles = tiles;
       CK(cudaMalloc(&p.d_tiles_per_chunk, 4 * std::max<uint64_t>(total, 1)));
       if (total) CK(cudaMemcpy(p.d_tiles_per_chunk, tpc.data(), 4 * total, cudaMemcpyHostToDevice));
       // copy-engine mode: chunk order, verify stream, per-chunk events
@@ -458,6 +467,105 @@ lam_status ce_topup(lam_ctx* c, Part& p) {
   return LAM_OK;
 }
 
+// ---------------------------------------------------------------------- chain repair (NEXT-1)
+// Ask the part's in-flight hop kernel for slot s to exit without poisoning anything (abort = 2).
+cudaError_t abort_part_kernel(lam_ctx* c, Part& p, int s) {
+  static const int32_t two = 2;
+  ChunkMeta m = meta_of(c, p, s);
+  // a separate stream: the write must not queue behind the kernel it stops
+  cudaError_t e = cudaMemcpyAsync(m.abort_flag, &two, sizeof two, cudaMemcpyHostToDevice, c->dev[p.device].side);
+  if (e != cudaSuccess) return e;
+  return cudaStreamSynchronize(c->dev[p.device].side);
+}
+
+// Resume list after a rebuild: every tile of every chunk the slot has not verified yet, with the
+// chunk's header sums and counter reset (chunks already verified keep their bytes and header).
+lam_status build_resume(lam_ctx* c, Part& p, int s, uint64_t u, uint32_t* n_out) {
+  ChunkMeta m = meta_of(c, p, s);
+  const uint64_t total = c->plan.total_chunks;
+  std::vector<uint64_t> flags(total);
+  CK(cudaStreamSynchronize(p.stream));
+  CK(cudaMemcpy(flags.data(), m.flags, 8 * total, cudaMemcpyDeviceToHost));
+  std::vector<HopTile> res;
+  std::vector<uint32_t> missing;
+  for (const HopTile& t : p.h_tiles) {
+    if (flags[t.chunk] == u) continue;
+    if (missing.empty() || missing.back() != t.chunk) missing.push_back(t.chunk);
+    res.push_back(t);
+  }
+  if (!res.empty()) CK(cudaMemcpy(p.d_resume, res.data(), sizeof(HopTile) * res.size(), cudaMemcpyHostToDevice));
+  for (uint32_t g : missing) {
+    CK(cudaMemsetAsync(m.hdr + g, 0, sizeof(lam_chunk_header), p.stream));
+    CK(cudaMemsetAsync(m.cnt + g, 0, 4, p.stream));
+  }
+  CK(cudaMemsetAsync(m.abort_flag, 0, 4, p.stream));
+  *n_out = (uint32_t)res.size();
+  return LAM_OK;
+}
+
+// Hop links of part p (my slot s) to predecessor node `pred` (slot ps) — for rebuilt chains.
+lam_status build_links(lam_ctx* c, Part& p, int s, int pred, int ps) {
+  std::vector<RankLink> links(c->cfg.fsdp_size);
+  for (int r : p.ranks) {
+    const Part& q = c->parts[c->node_rank_part[pred][r]];
+    ChunkMeta qm = meta_of(c, q, ps);
+    links[r].src = slot_data(q, ps) + q.rank_off[r];
+    links[r].src_flags = qm.flags;
+    links[r].src_hdr = qm.hdr;
+    links[r].dst = slot_data(p, s) + p.rank_off[r];
+  }
+  CK(cudaStreamSynchronize(p.stream));
+  CK(cudaMemcpy(p.d_links_dyn, links.data(), sizeof(RankLink) * links.size(), cudaMemcpyHostToDevice));
+  return LAM_OK;
+}
+
+uint64_t steady_ns() {
+  struct timespec ts;
+  clock_gettime(CLOCK_MONOTONIC, &ts);
+  return (uint64_t)ts.tv_sec * 1000000000ull + (uint64_t)ts.tv_nsec;
+}
+
+// A node failed: rebuild the chain (control plane) and stop this process's kernels of the dead
+// node (a simulated failure keeps its memory alive; nothing reads it after the rebuild).
+lam_status fail_node_locked(lam_ctx* c, int node) {
+  if (!ctl::fail_node(c->shm, c->S, node, steady_ns())) return LAM_EINVAL;
+  c->shm->stats.chain_rebuilds++;
+  for (Part& p : c->parts) {
+    if (!p.local || p.node != node) continue;
+    CK(cudaSetDevice(p.device));
+    for (int s = 0; s < c->S; ++s)
+      if (p.inflight_version[s]) {
+        CK(abort_part_kernel(c, p, s));
+        p.inflight_version[s] = 0;
+      }
+    p.ce_version = 0;
+  }
+  return LAM_OK;
+}
+
+// Heartbeats ("detects the failure via heartbeat monitoring"): every lam_relay_step
+// stamps this process; a process silent for longer than heartbeat_timeout_s is declared failed and
+// every relay node with a part on its GPUs is removed from the chain.
+lam_status heartbeat_locked(lam_ctx* c) {
+  Shm* sh = c->shm;
+  const uint64_t now = steady_ns();
+  sh->hb_ns[c->cfg.proc_rank] = now;
+  if (c->cfg.n_procs < 2 || c->cfg.heartbeat_timeout_s <= 0) return LAM_OK;
+  const uint64_t limit = (uint64_t)(c->cfg.heartbeat_timeout_s * 1e9);
+  for (int q = 0; q < c->cfg.n_procs; ++q) {
+    if (q == c->cfg.proc_rank || (sh->dead_procs >> q & 1ull) || sh->hb_ns[q] == 0) continue;
+    if (now - sh->hb_ns[q] <= limit) continue;
+    sh->dead_procs |= 1ull << q;
+    for (int node = 1; node < c->n_nodes; ++node)
+      for (int pi : c->node_parts[node])
+        if (c->cfg.proc_of_device[c->parts[pi].device] == q && !sh->node[node].dead) {
+          lam_status st = fail_node_locked(c, node);
+          if (st != LAM_OK) return st;
+        }
+  }
+  return LAM_OK;
+}
+
 // ----------------------------------------------------------------------------- progress engine
 // Launch the hop kernel of local part p (node >= 1) for FILLING slot s.  Returns true if launched.
 lam_status launch_hop_part(lam_ctx* c, Part& p, int s, bool* launched) {
@@ -465,16 +573,25 @@ lam_status launch_hop_part(lam_ctx* c, Part& p, int s, bool* launched) {
   ShmNode& n = c->shm->node[p.node];
   ShmSlot& sl = n.slot[s];
   const int ps = sl.src_slot;
+  const int pred = n.pred;
   const uint64_t u = sl.version;
   CK(cudaSetDevice(p.device));
+  // Restart after a chain rebuild (same version, new epoch): resume from the lowest missing chunks.
+  const bool resume = p.launched_version[s] == u && p.launched_epoch[s] != sl.epoch;
+  if (resume && p.inflight_version[s] == u) {
+    // the superseded kernel may be spinning on the failed predecessor: ask it to exit quietly
+    CK(abort_part_kernel(c, p, s));
+    CK(cudaStreamSynchronize(p.stream));
+    p.inflight_version[s] = 0;
+  }
   // predecessor parts on the same GPU must have finished (never spin on a kernel of the same GPU)
   std::set<int> waits;
   for (int r : p.ranks) {
-    int qi = c->node_rank_part[p.node - 1][r];
+    int qi = c->node_rank_part[pred][r];
     const Part& q = c->parts[qi];
     if (q.device != p.device) continue;
     if (!q.local) return LAM_EINVAL;  // one process per GPU: cannot happen
-    if (p.node - 1 == 0) {
+    if (pred == 0) {
       if (!(c->shm->node[0].slot[ps].launched_mask >> r & 1ull)) return LAM_OK;  // not yet published
       if (c->pubs[r].inflight_version[ps] == u) CK(cudaStreamWaitEvent(p.stream, c->pubs[r].ev[ps], 0));
     } else {
@@ -488,10 +605,23 @@ lam_status launch_hop_part(lam_ctx* c, Part& p, int s, bool* launched) {
     if (q.inflight_version[ps] == u) CK(cudaStreamWaitEvent(p.stream, q.done_ev[ps], 0));
   }
   ChunkMeta m = meta_of(c, p, s);
-  CK(cudaMemsetAsync((uint8_t*)m.hdr, 0, c->sm.abort + 64 - c->sm.hdr, p.stream));  // hdr, cnt, abort
+  const HopTile* tiles = p.d_tiles;
+  uint32_t n_tiles = p.n_tiles;
+  if (resume) {
+    // keep the chunks this slot already verified (own flag == u); redo every other chunk whole
+    lam_status st = build_resume(c, p, s, u, &n_tiles);
+    if (st != LAM_OK) return st;
+    tiles = p.d_resume;
+    c->shm->stats.chain_resumes++;
+    if (c->shm->last_fail_ns) c->shm->stats.last_repair_ns = steady_ns() - c->shm->last_fail_ns;
+  } else {
+    CK(cudaMemsetAsync((uint8_t*)m.hdr, 0, c->sm.abort + 64 - c->sm.hdr, p.stream));  // hdr, cnt, abort
+  }
   p.err_host[s] = 0;
+  p.launched_version[s] = u;
+  p.launched_epoch[s] = sl.epoch;
   cudaEvent_t t0 = prof_begin(c, p.device, p.stream);
-  if (c->cfg.hop_mode == LAM_HOP_COPY_ENGINE) {
+  if (c->cfg.hop_mode == LAM_HOP_COPY_ENGINE && !resume && pred == p.node - 1) {
     p.ce_slot = s;
     p.ce_ps = ps;
     p.ce_next = 0;
@@ -503,7 +633,12 @@ lam_status launch_hop_part(lam_ctx* c, Part& p, int s, bool* launched) {
     return ce_topup(c, p);
   } else {
     const RankLink* links = p.d_links + (size_t)(s * c->S + ps) * c->cfg.fsdp_size;
-    int rc = launch_hop(p.d_tiles, p.n_tiles, links, m, p.d_tiles_per_chunk, u, p.err_dev + s, c->timeout_ns,
+    if (pred != p.node - 1) {  // rebuilt chain: links to the new predecessor
+      lam_status st = build_links(c, p, s, pred, ps);
+      if (st != LAM_OK) return st;
+      links = p.d_links_dyn;
+    }
+    int rc = launch_hop(tiles, n_tiles, links, m, p.d_tiles_per_chunk, u, p.err_dev + s, c->timeout_ns,
                         c->hop_ctas, p.stream);
     if (rc) {
       fprintf(stderr, "liblam: hop launch failed: %s\n", cudaGetErrorString((cudaError_t)rc));
@@ -524,6 +659,8 @@ lam_status step_locked(lam_ctx* c, int* transitions, bool* busy) {
   const int S = c->S;
   lam_status first_err = LAM_OK;
   *busy = false;
+  lam_status hb = heartbeat_locked(c);
+  if (hb != LAM_OK) return hb;
   // (1) completions of local packs (node 0)
   for (int r = 0; r < c->cfg.fsdp_size; ++r) {
     if (!owns(c, c->cfg.actor_device[r])) continue;
@@ -551,7 +688,8 @@ lam_status step_locked(lam_ctx* c, int* transitions, bool* busy) {
       if (q == cudaErrorNotReady) { *busy = true; continue; }
       if (q != cudaSuccess) return LAM_ECUDA;
       const lam_status e = p.err_host[s] ? -(lam_status)p.err_host[s] : LAM_OK;
-      if (ctl::part_done(sh, p.node, s, p.inflight_version[s], (int)c->node_parts[p.node].size(), e)) {
+      if (ctl::part_done(sh, p.node, s, p.inflight_version[s], (int)c->node_parts[p.node].size(), e,
+                         p.launched_epoch[s])) {
         (*transitions)++;
         if (e != LAM_OK && first_err == LAM_OK) first_err = e;
       }
@@ -697,6 +835,7 @@ extern "C" lam_status lam_init(const lam_config* cfg, lam_ctx** out) {
   c->pubs.resize(cfg->fsdp_size);
   st = setup_shm(c.get());
   if (st != LAM_OK) return st;
+  if (cfg->n_procs == 1 || cfg->proc_rank == 0) ctl::init(c->shm, c->n_nodes);
   st = alloc_parts(c.get());
   if (st != LAM_OK) {
     lam_destroy(c.release());
@@ -894,6 +1033,12 @@ extern "C" lam_status lam_pull(lam_ctx* c, int32_t rid, const lam_tp_layout* L, 
   c->shm->stats.pulls++;
   if (vout) *vout = u;
   return LAM_OK;
+}
+
+extern "C" lam_status lam_fail_node(lam_ctx* c, int32_t node) {
+  if (!c || !c->connected || node <= 0 || node >= c->n_nodes) return LAM_EINVAL;
+  Lock l(c->shm);
+  return fail_node_locked(c, node);
 }
 
 extern "C" lam_status lam_latest(lam_ctx* c, int32_t node, uint64_t* vout) {

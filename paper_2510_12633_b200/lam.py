@@ -45,7 +45,8 @@ class lam_config(C.Structure):
                 ("rollout", lam_rollout_desc * LAM_MAX_ROLLOUTS), ("proc_rank", C.c_int32),
                 ("n_procs", C.c_int32), ("proc_of_device", C.c_int32 * LAM_MAX_DEVICES),
                 ("shm_name", C.c_char * 64), ("pack_ctas", C.c_int32), ("hop_ctas", C.c_int32),
-                ("pull_ctas", C.c_int32), ("spin_timeout_s", C.c_double), ("hop_mode", C.c_int32)]
+                ("pull_ctas", C.c_int32), ("spin_timeout_s", C.c_double), ("hop_mode", C.c_int32),
+                ("heartbeat_timeout_s", C.c_double)]
 
 
 class lam_shard(C.Structure):
@@ -90,7 +91,8 @@ class lam_copy_tile_info(C.Structure):
 class lam_stats(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in ("publishes", "publish_busy", "hops_launched", "versions_skipped",
                                           "pulls", "checksum_errors", "timeouts", "plan_cache_hits",
-                                          "plan_cache_misses")]
+                                          "plan_cache_misses", "chain_rebuilds", "chain_resumes",
+                                          "last_repair_ns")]
 
 
 _LIB = None
@@ -236,6 +238,7 @@ class Config:
     pull_ctas: int = 0
     spin_timeout_s: float = 0.0
     hop_mode: int = LAM_HOP_KERNEL
+    heartbeat_timeout_s: float = 0.0
 
     def to_c(self) -> lam_config:
         c = lam_config()
@@ -264,6 +267,7 @@ class Config:
         c.pack_ctas, c.hop_ctas, c.pull_ctas, c.spin_timeout_s = (self.pack_ctas, self.hop_ctas, self.pull_ctas,
                                                                   self.spin_timeout_s)
         c.hop_mode = self.hop_mode
+        c.heartbeat_timeout_s = self.heartbeat_timeout_s
         return c
 
 
@@ -317,6 +321,12 @@ class Context:
         v = C.c_uint64()
         _check(self.L.lam_latest(self.h, node, C.byref(v)), "lam_latest", ok=(LAM_OK, LAM_ENOVERSION))
         return v.value
+
+    def fail_node(self, node: int) -> None:
+        """Declare relay `node` failed: O(1) chain rebuild, successors resume (lam_fail_node)."""
+        f = self.L.lam_fail_node
+        f.restype, f.argtypes = C.c_int32, [C.c_void_p, C.c_int32]
+        _check(f(self.h, node), "lam_fail_node")
 
     def plan_info(self) -> lam_plan_info:
         p = lam_plan_info()
@@ -413,6 +423,7 @@ class Ctl:
                               ("lam_ctl_part_done", I32, [V, I32, I32, U64, I32, I32]),
                               ("lam_ctl_pin", U64, [V, I32, P(I32)]), ("lam_ctl_unpin", None, [V, I32, I32]),
                               ("lam_ctl_latest", U64, [V, I32]), ("lam_ctl_busy", I32, [V]),
+                              ("lam_ctl_fail", I32, [V, I32]), ("lam_ctl_pred", I32, [V, I32]),
                               ("lam_ctl_slot", I32, [V, I32, I32, P(U64), P(I32), P(I32)])]:
             f = getattr(L, fn)
             f.restype, f.argtypes = res, args
@@ -449,6 +460,12 @@ class Ctl:
 
     def busy(self) -> bool:
         return bool(self.L.lam_ctl_busy(self.h))
+
+    def fail(self, node: int) -> bool:
+        return bool(self.L.lam_ctl_fail(self.h, node))
+
+    def pred(self, node: int) -> int:
+        return self.L.lam_ctl_pred(self.h, node)
 
     def slot(self, node: int, slot: int):
         v, st, rd = C.c_uint64(), C.c_int32(), C.c_int32()

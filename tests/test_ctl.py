@@ -109,6 +109,66 @@ def test_matches_oracle_relay_model(seed):
     c.close()
 
 
+# ---------------------------------------------------------------------- chain repair (NEXT-1)
+def _publish_complete(c, v):
+    st, s = c.publish(v)
+    assert st == lam.LAM_OK
+    c.pack_done(s, v)
+
+
+def test_rebuild_chain_spec_example():
+    """chain [m,a,b,c], fail b -> [m,a,c], a's successor is c (O(1) relink)."""
+    c = lam.Ctl("", True, n_nodes=4, slots=2)
+    assert [c.pred(n) for n in (1, 2, 3)] == [0, 1, 2]
+    assert c.fail(2)
+    assert [c.pred(n) for n in (1, 2, 3)] == [0, -1, 1]
+    assert not c.fail(2) and not c.fail(0)                # already dead / the actor's slots
+    _publish_complete(c, 1)
+    for _ in range(4):
+        _round(c, 4)
+    assert [c.latest(n) for n in range(4)] == [1, 1, 0, 1]  # the dead node is skipped, never served
+    assert c.pin(2) == (0, -1)
+    assert not c.busy()
+    c.close()
+
+
+def test_fail_mid_broadcast_resumes_same_version():
+    c = lam.Ctl("", True, n_nodes=4, slots=2)
+    _publish_complete(c, 1)
+    s1, v1, _ = c.start(1)
+    c.part_done(1, s1, v1)                                # node 1 holds v1
+    s2, v2, _ = c.start(2)                                # node 2 filling v1 from node 1
+    s3, v3, _ = c.start(3)                                # node 3 filling v1 from node 2 (pipelined)
+    assert (v2, v3) == (1, 1)
+    assert c.fail(2)                                      # node 2 dies mid-broadcast
+    assert c.pred(3) == 1
+    ver, state, readers = c.slot(3, s3)
+    assert (ver, state) == (1, FILLING)                   # same version, now pinned at node 1
+    assert c.slot(1, s1)[2] == 1
+    c.part_done(3, s3, 1)
+    assert c.latest(3) == 1 and c.slot(1, s1)[2] == 0     # pin released at the new predecessor
+    c.close()
+
+
+def test_fail_abandons_version_the_new_predecessor_lacks():
+    c = lam.Ctl("", True, n_nodes=4, slots=2)
+    _publish_complete(c, 1)
+    for _ in range(3):
+        _round(c, 4)
+    _publish_complete(c, 2)
+    s1, v1, _ = c.start(1)                                # node 1 FILLING v2
+    s2, v2, _ = c.start(2)                                # node 2 FILLING v2 from node 1
+    assert c.fail(1)                                      # node 2 re-points to node 0, which has v2
+    assert c.pred(2) == 0 and c.slot(2, s2)[:2] == (2, FILLING)
+    assert c.fail(2)                                      # node 3 re-points to node 0 as well
+    assert c.pred(3) == 0
+    _publish_complete(c, 3)
+    for _ in range(3):
+        _round(c, 4)
+    assert c.latest(3) == 3 and not c.busy()
+    c.close()
+
+
 # ------------------------------------------------------------------------------ two processes
 def _worker(rank, world, port, name, versions, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -146,7 +206,7 @@ def _worker(rank, world, port, name, versions, q):
                     if (pv, pst) != (got, COMPLETE) or prd < 1:
                         errors.append(f"pinned slot not COMPLETE({got}): {(pv, pst, prd)}")
                     c.unpin(node, slot)
-                if c.latest(2) == versions:
+                if c.latest(1) == versions and c.latest(2) == versions:
                     break
         dist.barrier()
         if rank == 1:
