@@ -818,7 +818,9 @@ extern "C" lam_status lam_init(const lam_config* cfg, lam_ctx** out) {
   uint64_t C = cfg->chunk_bytes;
   if (C == 0) {
     double tb = cfg->t_byte_s > 0 ? cfg->t_byte_s : 1.0 / 750e9;
-    double tsu = cfg->t_start_s > 0 ? cfg->t_start_s : 5e-6;
+    // T_start calibrated on B200 (bench --chunk-mb sweep at N=4: 64 MB 38.0 ms, 138 MB 34.2 ms,
+    // 256 MB 33.1 ms): per-chunk flag propagation + pipeline refill is ~20 us, not RDMA's ~5 us
+    double tsu = cfg->t_start_s > 0 ? cfg->t_start_s : 20e-6;
     // the pack is one more pipeline stage ahead of the chain (reading R12)
     int64_t k = lam_optimal_chunks(c->n_nodes + 1, 2.0 * (double)c->params, tb, tsu, 1024);
     C = align_up(cdiv(2 * c->params, (uint64_t)k), kChunkAlign);
