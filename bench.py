@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--hop-ctas", type=int, default=0)
     ap.add_argument("--hop-mode", default="kernel", choices=["kernel", "ce"],
                     help="relay hop: TMA kernel or copy engines + k_verify")
+    ap.add_argument("--no-stream-pull", action="store_true",
+                    help="rollouts pull only after their relay committed (no chunk-by-chunk reshard)")
     ap.add_argument("--pack-ctas", type=int, default=0)
     ap.add_argument("--pull-ctas", type=int, default=0)
     ap.add_argument("--e2e-steps", type=int, default=2)
@@ -282,19 +284,26 @@ def main():
                     shards[r].buf.copy_(h2d[r], non_blocking=True)
             while ctx.publish(v, r, shards[r].shards(), actor_stream.cuda_stream) == lam.LAM_EBUSY:
                 ctx.relay_step()
-        pending = list(mine)
+        pending, streaming = list(mine), []
         while True:
             ctx.relay_step()
             for rid in list(pending):
-                if ctx.latest(rollouts[rid][0]) >= v:
-                    got = ctx.pull(rid, bufs[rid].tp, stream.cuda_stream)
+                if args.no_stream_pull:                     # classic: pull once the relay committed v
+                    got = ctx.pull(rid, bufs[rid].tp, stream.cuda_stream) if ctx.latest(rollouts[rid][0]) >= v else 0
+                else:                                       # reshard chunk by chunk while v arrives
+                    got = ctx.pull_stream(rid, bufs[rid].tp, stream.cuda_stream, None, v)
+                if got:
                     assert got >= v, (got, v)
+                    pending.remove(rid)
+                    streaming.append(rid)
+            for rid in list(streaming):
+                if args.no_stream_pull or ctx.pull_state(rid)[1] == 0:
                     if d2h is not None:
                         with torch.cuda.stream(stream):
                             for name, t in bufs[rid].bufs.items():
                                 d2h[rid][name].copy_(t, non_blocking=True)
-                    pending.remove(rid)
-            if not pending and (not my_ranks or ctx.latest(0) >= v):
+                    streaming.remove(rid)
+            if not pending and not streaming and (not my_ranks or ctx.latest(0) >= v):
                 break
         stream.synchronize()
         ctx.relay_step()

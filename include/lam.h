@@ -213,6 +213,21 @@ lam_status lam_relay_step(lam_ctx*, int32_t* n_transitions);
 lam_status lam_pull(lam_ctx*, int32_t rollout_id, const lam_tp_layout* layout, void* stream,
                     uint64_t* version_out);
 
+/* Streaming pull — for a rollout that is waiting for new weights (a rollout
+ * fetches on batch completion).  If the rollout's node holds a COMPLETE version >= min_version this is
+ * lam_pull.  Otherwise, if the node is receiving one (FILLING), that version is pinned and resharded
+ * chunk by chunk as its chunks arrive: every lam_relay_step of this process launches the reshard
+ * of the newly verified chunks on `stream` (host-driven: no kernel waits on another kernel of the
+ * same GPU); after the last chunk `done_event` (caller-created, rollout's device, may be NULL) is
+ * recorded on `stream`.  The destination buffers are valid only once lam_pull_state reports 0 and
+ * `stream` reached done_event.  *version_out = the version being pulled; 0 + LAM_ENOVERSION if none
+ * >= min_version is complete or in flight; LAM_EBUSY if the rollout has a streaming pull running. */
+lam_status lam_pull_stream(lam_ctx*, int32_t rollout_id, const lam_tp_layout* layout, void* stream,
+                           void* done_event, uint64_t min_version, uint64_t* version_out);
+/* State of the rollout's streaming pull: 1 = chunks still arriving, 0 = all enqueued (or none),
+ * < 0 = the version failed at the node (LAM_ECHECKSUM / LAM_ETIMEOUT): buffers hold no valid version. */
+lam_status lam_pull_state(lam_ctx*, int32_t rollout_id, uint64_t* version_out, int32_t* state);
+
 /* Newest COMPLETE version at a node (0 if none; node 0 = master). */
 lam_status lam_latest(lam_ctx*, int32_t node, uint64_t* version_out);
 

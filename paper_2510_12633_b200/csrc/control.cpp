@@ -5,6 +5,7 @@
 #include <errno.h>
 #include <fcntl.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 #include <sys/mman.h>
 #include <sys/stat.h>
@@ -33,8 +34,9 @@ static void init_mutex(Shm* s, bool shared) {
 }
 
 Shm* shm_heap() {
-  Shm* s = new (std::nothrow) Shm();
-  if (!s) return nullptr;
+  void* mem = nullptr;  // page-aligned: the runtime cudaHostRegister()s the block
+  if (posix_memalign(&mem, 4096, sizeof(Shm)) != 0) return nullptr;
+  Shm* s = reinterpret_cast<Shm*>(mem);
   memset(s, 0, sizeof(Shm));
   init_mutex(s, false);
   s->magic = kMagic;
@@ -97,7 +99,7 @@ void shm_release(Shm* s, const char* name, bool mapped, bool owner) {
     }
   } else {
     pthread_mutex_destroy(&s->mu);
-    delete s;
+    free(s);
   }
 }
 

@@ -48,7 +48,12 @@ struct Shm {
   uint64_t dead_procs;                 // bit mask
   uint64_t last_fail_ns;               // most recent failure (repair-time accounting)
   ShmNode node[LAM_MAX_NODES + 1];
+  // Host-visible mirror of every slot's chunk flags, written by the producer kernels through a
+  // mapped (cudaHostRegister) view of this block: lets the rollout's process launch a streaming
+  // pull's reshard chunk by chunk without any kernel waiting on another kernel of the same GPU.
+  uint64_t chunk_done[LAM_MAX_NODES + 1][LAM_MAX_SLOTS][2048];
 };
+constexpr uint32_t kShmMirrorChunks = 2048;
 constexpr uint64_t kMagic = 0x4c414d5f53484d33ull;  // "LAM_SHM3"
 
 struct ShmLock {

@@ -2,24 +2,28 @@
 // along a chain of relays, overlapping communication among different hops"; L693).
 // Included by kernels.cu (shares its primitives).
 //
-// Receiver-driven, TMA bulk pipeline (measured on B200 NVLink 5: 16 CTAs of bulk copies reach
-// ~760 GB/s and 32 reach ~785 GB/s, where 16-B peer loads need ~148 CTAs — tools/p2p_bench.cu).
-// Each CTA walks a fixed job list (its tiles cut into 32 KiB sub-blocks); stage ring of 6 x 32 KiB:
+// Receiver-driven.  The NVLink pull is the latency-bound part, so it goes to TMA (bulk copies reach
+// ~785 GB/s with 32 CTAs where 16-B peer loads need ~148 — tools/p2p_bench.cu); the local part is
+// done by the threads that read the stage anyway:
 //   producer (thread 0): before the first sub-block of a new chunk, check the predecessor's chunk
 //     flag (ld.acquire.sys over NVLink); cp.async.bulk peer global -> smem stage, completion on an
-//     mbarrier (expect_tx).  Refills are non-blocking, so a chunk's completion is never held
-//     behind the wait for the next chunk; only an empty pipeline makes it spin.
-//   all 128 threads: checksum (S1, S2) of the stage from shared memory (conflict-free 16-B reads);
-//     one __syncthreads per stage.
-//   thread 0: cp.async.bulk smem -> local HBM (one bulk group per stage).  A stage is refilled one
-//     iteration later (wait_group.read 1), so the store just issued is never waited on.
-//   tile end: block-reduce the checksum; the tile's completion (atomics into the chunk header,
-//     counter, flag) is deferred until two more store groups were issued (wait_group 2), so the
-//     drain of its stores overlaps the next tile.  The CTA completing a chunk compares with the
-//     predecessor's header and releases the flag (st.release.sys) — or poisons it on mismatch so
-//     the successor aborts too.
+//     mbarrier (expect_tx).  Refills are non-blocking, so the chunk in hand is never held behind the
+//     wait for the next one; only an empty pipeline makes it spin.
+//   all 512 threads, per 32 KiB stage: 16-B shared loads -> streaming 16-B stores to local HBM +
+//     checksum (S1, S2); one __syncthreads, after which the stage is refilled immediately.
+//   A CTA folds its share of a chunk into the chunk header once, after its last tile of that chunk
+//     (fence, 3 atomics); the CTA completing the chunk compares with the predecessor's header and
+//     releases the flag (st.release.sys) — or poisons it on mismatch so the successor aborts too
+//     (SPEC L643).
+// Cycle accounting of the previous design (128 threads, TMA store per stage; LAM_HOP_PROF): thread 0
+// spent only 11-23 % waiting for data and ~80 % in the checksum pass and in waiting for its store to
+// release the stage.
 
-constexpr int kHopThreads = 128;
+// Optional per-CTA cycle accounting of thread 0 (LAM_HOP_PROF=1; diagnostics only):
+// [0] data wait, [1] copy + checksum, [2] barrier, [3] chunk flush, [4] refill, [5] empty-pipeline spin, [6] total
+__device__ unsigned long long* g_hop_prof = nullptr;
+
+constexpr int kHopThreads = 512;
 constexpr int kHopStages = 6;
 constexpr uint32_t kHopSub = 32768;  // bytes per pipeline stage
 constexpr size_t kHopSmem = (size_t)kHopStages * kHopSub;
@@ -49,39 +53,30 @@ __device__ __forceinline__ void bulk_g2s(void* smem, const void* gsrc, uint32_t 
                "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
 }
-__device__ __forceinline__ void bulk_s2g(void* gdst, const void* smem, uint32_t bytes) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(smem)),
-               "r"(bytes)
-               : "memory");
-  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-}
-template <int N>
-__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
-template <int N>
-__device__ __forceinline__ void bulk_wait() {
-  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
-  asm volatile("fence.proxy.async.global;" ::: "memory");  // async-proxy writes before generic release
+__device__ __forceinline__ uint4 lds128(const void* p) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(smem_u32(p)));
+  return v;
 }
 
 __device__ void hop_fail(ChunkMeta meta, uint32_t* err_word, uint32_t chunk, uint64_t version, int why) {
   atomicExch(meta.abort_flag, 1);
   const uint32_t code = (why == kHopTimeout) ? (uint32_t)(-LAM_ETIMEOUT) : (uint32_t)(-LAM_ECHECKSUM);
   atomicCAS(err_word, 0u, code);
-  st_release_sys(meta.flags + chunk, version | kPoison);  // tell our successor
+  publish_flag(meta, chunk, version | kPoison);  // tell our successor
   __threadfence_system();
 }
 
-// Tile finished and its stores complete: fold its checksum into the chunk header; the CTA that
+// A CTA's share of chunk `chunk` (n tiles) is in local HBM: fold it into the header; the CTA that
 // completes the chunk verifies it against the predecessor and publishes (or poisons) the flag.
-__device__ void hop_complete_tile(ChunkMeta meta, const RankLink& L, const uint32_t* tiles_per_chunk, uint32_t chunk,
-                                  uint64_t s1, uint64_t s2, uint64_t version, uint32_t* err_word) {
-  __threadfence_system();
+__device__ void hop_flush(ChunkMeta meta, const RankLink& L, const uint32_t* tiles_per_chunk, uint32_t chunk,
+                          uint32_t n, uint64_t s1, uint64_t s2, uint64_t version, uint32_t* err_word) {
   lam_chunk_header* h = meta.hdr + chunk;
   atomicAdd((unsigned long long*)&h->s1, (unsigned long long)s1);
   atomicAdd((unsigned long long*)&h->s2, (unsigned long long)s2);
-  __threadfence();
-  const uint32_t prev = atomicAdd(meta.cnt + chunk, 1u);
-  if (prev + 1 != tiles_per_chunk[chunk]) return;
+  __threadfence_system();
+  const uint32_t prev = atomicAdd(meta.cnt + chunk, n);
+  if (prev + n != tiles_per_chunk[chunk]) return;
   __threadfence();
   const uint64_t got1 = atomicAdd((unsigned long long*)&h->s1, 0ull);
   const uint64_t got2 = atomicAdd((unsigned long long*)&h->s2, 0ull);
@@ -92,7 +87,7 @@ __device__ void hop_complete_tile(ChunkMeta meta, const RankLink& L, const uint3
     h->n = ld_relaxed_sys(&ph->n);
     h->bytes = ld_relaxed_sys(&ph->bytes);
     __threadfence_system();
-    st_release_sys(meta.flags + chunk, version);
+    publish_flag(meta, chunk, version);
   } else {
     hop_fail(meta, err_word, chunk, version, kHopPoison);
   }
@@ -151,82 +146,90 @@ __global__ void __launch_bounds__(kHopThreads, 1)
 
   if (threadIdx.x == 0 && total > 0) {
     try_issue(true);
-    while (issued < kHopStages - 1 && try_issue(false)) {}
+    while (issued < kHopStages && try_issue(false)) {}
   }
 
-  // consumer cursor (all threads); deferred tile completion (thread 0)
-  uint32_t c_tile = 0, c_sub = 0, phases = 0, k = 0;
+  unsigned long long* prof = g_hop_prof;
+  unsigned long long pc[7] = {}, t_a = clock64(), t_b;
+  const unsigned long long t_start = t_a;
+#define HOP_LAP(i)                            \
+  if (prof && threadIdx.x == 0) {             \
+    t_b = clock64();                          \
+    pc[i] += t_b - t_a;                       \
+    t_a = t_b;                                \
+  }
+  // consumer cursor (all threads); per-chunk accumulation of this CTA's checksum share
+  uint32_t c_tile = 0, c_sub = 0, phases = 0, k = 0, n_in_chunk = 0;
   uint64_t s1 = 0, s2 = 0;
-  bool pend = false;
-  uint32_t pend_chunk = 0, pend_rank = 0, groups_after = 0;
-  uint64_t pend_s1 = 0, pend_s2 = 0;
   for (; k < total; ++k) {
     const uint32_t st = k % kHopStages;
     if (threadIdx.x == 0 && issued <= k) {        // pipeline empty: wait for the predecessor
       if (!try_issue(true)) mbar_arrive(&bar[st]);  // failure: release the waiters, exit below
     }
+    HOP_LAP(5)
     mbar_wait(&bar[st], (phases >> st) & 1u);
     phases ^= 1u << st;
+    HOP_LAP(0)
     const HopTile T = tiles[blockIdx.x + c_tile * gridDim.x];
     const uint32_t off = c_sub * kHopSub;
     const uint32_t bytes = min(kHopSub, T.bytes - off);
     const uint8_t* sb = stage_buf + (size_t)st * kHopSub;
-    const uint64_t w0 = (uint64_t)T.word0 + off / 4;
-    for (uint32_t v = threadIdx.x; v < bytes / 16; v += kHopThreads)
-      cks4(w0 + 4ull * v, *reinterpret_cast<const uint4*>(sb + 16 * v), s1, s2);
-    __syncthreads();                               // stage fully read; s_status uniform from here
-    if (s_status != kHopOk) break;
     const RankLink& L = links[T.rank];
-    if (threadIdx.x == 0) {
-      bulk_s2g(L.dst + T.region_off + off, sb, bytes);
-      if (pend) ++groups_after;
-    }
-    if (off + bytes >= T.bytes) {                  // tile end
-      block_reduce2<kHopThreads>(s1, s2, red);
-      if (threadIdx.x == 0) {
-        if (pend) {                                // previous tile still pending: finish it now
-          bulk_wait<1>();
-          hop_complete_tile(meta, links[pend_rank], tiles_per_chunk, pend_chunk, pend_s1, pend_s2, version, err_word);
-        }
-        pend = true;
-        pend_chunk = T.chunk;
-        pend_rank = T.rank;
-        pend_s1 = s1;
-        pend_s2 = s2;
-        groups_after = 0;
+    uint8_t* dst = L.dst + T.region_off + off;
+    const uint64_t w0 = (uint64_t)T.word0 + off / 4;
+    if (s_status == kHopOk) {                      // (on failure the stage holds nothing valid)
+      for (uint32_t v = threadIdx.x; v < bytes / 16; v += kHopThreads) {
+        const uint4 w = lds128(sb + 16 * v);
+        st_v4(dst + 16 * (size_t)v, w);
+        cks4(w0 + 4ull * v, w, s1, s2);
       }
-      s1 = s2 = 0;
-      c_sub = 0;
+    }
+    HOP_LAP(1)
+    __syncthreads();                               // stage fully read; s_status uniform from here
+    HOP_LAP(2)
+    if (s_status != kHopOk) break;
+    if (threadIdx.x == 0)                          // refill: every stage but the ones in flight is free
+      while (issued < k + 1 + kHopStages && try_issue(false)) {}
+    HOP_LAP(4)
+    if (off + bytes >= T.bytes) {                  // tile end
+      ++n_in_chunk;
       ++c_tile;
+      c_sub = 0;
+      const bool chunk_end = c_tile >= my_tiles || tiles[blockIdx.x + c_tile * gridDim.x].chunk != T.chunk;
+      if (chunk_end) {                             // this CTA's last tile of the chunk: flush its share
+        __threadfence_system();                    // this thread's stores before the header / flag
+        block_reduce2<kHopThreads>(s1, s2, red);
+        if (threadIdx.x == 0) hop_flush(meta, L, tiles_per_chunk, T.chunk, n_in_chunk, s1, s2, version, err_word);
+        __syncthreads();                           // red[] reuse
+        s1 = s2 = 0;
+        n_in_chunk = 0;
+      }
+      HOP_LAP(3)
     } else {
       ++c_sub;
     }
-    if (threadIdx.x == 0) {
-      if (pend && groups_after >= 2) {
-        bulk_wait<2>();
-        hop_complete_tile(meta, links[pend_rank], tiles_per_chunk, pend_chunk, pend_s1, pend_s2, version, err_word);
-        pend = false;
-      }
-      bulk_wait_read<1>();                         // store k-1 has read its stage: refill it
-      while (issued < k + kHopStages && try_issue(false)) {}
-    }
   }
-  if (threadIdx.x == 0) {
-    bulk_wait<0>();
-    if (pend && s_status == kHopOk)
-      hop_complete_tile(meta, links[pend_rank], tiles_per_chunk, pend_chunk, pend_s1, pend_s2, version, err_word);
-    if (s_status != kHopOk) {
-      for (uint32_t j = k + 1; j < issued; ++j) {  // drain loads still landing in shared memory
-        const uint32_t st = j % kHopStages;
-        mbar_wait(&bar[st], (phases >> st) & 1u);
-        phases ^= 1u << st;
-      }
-      // abort flag 2 = superseded by a chain rebuild (runtime restarts the fill): exit quietly,
-      // keep the verified chunks and do not poison the successor
-      if (!(s_status == kHopAbort && *(volatile int32_t*)meta.abort_flag == 2))
-        hop_fail(meta, err_word, s_fail_chunk, version, s_status == kHopTimeout ? kHopTimeout : kHopPoison);
-    }
+  if (prof && threadIdx.x == 0) {
+    pc[6] = clock64() - t_start;
+    for (int i = 0; i < 7; ++i) atomicAdd(prof + i, pc[i]);
   }
+#undef HOP_LAP
+  if (threadIdx.x == 0 && s_status != kHopOk) {
+    for (uint32_t j = k + 1; j < issued; ++j) {    // drain loads still landing in shared memory
+      const uint32_t st = j % kHopStages;
+      mbar_wait(&bar[st], (phases >> st) & 1u);
+      phases ^= 1u << st;
+    }
+    // abort flag 2 = superseded by a chain rebuild (runtime restarts the fill): exit quietly, keep
+    // the verified chunks and do not poison the successor
+    if (!(s_status == kHopAbort && *(volatile int32_t*)meta.abort_flag == 2))
+      hop_fail(meta, err_word, s_fail_chunk, version, s_status == kHopTimeout ? kHopTimeout : kHopPoison);
+  }
+}
+
+// LAM_HOP_PROF diagnostics: point g_hop_prof of the current device at a 7-counter buffer (or null).
+int hop_set_profile(unsigned long long* buf) {
+  return (int)cudaMemcpyToSymbol(g_hop_prof, &buf, sizeof buf);
 }
 
 int launch_hop(const HopTile* tiles, uint32_t n_tiles, const RankLink* links, ChunkMeta meta,

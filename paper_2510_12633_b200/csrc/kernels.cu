@@ -51,6 +51,12 @@ __device__ __forceinline__ uint64_t globaltimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+// Release a chunk flag (device memory, read by the next relay over NVLink) and mirror it to host
+// shared memory, where lam_relay_step of any process sees it and drives streaming pulls.
+__device__ __forceinline__ void publish_flag(const ChunkMeta& meta, uint32_t chunk, uint64_t value) {
+  st_release_sys(meta.flags + chunk, value);
+  if (meta.mirror) st_release_sys(meta.mirror + chunk, value);
+}
 
 // fp32 bits -> bf16 bits, round to nearest even; every NaN -> 0x7FC0 (reading R1).
 __device__ __forceinline__ uint32_t rne_bf16(uint32_t u) {
@@ -115,7 +121,7 @@ __device__ void pack_flush(ChunkMeta meta, const uint32_t* units_per_chunk, cons
     h->n = n_total;
     h->bytes = chunk_len[g];
     __threadfence_system();
-    st_release_sys(meta.flags + g, version);
+    publish_flag(meta, g, version);
   }
 }
 
@@ -336,10 +342,10 @@ __global__ void __launch_bounds__(kVerifyThreads) k_verify(const uint8_t* __rest
     h->n = ld_relaxed_sys(&ph->n);
     h->bytes = ld_relaxed_sys(&ph->bytes);
     __threadfence_system();
-    st_release_sys(meta.flags + chunk, version);
+    publish_flag(meta, chunk, version);
   } else {
     atomicCAS(err_word, 0u, (uint32_t)(-LAM_ECHECKSUM));
-    st_release_sys(meta.flags + chunk, version | kPoison);
+    publish_flag(meta, chunk, version | kPoison);
     for (uint32_t j = pos + 1; j < n_my; ++j) st_release_sys(pred_flags + my_chunks[j], version | kPoison);
     __threadfence_system();
   }

@@ -103,6 +103,9 @@ void build_hop_tiles(const ImagePlan& p, const std::vector<int>& ranks, std::vec
 // dst_base[k] = device address of destination k; src rank alignment assumed >= 256 B.
 bool build_copy_tiles(const ImagePlan& p, const std::vector<Tensor>& ts, const lam_tp_layout& L,
                       std::vector<CopyTile>* tiles, uint64_t* bytes, std::string* err);
+// Source chunk of a tile; cut tiles at source-chunk boundaries and order them by chunk.
+uint32_t chunk_of(const ImagePlan& p, const CopyTile& t);
+std::vector<CopyTile> split_by_chunk(const ImagePlan& p, const std::vector<CopyTile>& in);
 
 // ------------------------------------------------------------------------------ kernel entry
 struct ChunkMeta {          // device view of one slot's metadata in a node part
@@ -110,7 +113,9 @@ struct ChunkMeta {          // device view of one slot's metadata in a node part
   lam_chunk_header* hdr;    // [total_chunks]
   uint32_t* cnt;            // [total_chunks]
   int32_t* abort_flag;      // [1]
+  uint64_t* mirror;         // [total_chunks] host-visible copy of flags (shared memory) or null
 };
+constexpr uint32_t kMirrorChunks = 2048;  // chunks per slot mirrored to the host (streaming pulls)
 
 int launch_pack(const PackUnit* units, uint32_t n_units, const float* const* shard_ptrs, uint8_t* dst,
                 ChunkMeta meta, const uint32_t* units_per_chunk, uint64_t version, uint64_t n_total,
@@ -120,6 +125,8 @@ int launch_hop(const HopTile* tiles, uint32_t n_tiles, const RankLink* links, Ch
                uint64_t timeout_ns, int ctas, void* stream);
 int launch_pull(const CopyTile* tiles, uint32_t n_tiles, const uint8_t* const* rank_base, int ctas,
                 void* stream);
+// Diagnostics (LAM_HOP_PROF=1): 7 per-device cycle counters accumulated by k_hop's thread 0.
+int hop_set_profile(unsigned long long* buf);
 // One-thread kernel: spin until (int64)(*flag - v) >= 0 or timeout (fallback for stream memory ops).
 int launch_wait_flag(const uint64_t* flag, uint64_t v, uint64_t timeout_ns, void* stream);
 // Copy-engine hop: verify chunk `chunk` (len bytes at `data`, already copied from the predecessor)

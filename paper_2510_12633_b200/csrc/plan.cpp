@@ -265,6 +265,72 @@ bool build_copy_tiles(const ImagePlan& p, const std::vector<Tensor>& ts, const l
   return true;
 }
 
+// Source chunk of a copy tile (tiles never straddle chunks after split_by_chunk).
+uint32_t chunk_of(const ImagePlan& p, const CopyTile& t) {
+  return (uint32_t)(p.chunk_base[t.src_rank] + t.src_off / p.C);
+}
+
+// Cut copy tiles at source-chunk boundaries (whole rows where possible, a row crossing a boundary
+// is split in two) and order them by chunk, so a pull can be launched chunk by chunk.
+std::vector<CopyTile> split_by_chunk(const ImagePlan& p, const std::vector<CopyTile>& in) {
+  const uint64_t C = p.C;
+  std::vector<CopyTile> out;
+  out.reserve(in.size());
+  auto piece = [&](const CopyTile& t, uint64_t r0, uint64_t nrows) {
+    CopyTile u = t;
+    u.src_off = t.src_off + r0 * t.src_pitch;
+    u.dst = t.dst + r0 * t.dst_pitch;
+    u.rows = (uint32_t)nrows;
+    if (nrows == 1) u.src_pitch = u.dst_pitch = 0;
+    out.push_back(u);
+  };
+  for (const CopyTile& t : in) {
+    if (t.rows == 1) {  // cut the row at every chunk boundary it crosses (a row may span many chunks)
+      auto widest = [](uint64_t x) -> uint32_t { return x % 16 == 0 ? 16 : (x % 4 == 0 ? 4 : 2); };
+      uint64_t a = t.src_off, dst = t.dst, left = t.row_bytes;
+      while (left > 0) {
+        const uint64_t n = std::min<uint64_t>(left, (a / C + 1) * C - a);
+        CopyTile u = t;
+        u.src_off = a;
+        u.dst = dst;
+        u.row_bytes = (uint32_t)n;
+        u.src_pitch = u.dst_pitch = 0;
+        u.align = n == t.row_bytes ? t.align : std::min(t.align, widest(u.src_off | u.dst | u.row_bytes));
+        out.push_back(u);
+        a += n;
+        dst += n;
+        left -= n;
+      }
+      continue;
+    }
+    uint64_t r0 = 0;
+    for (uint64_t r = 0; r < t.rows; ++r) {
+      const uint64_t a = t.src_off + r * t.src_pitch, b = a + t.row_bytes;
+      const bool crosses = a / C != (b - 1) / C;
+      const bool new_chunk = r > r0 && a / C != (t.src_off + r0 * t.src_pitch) / C;
+      if (new_chunk || crosses) {
+        if (r > r0) piece(t, r0, r - r0);
+        r0 = r;
+      }
+      if (crosses) {
+        CopyTile one = t;
+        one.src_off = a;
+        one.dst = t.dst + r * t.dst_pitch;
+        one.rows = 1;
+        one.src_pitch = one.dst_pitch = 0;
+        std::vector<CopyTile> tmp{one};
+        std::vector<CopyTile> cut = split_by_chunk(p, tmp);
+        out.insert(out.end(), cut.begin(), cut.end());
+        r0 = r + 1;
+      }
+    }
+    if (t.rows > r0) piece(t, r0, t.rows - r0);
+  }
+  std::stable_sort(out.begin(), out.end(),
+                   [&](const CopyTile& x, const CopyTile& y) { return chunk_of(p, x) < chunk_of(p, y); });
+  return out;
+}
+
 }  // namespace lam
 
 using namespace lam;
@@ -293,6 +359,7 @@ extern "C" int64_t lam_plan_copy_tiles(const lam_model_dims* d, int32_t layout, 
   uint64_t bytes = 0;
   std::string err;
   if (!build_copy_tiles(p, ts, *L, &tiles, &bytes, &err)) return LAM_EINVAL;
+  tiles = split_by_chunk(p, tiles);
   if (out) {
     for (size_t i = 0; i < tiles.size() && (int64_t)i < cap; ++i) {
       const CopyTile& t = tiles[i];

@@ -75,6 +75,7 @@ struct Part {
   std::vector<HopTile> h_tiles;      // host copy of the full tile list
   HopTile* d_resume = nullptr;       // tiles of the chunks still missing after a rebuild
   RankLink* d_links_dyn = nullptr;   // links to a predecessor other than node - 1
+  unsigned long long* prof_host = nullptr;  // LAM_HOP_PROF counters (host-mapped)
 };
 
 struct RankPub {   // per local actor rank (node 0)
@@ -90,9 +91,11 @@ struct RankPub {   // per local actor rank (node 0)
 };
 
 struct PullPlan {
-  CopyTile* d_tiles = nullptr;
+  CopyTile* d_tiles = nullptr;        // ordered by source chunk
   uint32_t n_tiles = 0;
   uint64_t bytes = 0, local_bytes = 0, remote_bytes = 0;
+  std::vector<uint32_t> chunk_ids;    // source chunks in order
+  std::vector<uint32_t> chunk_begin;  // [chunk_ids.size() + 1] tile ranges per chunk
 };
 
 struct PendingPull {
@@ -131,6 +134,19 @@ struct lam_ctx {
   lam_status pending_error = LAM_OK;
   uint64_t timeout_ns = 60ull * 1000000000ull;
   int pack_ctas = 0, hop_ctas = 0, pull_ctas = 0;
+  uint64_t* mirror_dev = nullptr;     // device view of shm->chunk_done (null: no streaming pulls)
+  bool shm_registered = false;
+  struct StreamPull {                 // lam_pull_stream in progress (per rollout)
+    bool active = false;
+    int node = 0, slot = 0, device = 0;
+    uint64_t v = 0;
+    lam_status status = LAM_OK;
+    PullPlan* plan = nullptr;
+    uint32_t next = 0;                // next chunk (index into plan->chunk_ids) to launch
+    cudaStream_t stream = nullptr;
+    cudaEvent_t done = nullptr;
+  };
+  std::vector<StreamPull> streams;    // [n_rollouts]
   // kernel timing (lam_set_profiling)
   bool profiling = false;
   struct Timed { int kind, dev; cudaEvent_t a, b; };
@@ -197,6 +213,7 @@ ChunkMeta meta_of(const lam_ctx* c, const Part& p, int slot) {
   cm.hdr = reinterpret_cast<lam_chunk_header*>(m + c->sm.hdr);
   cm.cnt = reinterpret_cast<uint32_t*>(m + c->sm.cnt);
   cm.abort_flag = reinterpret_cast<int32_t*>(m + c->sm.abort);
+  cm.mirror = c->mirror_dev ? c->mirror_dev + ((uint64_t)p.node * LAM_MAX_SLOTS + slot) * kShmMirrorChunks : nullptr;
   return cm;
 }
 
@@ -307,6 +324,13 @@ lam_status alloc_parts(lam_ctx* c) {
       p.n_tiles = (uint32_t)tiles.size();
       CK(cudaMalloc(&p.d_tiles, sizeof(HopTile) * std::max<size_t>(tiles.size(), 1)));
       if (!tiles.empty()) CK(cudaMemcpy(p.d_tiles, tiles.data(), sizeof(HopTile) * tiles.size(), cudaMemcpyHostToDevice));
+      if (getenv("LAM_HOP_PROF")) {
+        unsigned long long* dptr = nullptr;
+        CK(cudaHostAlloc(&p.prof_host, 8 * 8, cudaHostAllocMapped | cudaHostAllocPortable));
+        memset(p.prof_host, 0, 64);
+        CK(cudaHostGetDevicePointer((void**)&dptr, p.prof_host, 0));
+        if (hop_set_profile(dptr)) return LAM_ECUDA;
+      }
       CK(cudaMalloc(&p.d_resume, sizeof(HopTile) * std::max<size_t>(tiles.size(), 1)));
       CK(cudaMalloc(&p.d_links_dyn, sizeof(RankLink) * N));
       p.h_tiles = tiles;
@@ -654,6 +678,43 @@ lam_status launch_hop_part(lam_ctx* c, Part& p, int s, bool* launched) {
   return LAM_OK;
 }
 
+// Streaming pull progress (lam_pull_stream): launch the reshard of every newly verified chunk (the
+// producers mirror chunk flags into the shared control block), then close with the done event.
+lam_status stream_progress(lam_ctx* c, int rid, int* transitions) {
+  lam_ctx::StreamPull& sp = c->streams[rid];
+  if (!sp.active) return LAM_OK;
+  Shm* sh = c->shm;
+  const ShmSlot& sl = sh->node[sp.node].slot[sp.slot];
+  CK(cudaSetDevice(sp.device));
+  const bool failed = sl.version != sp.v || (sl.state != S_FILLING && sl.state != S_COMPLETE) || sh->node[sp.node].dead;
+  const uint32_t n = (uint32_t)sp.plan->chunk_ids.size();
+  if (!failed) {
+    const uint64_t* mir = sh->chunk_done[sp.node][sp.slot];
+    const uint32_t first = sp.next;
+    while (sp.next < n && (sl.state == S_COMPLETE ||
+                           __atomic_load_n(mir + sp.plan->chunk_ids[sp.next], __ATOMIC_ACQUIRE) == sp.v))
+      ++sp.next;
+    if (sp.next > first) {
+      auto rb = c->d_rank_base.find({sp.node * LAM_MAX_SLOTS + sp.slot, sp.device});
+      const uint32_t b = sp.plan->chunk_begin[first], e = sp.plan->chunk_begin[sp.next];
+      cudaEvent_t t0 = prof_begin(c, sp.device, sp.stream);
+      if (launch_pull(sp.plan->d_tiles + b, e - b, rb->second, c->pull_ctas, sp.stream)) return LAM_ECUDA;
+      prof_end(c, 2, sp.device, sp.stream, t0);
+      (*transitions)++;
+    }
+    if (sp.next < n) return LAM_OK;
+  } else {
+    sp.status = LAM_ECHECKSUM;
+  }
+  if (sp.done) CK(cudaEventRecord(sp.done, sp.stream));
+  cudaEvent_t ev = get_event(c, sp.device);
+  CK(cudaEventRecord(ev, sp.stream));
+  c->pending.push_back({ev, sp.node, sp.slot, sp.device});  // unpin once the stream gets there
+  sp.active = false;
+  (*transitions)++;
+  return LAM_OK;
+}
+
 lam_status step_locked(lam_ctx* c, int* transitions, bool* busy) {
   Shm* sh = c->shm;
   const int S = c->S;
@@ -687,6 +748,14 @@ lam_status step_locked(lam_ctx* c, int* transitions, bool* busy) {
       cudaError_t q = cudaEventQuery(p.done_ev[s]);
       if (q == cudaErrorNotReady) { *busy = true; continue; }
       if (q != cudaSuccess) return LAM_ECUDA;
+      if (p.prof_host) {
+        const unsigned long long* q = p.prof_host;
+        const double tot = (double)(q[6] ? q[6] : 1);
+        fprintf(stderr, "k_hop node %d dev %d: wait %.1f%% cks %.1f%% bar %.1f%% tile %.1f%% refill %.1f%% spin %.1f%% (%.2f Gcyc)\n",
+                p.node, p.device, 100 * q[0] / tot, 100 * q[1] / tot, 100 * q[2] / tot, 100 * q[3] / tot,
+                100 * q[4] / tot, 100 * q[5] / tot, tot / 1e9);
+        memset(p.prof_host, 0, 64);
+      }
       const lam_status e = p.err_host[s] ? -(lam_status)p.err_host[s] : LAM_OK;
       if (ctl::part_done(sh, p.node, s, p.inflight_version[s], (int)c->node_parts[p.node].size(), e,
                          p.launched_epoch[s])) {
@@ -695,6 +764,13 @@ lam_status step_locked(lam_ctx* c, int* transitions, bool* busy) {
       }
       p.inflight_version[s] = 0;
     }
+  }
+  // (2b) streaming pulls of this process's rollouts
+  for (int rid = 0; rid < (int)c->streams.size(); ++rid) {
+    if (!c->streams[rid].active) continue;
+    lam_status st = stream_progress(c, rid, transitions);
+    if (st != LAM_OK) return st;
+    if (c->streams[rid].active) *busy = true;
   }
   // (3) pull pins
   for (size_t i = 0; i < c->pending.size();) {
@@ -747,9 +823,18 @@ lam_status get_plan(lam_ctx* c, const lam_rollout_desc& ro, const lam_tp_layout&
     fprintf(stderr, "liblam: lam_pull: %s\n", err.c_str());
     return LAM_EINVAL;
   }
+  tiles = split_by_chunk(c->plan, tiles);
   PullPlan pp;
   pp.n_tiles = (uint32_t)tiles.size();
   pp.bytes = bytes;
+  for (uint32_t i = 0; i < tiles.size(); ++i) {
+    const uint32_t g = chunk_of(c->plan, tiles[i]);
+    if (pp.chunk_ids.empty() || pp.chunk_ids.back() != g) {
+      pp.chunk_ids.push_back(g);
+      pp.chunk_begin.push_back(i);
+    }
+  }
+  pp.chunk_begin.push_back((uint32_t)tiles.size());
   for (const CopyTile& t : tiles) {
     const Part& q = c->parts[c->node_rank_part[ro.node][t.src_rank]];
     (q.device == ro.device ? pp.local_bytes : pp.remote_bytes) += (uint64_t)t.rows * t.row_bytes;
@@ -838,6 +923,21 @@ extern "C" lam_status lam_init(const lam_config* cfg, lam_ctx** out) {
   st = setup_shm(c.get());
   if (st != LAM_OK) return st;
   if (cfg->n_procs == 1 || cfg->proc_rank == 0) ctl::init(c->shm, c->n_nodes);
+  c->streams.resize(cfg->n_rollouts);
+  // map the control block for the producer kernels' chunk-flag mirror (streaming pulls)
+  for (int d = 0; d < LAM_MAX_DEVICES; ++d)
+    if (owns(c.get(), d)) {
+      cudaSetDevice(d);
+      break;
+    }
+  if (c->plan.total_chunks <= kShmMirrorChunks &&
+      cudaHostRegister(c->shm, sizeof(Shm), cudaHostRegisterMapped | cudaHostRegisterPortable) == cudaSuccess) {
+    c->shm_registered = true;
+    void* dp = nullptr;
+    if (cudaHostGetDevicePointer(&dp, c->shm, 0) == cudaSuccess)
+      c->mirror_dev = reinterpret_cast<Shm*>(dp)->chunk_done[0][0];
+  }
+  cudaGetLastError();
   st = alloc_parts(c.get());
   if (st != LAM_OK) {
     lam_destroy(c.release());
@@ -1037,6 +1137,60 @@ extern "C" lam_status lam_pull(lam_ctx* c, int32_t rid, const lam_tp_layout* L, 
   return LAM_OK;
 }
 
+extern "C" lam_status lam_pull_stream(lam_ctx* c, int32_t rid, const lam_tp_layout* L, void* stream, void* done,
+                                      uint64_t min_version, uint64_t* vout) {
+  if (vout) *vout = 0;
+  if (!c || !c->connected || !L || rid < 0 || rid >= c->cfg.n_rollouts) return LAM_EINVAL;
+  const lam_rollout_desc ro = c->cfg.rollout[rid];
+  if (!owns(c, ro.device)) return LAM_EINVAL;
+  CK(cudaSetDevice(ro.device));
+  std::string key = layout_key(ro.node, *L);
+  Lock l(c->shm);
+  lam_ctx::StreamPull& sp = c->streams[rid];
+  if (sp.active) return LAM_EBUSY;
+  ShmNode& n = c->shm->node[ro.node];
+  if (n.dead) return LAM_ENOVERSION;
+  if (n.latest && n.latest >= min_version) {         // already complete: an ordinary pull
+    lam_status st = lam_pull(c, rid, L, stream, vout);
+    if (st == LAM_OK && done) CK(cudaEventRecord((cudaEvent_t)done, (cudaStream_t)stream));
+    sp.v = vout ? *vout : 0;
+    sp.status = LAM_OK;
+    return st;
+  }
+  int s = -1;
+  for (int i = 0; i < c->S; ++i)
+    if (n.slot[i].state == S_FILLING && n.slot[i].version >= min_version) s = i;
+  if (s < 0 || !c->mirror_dev || !c->d_rank_base.count({ro.node * LAM_MAX_SLOTS + s, ro.device}))
+    return LAM_ENOVERSION;
+  PullPlan* pp = nullptr;
+  lam_status pst = get_plan(c, ro, *L, key, &pp);
+  if (pst != LAM_OK) return pst;
+  n.slot[s].readers++;                                 // pin the version being received
+  sp.active = true;
+  sp.node = ro.node;
+  sp.slot = s;
+  sp.device = ro.device;
+  sp.v = n.slot[s].version;
+  sp.status = LAM_OK;
+  sp.plan = pp;
+  sp.next = 0;
+  sp.stream = (cudaStream_t)stream;
+  sp.done = (cudaEvent_t)done;
+  c->shm->stats.pulls++;
+  if (vout) *vout = sp.v;
+  int t = 0;
+  return stream_progress(c, rid, &t);
+}
+
+extern "C" lam_status lam_pull_state(lam_ctx* c, int32_t rid, uint64_t* vout, int32_t* state) {
+  if (!c || rid < 0 || rid >= c->cfg.n_rollouts || !state) return LAM_EINVAL;
+  Lock l(c->shm);
+  const lam_ctx::StreamPull& sp = c->streams[rid];
+  if (vout) *vout = sp.v;
+  *state = sp.active ? 1 : (sp.status < 0 ? sp.status : 0);
+  return LAM_OK;
+}
+
 extern "C" lam_status lam_fail_node(lam_ctx* c, int32_t node) {
   if (!c || !c->connected || node <= 0 || node >= c->n_nodes) return LAM_EINVAL;
   Lock l(c->shm);
@@ -1217,6 +1371,7 @@ extern "C" void lam_destroy(lam_ctx* c) {
   for (auto& kv : c->tev_pool)
     for (cudaEvent_t e : kv.second) cudaEventDestroy(e);
   for (auto& t : c->timed) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }
+  if (c->shm_registered) cudaHostUnregister(c->shm);
   shm_release(c->shm, c->cfg.shm_name, c->shm_mapped, c->shm_owner);
   delete c;
 }

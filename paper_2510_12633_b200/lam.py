@@ -322,6 +322,28 @@ class Context:
         _check(self.L.lam_latest(self.h, node, C.byref(v)), "lam_latest", ok=(LAM_OK, LAM_ENOVERSION))
         return v.value
 
+    def pull_stream(self, rollout: int, layout: TPLayout, stream: int = 0, done_event: int | None = None,
+                    min_version: int = 1) -> int:
+        """lam_pull_stream: pull the first version >= min_version, chunk by chunk as it arrives.
+        Returns the version (0 if none is complete or in flight); LAM_EBUSY raises."""
+        f = self.L.lam_pull_stream
+        f.restype = C.c_int32
+        f.argtypes = [C.c_void_p, C.c_int32, C.POINTER(lam_tp_layout), C.c_void_p, C.c_void_p, C.c_uint64,
+                      C.POINTER(C.c_uint64)]
+        v = C.c_uint64()
+        st = f(self.h, rollout, C.byref(layout.c), stream, done_event, min_version, C.byref(v))
+        _check(st, "lam_pull_stream", ok=(LAM_OK, LAM_ENOVERSION))
+        return v.value
+
+    def pull_state(self, rollout: int) -> tuple[int, int]:
+        """(version, state): state 1 = chunks still arriving, 0 = done, < 0 = failed."""
+        f = self.L.lam_pull_state
+        f.restype = C.c_int32
+        f.argtypes = [C.c_void_p, C.c_int32, C.POINTER(C.c_uint64), C.POINTER(C.c_int32)]
+        v, s = C.c_uint64(), C.c_int32()
+        _check(f(self.h, rollout, C.byref(v), C.byref(s)), "lam_pull_state")
+        return v.value, s.value
+
     def fail_node(self, node: int) -> None:
         """Declare relay `node` failed: O(1) chain rebuild, successors resume (lam_fail_node)."""
         f = self.L.lam_fail_node

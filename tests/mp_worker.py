@@ -38,6 +38,7 @@ def main():
     ap.add_argument("--versions", type=int, default=2)
     ap.add_argument("--chunk-kb", type=int, default=64)
     ap.add_argument("--hop-mode", type=int, default=0)
+    ap.add_argument("--stream", action="store_true", help="rollouts use lam_pull_stream during the broadcast")
     a = ap.parse_args()
     import faulthandler
     faulthandler.dump_traceback_later(float(os.environ.get("LAM_MP_WATCHDOG", "500")), exit=True)
@@ -76,6 +77,21 @@ def main():
         for r in my_ranks:
             assert ctx.publish(v, r, shards[r].shards(), torch.cuda.current_stream().cuda_stream) == lam.LAM_OK
         t0 = time.time()
+        streamed = {}
+        if a.stream:                                # start every rollout's pull while v is in flight
+            ss = torch.cuda.Stream()
+            todo = list(mine)
+            while todo or any(ctx.pull_state(rid)[1] == 1 for rid in streamed):
+                ctx.relay_step()
+                for rid in list(todo):
+                    node, dev, tp, tr = ro[rid]
+                    rb = RolloutBuffers(MODELS[a.model], tp, tr, dev) if rid not in streamed else streamed[rid]
+                    streamed[rid] = rb
+                    if ctx.pull_stream(rid, rb.tp, ss.cuda_stream, None, v):
+                        todo.remove(rid)
+                if time.time() - t0 > 120:
+                    raise TimeoutError(f"rank {rank}: streaming pulls of v{v} never finished")
+            ss.synchronize()
         while not all(ctx.latest(n) >= v for n in range(len(T["relays"]) + 1)):
             ctx.relay_step()
             if time.time() - t0 > 120:
@@ -101,9 +117,13 @@ def main():
         s = torch.cuda.Stream()
         for rid in mine:
             node, dev, tp, tr = ro[rid]
-            rb = RolloutBuffers(MODELS[a.model], tp, tr, dev)
-            got_v = ctx.pull(rid, rb.tp, s.cuda_stream)
-            s.synchronize()
+            if rid in streamed:
+                rb = streamed[rid]
+                got_v = ctx.pull_state(rid)[0]
+            else:
+                rb = RolloutBuffers(MODELS[a.model], tp, tr, dev)
+                got_v = ctx.pull(rid, rb.tp, s.cuda_stream)
+                s.synchronize()
             if got_v != v:
                 failures.append(f"rollout {rid}: pulled {got_v}, expected {v}")
             if a.model == "tiny":

@@ -101,6 +101,15 @@ def test_copy_plan_reproduces_oracle_pull(layout, N, C, tp):
             o += -(-x.rows * x.cols * 2 // 256) * 256
         tpl = lam.TPLayout(tp, rank, [(x.parts, base + offs[x.name], 0) for x in layout_c])
         tiles = lam.plan_copy_tiles(MODELS["tiny"], LAYOUT[layout], N, C, tpl)
+        # streaming pulls launch tiles chunk by chunk: every tile must lie inside one source chunk,
+        # and tiles must come in chunk order
+        chunks = []
+        for t in tiles:
+            lo = t.src_off
+            hi = t.src_off + (t.rows - 1) * t.src_pitch + t.row_bytes
+            assert lo // C == (hi - 1) // C, (t.src_rank, lo, hi, C)
+            chunks.append(plan.chunk_base[t.src_rank] + lo // C)
+        assert chunks == sorted(chunks)
         out = np.full(o, 0xAB, dtype=np.uint8)
         _execute_plan(tiles, rank_base, img, base, out)
         for x in layout_c:

@@ -35,6 +35,10 @@ CASES = [  # (min GPUs, args)
     (2, ["--config", "chain", "--model", "7b", "--chunk-kb", str(128 << 10)]),
     (4, ["--config", "chain", "--model", "tiny", "--versions", "3", "--chunk-kb", "16", "--hop-mode", "1"]),
     (4, ["--config", "relay-tp", "--model", "tiny", "--tp", "2", "--hop-mode", "1"]),
+    (4, ["--config", "chain", "--model", "tiny", "--versions", "3", "--chunk-kb", "16", "--stream"]),
+    (4, ["--config", "colocated", "--model", "tiny", "--tp", "4", "--stream"]),
+    (4, ["--config", "relay-tp", "--model", "tiny", "--tp", "2", "--stream"]),
+    (2, ["--config", "chain", "--model", "7b", "--chunk-kb", str(128 << 10), "--stream"]),
 ]
 
 

@@ -1,0 +1,119 @@
+"""Streaming pulls (lam_pull_stream): a waiting rollout reshards a version chunk by chunk while its
+relay is still receiving it; the result must be exactly the oracle's pull of that version, and a
+version that fails at the relay must be reported, never served."""
+import time
+
+import numpy as np
+import pytest
+import torch
+
+from oracle.model import MODELS as OMODELS
+from oracle.tp import direct_pull, dst_elements
+from paper_2510_12633_b200 import lam
+from paper_2510_12633_b200.workload import MODELS, ActorShard, RolloutBuffers
+from synth import SEED
+
+pytestmark = pytest.mark.gpu
+
+
+def drive(ctx, rid, timeout=120):
+    t0 = time.time()
+    while True:
+        ctx.relay_step()
+        v, st = ctx.pull_state(rid)
+        if st <= 0:
+            return v, st
+        assert time.time() - t0 < timeout, "streaming pull never finished"
+
+
+@pytest.mark.parametrize("tp", [1, 2])
+def test_stream_pull_tiny_chain(tp):
+    n = torch.cuda.device_count()
+    devs = [1 % n, 2 % n]
+    od = OMODELS["tiny"]
+    ctx = lam.Context(lam.Config(model=MODELS["tiny"], relays=[[devs[0]], [devs[1]]],
+                                 rollouts=[(2, devs[1]), (0, 0)], chunk_bytes=8 * 4096))
+    shard = ActorShard(MODELS["tiny"], 1, 0, 0)
+    rb = RolloutBuffers(MODELS["tiny"], tp, tp - 1, devs[1])
+    s = torch.cuda.Stream(device=devs[1])
+    for v in (1, 2, 3):
+        shard.fill(SEED, v, specials=True)
+        torch.cuda.synchronize()
+        rb.fill_(0xFFFF)
+        torch.cuda.synchronize()
+        assert ctx.publish(v, 0, shard.shards()) == lam.LAM_OK
+        got = 0
+        t0 = time.time()
+        while got == 0:                                     # wait until relay 2 starts receiving v
+            ctx.relay_step()
+            got = ctx.pull_stream(0, rb.tp, s.cuda_stream, None, v)
+            assert time.time() - t0 < 60
+        assert got == v
+        assert drive(ctx, 0) == (v, 0)
+        s.synchronize()
+        want = direct_pull(od, tp, tp - 1, SEED, v, specials=True)
+        for name, t in rb.bufs.items():
+            g = t.view(torch.int16).cpu().numpy().view(np.uint16)
+            assert np.array_equal(g, want[name].reshape(g.shape)), (v, name)
+        for _ in range(100000):
+            if ctx.relay_step()[0] == lam.LAM_IDLE:
+                break
+    ctx.close()
+
+
+def test_stream_pull_from_master_while_packing():
+    od = OMODELS["7b"]
+    ctx = lam.Context(lam.Config(model=MODELS["7b"], rollouts=[(0, 0)], chunk_bytes=128 << 20))
+    shard = ActorShard(MODELS["7b"], 1, 0, 0)
+    shard.fill(SEED, 4)
+    rb = RolloutBuffers(MODELS["7b"], 1, 0, 0)
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+    done = torch.cuda.Event()
+    assert ctx.publish(4, 0, shard.shards()) == lam.LAM_OK
+    assert ctx.pull_stream(0, rb.tp, s.cuda_stream, done.cuda_event, 4) == 4   # FILLING at node 0
+    assert drive(ctx, 0) == (4, 0)
+    done.synchronize()
+    rng = np.random.default_rng(7)
+    for name, t in rb.bufs.items():
+        idx = rng.integers(0, t.numel(), 64)
+        g = t.view(-1).view(torch.int16).cpu().numpy().view(np.uint16)[idx]
+        assert np.array_equal(g, dst_elements(od, 1, 0, name, idx, SEED, 4)), name
+    ctx.close()
+
+
+def test_stream_pull_of_a_corrupt_version_fails():
+    ctx = lam.Context(lam.Config(model=MODELS["tiny"], relays=[[0]], rollouts=[(1, 0)], chunk_bytes=16 * 4096))
+    shard = ActorShard(MODELS["tiny"], 1, 0, 0)
+    shard.fill(SEED, 1)
+    torch.cuda.synchronize()
+    assert ctx.publish(1, 0, shard.shards()) == lam.LAM_OK
+    torch.cuda.synchronize()                                # packed; relay hop not launched yet
+    ptr = ctx.debug_region(0, 1, 0) + 3 * 16 * 4096 + 100
+    byte = torch.empty(1, dtype=torch.uint8, device="cuda:0")
+    import ctypes
+    cp = ctypes.CDLL("libcudart.so.12").cudaMemcpy
+    assert cp(ctypes.c_void_p(byte.data_ptr()), ctypes.c_void_p(ptr), ctypes.c_size_t(1), 4) == 0
+    byte ^= 0xFF
+    assert cp(ctypes.c_void_p(ptr), ctypes.c_void_p(byte.data_ptr()), ctypes.c_size_t(1), 4) == 0
+    rb = RolloutBuffers(MODELS["tiny"], 1, 0, 0)
+    got = 0
+    for _ in range(1000):
+        try:
+            ctx.relay_step()
+        except lam.LamError:
+            pass
+        got = got or ctx.pull_stream(0, rb.tp, 0, None, 1)
+        if got:
+            break
+    assert got == 1
+    t0 = time.time()
+    while ctx.pull_state(0)[1] == 1:
+        try:
+            ctx.relay_step()
+        except lam.LamError as e:
+            assert e.status == lam.LAM_ECHECKSUM
+        assert time.time() - t0 < 60
+    assert ctx.pull_state(0) == (1, lam.LAM_ECHECKSUM)
+    assert ctx.latest(1) == 0
+    ctx.close()
