@@ -47,6 +47,8 @@ def parse():
                     help="relay hop: TMA kernel or copy engines + k_verify")
     ap.add_argument("--no-stream-pull", action="store_true",
                     help="rollouts pull only after their relay committed (no chunk-by-chunk reshard)")
+    ap.add_argument("--no-subscribe", action="store_true",
+                    help="colocated rollouts pull after the pack instead of being written by it")
     ap.add_argument("--pack-ctas", type=int, default=0)
     ap.add_argument("--pull-ctas", type=int, default=0)
     ap.add_argument("--e2e-steps", type=int, default=2)
@@ -275,16 +277,23 @@ def main():
     torch.cuda.synchronize()
     state = {"v": 0}
 
+    # colocated rollouts (node 0, an actor GPU, TP=1) are written by the pack itself (lam_subscribe)
+    subs = [] if args.no_subscribe else [rid for rid in mine if rollouts[rid][0] == 0 and rollouts[rid][2] == 1
+                                          and rollouts[rid][1] in T["actors"]]
+    sub_done = {rid: torch.cuda.Event() for rid in subs}
+
     def step(h2d=None, d2h=None):
         state["v"] += 1
         v = state["v"]
+        for rid in subs:
+            ctx.subscribe(rid, bufs[rid].tp, sub_done[rid].cuda_event)
         for r in my_ranks:
             if h2d is not None:                        # e2e: the step's inputs arrive from host memory
                 with torch.cuda.stream(actor_stream):
                     shards[r].buf.copy_(h2d[r], non_blocking=True)
             while ctx.publish(v, r, shards[r].shards(), actor_stream.cuda_stream) == lam.LAM_EBUSY:
                 ctx.relay_step()
-        pending, streaming = list(mine), []
+        pending, streaming = [rid for rid in mine if rid not in subs], list(subs)
         while True:
             ctx.relay_step()
             for rid in list(pending):
@@ -297,7 +306,9 @@ def main():
                     pending.remove(rid)
                     streaming.append(rid)
             for rid in list(streaming):
-                if args.no_stream_pull or ctx.pull_state(rid)[1] == 0:
+                if (args.no_stream_pull and rid not in subs) or ctx.pull_state(rid)[1] == 0:
+                    if rid in subs:                         # written by the pack on the side stream
+                        stream.wait_event(sub_done[rid])
                     if d2h is not None:
                         with torch.cuda.stream(stream):
                             for name, t in bufs[rid].bufs.items():
@@ -350,8 +361,9 @@ def main():
     # per-rank roofline candidates of this rank's dominant kernel work
     cand = []
     if avg["pack"]:
-        b = 6.0 * sum(sh.numel for sh in shards.values())
-        cand.append(dict(kernel="k_pack", ms=avg["pack"], bound="hbm", bytes=b))
+        # 4 B fp32 read + 2 B bf16 slot write per param, + 2 B per param into a colocated subscriber
+        b = (8.0 if subs else 6.0) * sum(sh.numel for sh in shards.values())
+        cand.append(dict(kernel="k_pack" + ("+subscriber" if subs else ""), ms=avg["pack"], bound="hbm", bytes=b))
     if avg["hop"]:
         part_bytes = sum(info.snapshot_bytes for _ in [0]) if args.config == "chain" else M / max(1, T["fsdp"])
         cand.append(dict(kernel="k_hop", ms=avg["hop"], bound="nvlink", bytes=float(part_bytes)))

@@ -224,6 +224,15 @@ lam_status lam_pull(lam_ctx*, int32_t rollout_id, const lam_tp_layout* layout, v
  * >= min_version is complete or in flight; LAM_EBUSY if the rollout has a streaming pull running. */
 lam_status lam_pull_stream(lam_ctx*, int32_t rollout_id, const lam_tp_layout* layout, void* stream,
                            void* done_event, uint64_t min_version, uint64_t* version_out);
+/* Colocated subscription: rollout `rollout_id` sits on an actor GPU (node 0, same device) with a
+ * TP=1 dense layout covering every tensor.  The next version published by the actor rank(s) on that
+ * GPU is also written into the rollout's buffers by the pack kernel itself, in the same pass (the
+ * bf16 bytes go to the master slot and to the rollout: 8 instead of 4 + 6 B/param of HBM traffic).
+ * `done_event` (caller-created, may be NULL) is recorded after that pack; lam_pull_state then
+ * reports (version, 0).  One-shot: subscribe again for the next version.  LAM_EINVAL if the rollout
+ * or layout does not qualify (use lam_pull / lam_pull_stream instead). */
+lam_status lam_subscribe(lam_ctx*, int32_t rollout_id, const lam_tp_layout* layout, void* done_event);
+
 /* State of the rollout's streaming pull: 1 = chunks still arriving, 0 = all enqueued (or none),
  * < 0 = the version failed at the node (LAM_ECHECKSUM / LAM_ETIMEOUT): buffers hold no valid version. */
 lam_status lam_pull_state(lam_ctx*, int32_t rollout_id, uint64_t* version_out, int32_t* state);

@@ -58,6 +58,21 @@ __device__ __forceinline__ void publish_flag(const ChunkMeta& meta, uint32_t chu
   if (meta.mirror) st_release_sys(meta.mirror + chunk, value);
 }
 
+// 16 bytes to an address that may be only 2-B aligned (colocated subscriber of an odd FSDP split)
+__device__ __forceinline__ void st_v4_any(uint8_t* p, uint4 v) {
+  if ((((uintptr_t)p) & 15) == 0) {
+    st_v4(p, v);
+  } else if ((((uintptr_t)p) & 3) == 0) {
+    uint32_t* q = reinterpret_cast<uint32_t*>(p);
+    q[0] = v.x; q[1] = v.y; q[2] = v.z; q[3] = v.w;
+  } else {
+    uint16_t* q = reinterpret_cast<uint16_t*>(p);
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) { q[2 * i] = (uint16_t)w[i]; q[2 * i + 1] = (uint16_t)(w[i] >> 16); }
+  }
+}
+
 // fp32 bits -> bf16 bits, round to nearest even; every NaN -> 0x7FC0 (reading R1).
 __device__ __forceinline__ uint32_t rne_bf16(uint32_t u) {
   uint32_t r = (u + 0x7FFFu + ((u >> 16) & 1u)) >> 16;
@@ -130,7 +145,8 @@ __global__ void __launch_bounds__(kPackThreads) k_pack(const PackUnit* __restric
                                                        uint8_t* __restrict__ dst, ChunkMeta meta,
                                                        const uint32_t* __restrict__ units_per_chunk,
                                                        uint64_t version, uint64_t n_total,
-                                                       const uint64_t* __restrict__ chunk_len) {
+                                                       const uint64_t* __restrict__ chunk_len,
+                                                       uint8_t* const* __restrict__ sub_dst) {
   __shared__ uint64_t red[2][kPackThreads / 32];
   // Per-CTA accumulation: the CTA's checksum and unit count for its current chunk are flushed once
   // when it moves on to another chunk (units are chunk-ordered), not per unit — the per-unit atomics
@@ -151,6 +167,8 @@ __global__ void __launch_bounds__(kPackThreads) k_pack(const PackUnit* __restric
     }
     const float* src = shard_ptrs[u.shard] + u.src_elem;
     uint8_t* out = dst + u.dst_off;
+    // colocated subscriber (lam_subscribe): the same bf16 bytes also go to its TP=1 buffer
+    uint8_t* out2 = sub_dst ? sub_dst[ui] : nullptr;
     uint64_t s1 = 0, s2 = 0;
     const uint32_t nvec = u.n >> 3;  // groups of 8 elements = 32 B in, 16 B out
     if ((((uintptr_t)src) & 15) == 0) {
@@ -169,6 +187,7 @@ __global__ void __launch_bounds__(kPackThreads) k_pack(const PackUnit* __restric
           const uint4 w = make_uint4(pack2(a[k].x, a[k].y), pack2(a[k].z, a[k].w), pack2(b[k].x, b[k].y),
                                      pack2(b[k].z, b[k].w));
           st_v4(out + 16 * (size_t)vk, w);
+          if (out2) st_v4_any(out2 + 16 * (size_t)vk, w);
           cks4((uint64_t)u.word0 + 4ull * vk, w, s1, s2);
         }
       }
@@ -176,6 +195,7 @@ __global__ void __launch_bounds__(kPackThreads) k_pack(const PackUnit* __restric
         const uint4 a = ld_stream_v4(src + 8 * (size_t)v), b = ld_stream_v4(src + 8 * (size_t)v + 4);
         const uint4 w = make_uint4(pack2(a.x, a.y), pack2(a.z, a.w), pack2(b.x, b.y), pack2(b.z, b.w));
         st_v4(out + 16 * (size_t)v, w);
+        if (out2) st_v4_any(out2 + 16 * (size_t)v, w);
         cks4((uint64_t)u.word0 + 4ull * v, w, s1, s2);
       }
     } else {  // caller's shard pointer not 16-B aligned: scalar loads, same 16-B stores
@@ -184,6 +204,7 @@ __global__ void __launch_bounds__(kPackThreads) k_pack(const PackUnit* __restric
         const uint32_t* q = s32 + 8 * (size_t)v;
         const uint4 w = make_uint4(pack2(q[0], q[1]), pack2(q[2], q[3]), pack2(q[4], q[5]), pack2(q[6], q[7]));
         st_v4(out + 16 * (size_t)v, w);
+        if (out2) st_v4_any(out2 + 16 * (size_t)v, w);
         cks4((uint64_t)u.word0 + 4ull * v, w, s1, s2);
       }
     }
@@ -196,6 +217,10 @@ __global__ void __launch_bounds__(kPackThreads) k_pack(const PackUnit* __restric
         const uint32_t hi = (e + 1 < u.n) ? rne_bf16(s32[e + 1]) : 0u;
         o16[e] = (uint16_t)lo;
         if (e + 1 < u.n) o16[e + 1] = (uint16_t)hi;
+        if (out2) {
+          reinterpret_cast<uint16_t*>(out2)[e] = (uint16_t)lo;
+          if (e + 1 < u.n) reinterpret_cast<uint16_t*>(out2)[e + 1] = (uint16_t)hi;
+        }
         const uint64_t w = lo | (hi << 16);
         s1 += w;
         s2 += ((uint64_t)u.word0 + e / 2 + 1) * w;
@@ -214,12 +239,12 @@ __global__ void __launch_bounds__(kPackThreads) k_pack(const PackUnit* __restric
 
 int launch_pack(const PackUnit* units, uint32_t n_units, const float* const* shard_ptrs, uint8_t* dst,
                 ChunkMeta meta, const uint32_t* units_per_chunk, uint64_t version, uint64_t n_total,
-                const uint64_t* chunk_len, int ctas, void* stream) {
+                const uint64_t* chunk_len, int ctas, void* stream, uint8_t* const* sub_dst) {
   if (n_units == 0) return 0;
   if (ctas <= 0) ctas = resident_ctas(k_pack, kPackThreads);
   unsigned grid = (unsigned)(n_units < (uint32_t)ctas ? n_units : (uint32_t)ctas);
   k_pack<<<grid, kPackThreads, 0, (cudaStream_t)stream>>>(units, n_units, shard_ptrs, dst, meta,
-                                                          units_per_chunk, version, n_total, chunk_len);
+                                                          units_per_chunk, version, n_total, chunk_len, sub_dst);
   return (int)cudaGetLastError();
 }
 

@@ -88,6 +88,14 @@ struct RankPub {   // per local actor rank (node 0)
   const float** d_ptrs = nullptr;
   uint32_t cap_ptrs = 0;
   const float** h_ptrs = nullptr;    // pinned staging of the shard pointer table
+  std::vector<PackUnit> h_units;     // host copy of the units (colocated subscriptions)
+  uint64_t units_gen = 0;            // bumped whenever the units are rebuilt
+  // colocated subscription (lam_subscribe): per-unit destination in the subscriber's buffers
+  int32_t sub_rid = -1;              // pending subscriber (-1: none)
+  std::vector<uint64_t> sub_tensor_dst;  // [n_tensors] dst address of element 0 of each tensor
+  uint64_t sub_gen = ~0ull;          // units_gen the table was built for
+  uint8_t** d_sub = nullptr;
+  uint32_t cap_sub = 0;
 };
 
 struct PullPlan {
@@ -138,6 +146,7 @@ struct lam_ctx {
   bool shm_registered = false;
   struct StreamPull {                 // lam_pull_stream in progress (per rollout)
     bool active = false;
+    bool subscription = false;        // lam_subscribe: completed by the pack, not by chunk progress
     int node = 0, slot = 0, device = 0;
     uint64_t v = 0;
     lam_status status = LAM_OK;
@@ -768,6 +777,10 @@ lam_status step_locked(lam_ctx* c, int* transitions, bool* busy) {
   // (2b) streaming pulls of this process's rollouts
   for (int rid = 0; rid < (int)c->streams.size(); ++rid) {
     if (!c->streams[rid].active) continue;
+    if (c->streams[rid].subscription) {
+      *busy = true;
+      continue;
+    }
     lam_status st = stream_progress(c, rid, transitions);
     if (st != LAM_OK) return st;
     if (c->streams[rid].active) *busy = true;
@@ -1059,6 +1072,8 @@ extern "C" lam_status lam_publish(lam_ctx* c, uint64_t v, int32_t rank, const la
     for (int i = 0; i < n; ++i) ptrs[i] = shards[i].ptr;
     if (n) CK(cudaMemcpy((void*)rp.d_ptrs, ptrs.data(), sizeof(float*) * n, cudaMemcpyHostToDevice));
     rp.key = key;
+    rp.h_units = units;
+    rp.units_gen++;
   }
   Lock l(c->shm);
   Shm* sh = c->shm;
@@ -1078,8 +1093,33 @@ extern "C" lam_status lam_publish(lam_ctx* c, uint64_t v, int32_t rank, const la
     CK(cudaMemsetAsync(m.cnt + g0, 0, 4 * ng, side));
   }
   cudaEvent_t t0 = prof_begin(c, dev, side);
+  uint8_t* const* sub = nullptr;
+  const int sub_rid = rp.sub_rid;
+  if (sub_rid >= 0) {  // colocated subscriber: per-unit destinations (rebuilt only when units change)
+    if (rp.sub_gen != rp.units_gen) {
+      std::vector<uint8_t*> tab(rp.n_units);
+      for (uint32_t i = 0; i < rp.n_units; ++i) {
+        const PackUnit& u = rp.h_units[i];
+        const lam_shard& sh = rp.key[u.shard];
+        tab[i] = (uint8_t*)(uintptr_t)(rp.sub_tensor_dst[sh.tensor_id] + 2 * (sh.elem_offset + u.src_elem));
+        if ((uintptr_t)tab[i] % 2) {  // k_pack narrows its stores to whatever alignment remains
+          fprintf(stderr, "liblam: lam_subscribe: destination not 2-B aligned\n");
+          return LAM_EINVAL;
+        }
+      }
+      if (rp.n_units > rp.cap_sub) {
+        if (rp.d_sub) cudaFree(rp.d_sub);
+        CK(cudaMalloc(&rp.d_sub, sizeof(uint8_t*) * std::max<uint32_t>(rp.n_units, 1)));
+        rp.cap_sub = rp.n_units;
+      }
+      CK(cudaStreamSynchronize(side));
+      if (rp.n_units) CK(cudaMemcpy(rp.d_sub, tab.data(), sizeof(uint8_t*) * rp.n_units, cudaMemcpyHostToDevice));
+      rp.sub_gen = rp.units_gen;
+    }
+    sub = rp.d_sub;
+  }
   int rc = launch_pack(rp.d_units, rp.n_units, rp.d_ptrs, slot_data(p, s), m, rp.d_units_per_chunk, v,
-                       c->plan.total_chunks, c->dev[dev].d_chunk_len, c->pack_ctas, side);
+                       c->plan.total_chunks, c->dev[dev].d_chunk_len, c->pack_ctas, side, sub);
   if (rc) {
     fprintf(stderr, "liblam: pack launch failed: %s\n", cudaGetErrorString((cudaError_t)rc));
     return LAM_ECUDA;
@@ -1088,6 +1128,67 @@ extern "C" lam_status lam_publish(lam_ctx* c, uint64_t v, int32_t rank, const la
   if (reads_done) CK(cudaEventRecord((cudaEvent_t)reads_done, side));
   CK(cudaEventRecord(rp.ev[s], side));
   rp.inflight_version[s] = v;
+  if (sub_rid >= 0) {  // one-shot: complete the subscription once every local rank packed v
+    rp.sub_rid = -1;
+    lam_ctx::StreamPull& sp = c->streams[sub_rid];
+    bool all = true;
+    for (int r = 0; r < c->cfg.fsdp_size; ++r)
+      if (c->cfg.actor_device[r] == dev && c->pubs[r].sub_rid == sub_rid) all = false;
+    if (all) {
+      if (sp.done) CK(cudaEventRecord(sp.done, side));
+      sp.active = false;
+      sp.subscription = false;
+      sp.v = v;
+      sp.status = LAM_OK;
+      c->shm->stats.pulls++;
+    }
+  }
+  return LAM_OK;
+}
+
+extern "C" lam_status lam_subscribe(lam_ctx* c, int32_t rid, const lam_tp_layout* L, void* done) {
+  if (!c || !c->connected || !L || rid < 0 || rid >= c->cfg.n_rollouts) return LAM_EINVAL;
+  const lam_rollout_desc ro = c->cfg.rollout[rid];
+  if (ro.node != 0 || !owns(c, ro.device) || L->tp_size != 1) return LAM_EINVAL;
+  // the layout must put every tensor, whole and dense, somewhere in the rollout's buffers
+  std::vector<uint64_t> tdst(c->ts.size(), 0);
+  for (int k = 0; k < L->n_dsts; ++k) {
+    const lam_dst& d = L->dsts[k];
+    if (d.transpose || !d.dst) return LAM_EINVAL;
+    uint64_t off = 0;
+    for (int q = 0; q < d.n_parts; ++q) {
+      const uint32_t t = d.parts[q].tensor_id;
+      if (t >= c->ts.size() || tdst[t]) return LAM_EINVAL;
+      if (d.dst_row_pitch_bytes && (uint64_t)d.dst_row_pitch_bytes != 2 * (uint64_t)c->ts[t].d1) return LAM_EINVAL;
+      tdst[t] = (uint64_t)(uintptr_t)d.dst + off;
+      off += 2 * c->ts[t].numel();
+    }
+  }
+  for (uint64_t a : tdst)
+    if (!a) return LAM_EINVAL;
+  Lock l(c->shm);
+  lam_ctx::StreamPull& sp = c->streams[rid];
+  if (sp.active) return LAM_EBUSY;
+  bool any = false;
+  for (int r = 0; r < c->cfg.fsdp_size; ++r) {
+    if (c->cfg.actor_device[r] != ro.device) continue;
+    RankPub& rp = c->pubs[r];
+    if (rp.sub_tensor_dst != tdst) {
+      rp.sub_tensor_dst = tdst;
+      rp.sub_gen = ~0ull;
+    }
+    rp.sub_rid = rid;
+    any = true;
+  }
+  if (!any) return LAM_EINVAL;
+  sp.active = true;      // until the pack of the next version is enqueued
+  sp.subscription = true;
+  sp.node = 0;
+  sp.device = ro.device;
+  sp.v = 0;
+  sp.status = LAM_OK;
+  sp.plan = nullptr;
+  sp.done = (cudaEvent_t)done;
   return LAM_OK;
 }
 
@@ -1167,6 +1268,7 @@ extern "C" lam_status lam_pull_stream(lam_ctx* c, int32_t rid, const lam_tp_layo
   if (pst != LAM_OK) return pst;
   n.slot[s].readers++;                                 // pin the version being received
   sp.active = true;
+  sp.subscription = false;
   sp.node = ro.node;
   sp.slot = s;
   sp.device = ro.device;
@@ -1346,6 +1448,7 @@ extern "C" void lam_destroy(lam_ctx* c) {
     if (rp.d_units) cudaFree(rp.d_units);
     if (rp.d_units_per_chunk) cudaFree(rp.d_units_per_chunk);
     if (rp.d_ptrs) cudaFree((void*)rp.d_ptrs);
+    if (rp.d_sub) cudaFree(rp.d_sub);
     for (int s = 0; s < LAM_MAX_SLOTS; ++s)
       if (rp.ev[s]) cudaEventDestroy(rp.ev[s]);
   }

@@ -335,6 +335,13 @@ class Context:
         _check(st, "lam_pull_stream", ok=(LAM_OK, LAM_ENOVERSION))
         return v.value
 
+    def subscribe(self, rollout: int, layout: TPLayout, done_event: int | None = None) -> None:
+        """lam_subscribe: the next publish on the rollout's (actor) GPU also writes its TP=1 buffers."""
+        f = self.L.lam_subscribe
+        f.restype = C.c_int32
+        f.argtypes = [C.c_void_p, C.c_int32, C.POINTER(lam_tp_layout), C.c_void_p]
+        _check(f(self.h, rollout, C.byref(layout.c), done_event), "lam_subscribe")
+
     def pull_state(self, rollout: int) -> tuple[int, int]:
         """(version, state): state 1 = chunks still arriving, 0 = done, < 0 = failed."""
         f = self.L.lam_pull_state

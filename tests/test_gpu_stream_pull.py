@@ -82,6 +82,52 @@ def test_stream_pull_from_master_while_packing():
     ctx.close()
 
 
+@pytest.mark.parametrize("model,N", [("tiny", 1), ("tiny", 3), ("7b", 1)])
+def test_colocated_subscription(model, N):
+    """lam_subscribe: the pack writes the colocated TP=1 rollout in the same pass; the rollout's
+    buffers equal the oracle's pull of that version, and the master slot is still IMG(v)."""
+    od = OMODELS[model]
+    C = 64 << 20 if model == "7b" else 16 * 4096
+    ctx = lam.Context(lam.Config(model=MODELS[model], fsdp_size=N, actor_devices=[0] * N, rollouts=[(0, 0)],
+                                 chunk_bytes=C))
+    shards = [ActorShard(MODELS[model], N, r, 0) for r in range(N)]
+    rb = RolloutBuffers(MODELS[model], 1, 0, 0)
+    for v in (1, 2):
+        for sh in shards:
+            sh.fill(SEED, v, specials=model == "tiny")
+        rb.fill_(0xFFFF)
+        torch.cuda.synchronize()
+        done = torch.cuda.Event()
+        ctx.subscribe(0, rb.tp, done.cuda_event)
+        assert ctx.pull_state(0)[1] == 1
+        for r, sh in enumerate(shards):
+            assert ctx.publish(v, r, sh.shards()) == lam.LAM_OK
+        assert ctx.pull_state(0) == (v, 0)
+        done.synchronize()
+        if model == "tiny":
+            want = direct_pull(od, 1, 0, SEED, v, specials=True)
+            for name, t in rb.bufs.items():
+                g = t.view(torch.int16).cpu().numpy().view(np.uint16)
+                assert np.array_equal(g, want[name].reshape(g.shape)), name
+        else:
+            rng = np.random.default_rng(v)
+            for name, t in rb.bufs.items():
+                idx = rng.integers(0, t.numel(), 64)
+                g = t.view(-1).view(torch.int16).cpu().numpy().view(np.uint16)[idx]
+                assert np.array_equal(g, dst_elements(od, 1, 0, name, idx, SEED, v)), name
+        for _ in range(100000):
+            if ctx.relay_step()[0] == lam.LAM_IDLE:
+                break
+        assert ctx.latest(0) == v
+    if model == "tiny":                                     # the master slot is untouched by the fusion
+        from oracle.image import image_plan, publish
+        from oracle.model import tensors as otensors
+        oimg, ohdr = publish(image_plan([s for _, s in otensors(od)], N, C), SEED, 2, specials=True)
+        assert np.array_equal(ctx.read_image(0, 2, 0, oimg.size), oimg)
+        assert ctx.read_headers(0, 2) == ohdr
+    ctx.close()
+
+
 def test_stream_pull_of_a_corrupt_version_fails():
     ctx = lam.Context(lam.Config(model=MODELS["tiny"], relays=[[0]], rollouts=[(1, 0)], chunk_bytes=16 * 4096))
     shard = ActorShard(MODELS["tiny"], 1, 0, 0)
