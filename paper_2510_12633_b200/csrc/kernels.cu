@@ -140,6 +140,9 @@ __device__ void pack_flush(ChunkMeta meta, const uint32_t* units_per_chunk, cons
   }
 }
 
+// SUB: compiled with the colocated-subscriber stores (separate instantiation: the plain pack keeps
+// its register budget and occupancy)
+template <bool SUB>
 __global__ void __launch_bounds__(kPackThreads) k_pack(const PackUnit* __restrict__ units, uint32_t n_units,
                                                        const float* const* __restrict__ shard_ptrs,
                                                        uint8_t* __restrict__ dst, ChunkMeta meta,
@@ -168,7 +171,7 @@ __global__ void __launch_bounds__(kPackThreads) k_pack(const PackUnit* __restric
     const float* src = shard_ptrs[u.shard] + u.src_elem;
     uint8_t* out = dst + u.dst_off;
     // colocated subscriber (lam_subscribe): the same bf16 bytes also go to its TP=1 buffer
-    uint8_t* out2 = sub_dst ? sub_dst[ui] : nullptr;
+    uint8_t* out2 = SUB ? sub_dst[ui] : nullptr;
     uint64_t s1 = 0, s2 = 0;
     const uint32_t nvec = u.n >> 3;  // groups of 8 elements = 32 B in, 16 B out
     if ((((uintptr_t)src) & 15) == 0) {
@@ -241,10 +244,14 @@ int launch_pack(const PackUnit* units, uint32_t n_units, const float* const* sha
                 ChunkMeta meta, const uint32_t* units_per_chunk, uint64_t version, uint64_t n_total,
                 const uint64_t* chunk_len, int ctas, void* stream, uint8_t* const* sub_dst) {
   if (n_units == 0) return 0;
-  if (ctas <= 0) ctas = resident_ctas(k_pack, kPackThreads);
+  if (ctas <= 0) ctas = sub_dst ? resident_ctas(k_pack<true>, kPackThreads) : resident_ctas(k_pack<false>, kPackThreads);
   unsigned grid = (unsigned)(n_units < (uint32_t)ctas ? n_units : (uint32_t)ctas);
-  k_pack<<<grid, kPackThreads, 0, (cudaStream_t)stream>>>(units, n_units, shard_ptrs, dst, meta,
-                                                          units_per_chunk, version, n_total, chunk_len, sub_dst);
+  if (sub_dst)
+    k_pack<true><<<grid, kPackThreads, 0, (cudaStream_t)stream>>>(units, n_units, shard_ptrs, dst, meta,
+                                                                  units_per_chunk, version, n_total, chunk_len, sub_dst);
+  else
+    k_pack<false><<<grid, kPackThreads, 0, (cudaStream_t)stream>>>(units, n_units, shard_ptrs, dst, meta,
+                                                                   units_per_chunk, version, n_total, chunk_len, nullptr);
   return (int)cudaGetLastError();
 }
 
