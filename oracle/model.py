@@ -27,6 +27,9 @@ MODELS = {
     "7b": Dims(H=3584, I=18944, L=28, nh=28, nkv=4, hd=128, V=152064),  # Qwen2.5-7B
     "32b": Dims(H=5120, I=27648, L=64, nh=40, nkv=8, hd=128, V=152064),  # Qwen2.5-32B
     "72b": Dims(H=8192, I=29568, L=80, nh=64, nkv=8, hd=128, V=152064),  # Qwen2.5-72B
+    # Edge-case model (ours): V = 130 needs vocabulary padding (to 192, so at
+    # TP=8 ranks 6-7 hold only padding) and nkv = 2 < tp = 4, 8 needs KV-head replication.
+    "odd": Dims(H=64, I=192, L=2, nh=8, nkv=2, hd=8, V=130),
 }
 
 

@@ -19,6 +19,7 @@ MODELS = {
     "7b": lam.dims(3584, 18944, 28, 28, 4, 128, 152064),
     "32b": lam.dims(5120, 27648, 64, 40, 8, 128, 152064),
     "72b": lam.dims(8192, 29568, 80, 64, 8, 128, 152064),
+    "odd": lam.dims(64, 192, 2, 8, 2, 8, 130),   # vocab padding + KV-head replication cases
 }
 
 

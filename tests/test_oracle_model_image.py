@@ -13,16 +13,19 @@ from synth import SEED, gen_bits
 
 # Published parameter counts of the Qwen2.5 checkpoints' configs (untied embeddings) and our tiny model.
 PUBLISHED = {"tiny": (10_227_968, 51), "7b": (7_615_616_512, 339), "32b": (32_763_876_352, 771),
-             "72b": (72_706_203_648, 963)}
+             "72b": (72_706_203_648, 963),
+             # odd: embed 130*64 + 2 layers * (q 64*64+64, k,v 2*(16*64+16), o 64*64, gate/up/down
+             # 3*192*64, norms 2*64) + norm 64 + lm_head 130*64, counted by hand
+             "odd": (111_360, 27)}
 
 
-@pytest.mark.parametrize("name", ["tiny", "7b", "32b", "72b"])
+@pytest.mark.parametrize("name", ["tiny", "7b", "32b", "72b", "odd"])
 def test_param_counts(name):
     d = MODELS[name]
     assert (param_count(d), len(tensors(d))) == PUBLISHED[name]
 
 
-@pytest.mark.parametrize("name", ["tiny", "7b"])
+@pytest.mark.parametrize("name", ["tiny", "7b", "odd"])
 def test_tensor_table_matches_transformers_qwen2(name):
     transformers = pytest.importorskip("transformers")
     d = MODELS[name]
