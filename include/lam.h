@@ -63,8 +63,20 @@ enum {
 /* Actor partition layouts ("FSDP"). */
 enum { LAM_FSDP2_DIM0 = 0, LAM_FSDP1_FLAT = 1 };
 
-/* TP rules of a destination part (vLLM convention). */
-enum { LAM_REPLICATE = 0, LAM_SHARD_DIM0 = 1, LAM_SHARD_DIM1 = 2, LAM_VOCAB_DIM0 = 3 };
+/* TP rules of a destination part (vLLM convention; "reshards them
+ * according to the rollout sharding strategy", L1357 TP 1/4/8).  For rank r of tp, a part of source
+ * tensor A (d0 x d1) contributes:
+ *   LAM_REPLICATE   all of A
+ *   LAM_SHARD_DIM0  rows [r*d0/tp, (r+1)*d0/tp)                     (d0 % tp == 0)
+ *   LAM_SHARD_DIM1  columns [r*d1/tp, (r+1)*d1/tp) of every row      (2-D, d1 % tp == 0)
+ *   LAM_VOCAB_DIM0  the vocabulary padded to Vp = 64*ceil(d0/64) rows; rank r owns padded rows
+ *                   [r*Vp/tp, (r+1)*Vp/tp): its real rows, then zero rows for the padding (written
+ *                   by the pull) — vLLM's VocabParallelEmbedding (R15)
+ *   LAM_HEAD_DIM0   whole attention heads of head_dim rows (q/k/v weights and biases only; heads =
+ *                   d0 / head_dim): tp <= heads: heads [r*heads/tp, (r+1)*heads/tp); tp > heads
+ *                   (tp % heads == 0): head r / (tp/heads), i.e. KV heads replicated — vLLM's
+ *                   QKVParallelLinear (R14) */
+enum { LAM_REPLICATE = 0, LAM_SHARD_DIM0 = 1, LAM_SHARD_DIM1 = 2, LAM_VOCAB_DIM0 = 3, LAM_HEAD_DIM0 = 4 };
 
 #define LAM_MAX_RANKS 64
 #define LAM_MAX_NODES 32
@@ -132,7 +144,10 @@ typedef struct {
 } lam_shard;
 
 /* A destination buffer of a rollout TP rank: the parts' TP slices concatenated along dim 0
- * (e.g. qkv = [q_r; k_r; v_r]).  dst_row_pitch_bytes = 0 means dense rows. */
+ * (e.g. qkv = [q_r; k_r; v_r]) into a (rows x cols) bf16 matrix A.
+ *   transpose = 0: row-major, A[i][c] at dst + i*pitch + 2c; dst_row_pitch_bytes = 0 means 2*cols.
+ *   transpose = 1: K-major (R16), A[i][c] at dst + c*pitch + 2i; dst_row_pitch_bytes =
+ *                  0 means 2*rows, else >= 2*rows.  1-D destinations ignore the flag. */
 typedef struct {
   uint32_t tensor_id;
   int32_t rule;
@@ -141,7 +156,7 @@ typedef struct {
 typedef struct {
   const lam_part* parts;
   int32_t n_parts;
-  int32_t transpose;                       /* reserved: must be 0 */
+  int32_t transpose;                       /* 0 row-major, 1 K-major (transposed) */
   void* dst;                               /* device pointer on the rollout's GPU */
   int64_t dst_row_pitch_bytes;
 } lam_dst;
@@ -298,7 +313,12 @@ int64_t lam_plan_segments(const lam_model_dims*, int32_t actor_layout, int32_t f
                           lam_segment_info* out, int64_t cap);
 /* The pull copy plan for a TP layout (destination pointers are taken as plain integers):
  * each tile copies `rows` rows of `row_bytes` from image rank region `src_rank` at byte
- * `src_off` (row stride src_pitch) to address `dst` (row stride dst_pitch). */
+ * `src_off` (row stride src_pitch) to address `dst` (row stride dst_pitch).  Two variants, marked
+ * in `align` (low byte = 16/4/2, the widest access every address allows):
+ *   align & LAM_TILE_TRANSPOSE: element k of row r goes to dst + k*dst_pitch + 2r instead;
+ *   src_rank == LAM_TILE_ZERO:  no source; the block is zero-filled (vocabulary padding rows). */
+#define LAM_TILE_TRANSPOSE 0x100u
+#define LAM_TILE_ZERO 0xFFFFFFFFu
 typedef struct {
   uint64_t src_off, dst;
   uint32_t src_pitch, dst_pitch, rows, row_bytes, src_rank, align;

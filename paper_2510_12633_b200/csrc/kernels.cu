@@ -13,6 +13,7 @@
 //   k_pull  — pull-time TP reshard (A6): copy-plan driven 2-D block copy from
 //             the pinned relay slot (local HBM or peer GPU) into the rollout's TP buffers.
 #include <cuda_runtime.h>
+#include <stdlib.h>
 
 #include <algorithm>
 
@@ -261,12 +262,143 @@ int launch_pack(const PackUnit* units, uint32_t n_units, const float* const* sha
 constexpr int kPullThreads = 512;
 constexpr int kPullUnroll = 4;
 
-__global__ void __launch_bounds__(kPullThreads) k_pull(const CopyTile* __restrict__ tiles, uint32_t n_tiles,
-                                                       const uint8_t* const* __restrict__ rank_base) {
+// 8x8 transpose of bf16 in registers: in[j] = 8 consecutive elements of source row j; column i of
+// the micro-tile (word m = (in[2m].e_i, in[2m+1].e_i)) is assembled by byte permutes only.
+__device__ __forceinline__ uint32_t word_of(const uint4& v, int q) {
+  return q == 0 ? v.x : (q == 1 ? v.y : (q == 2 ? v.z : v.w));
+}
+__device__ __forceinline__ uint4 transpose_col(const uint4 (&in)[8], int i) {
+  const uint32_t sel = (i & 1) ? 0x7632u : 0x5410u;
+  uint4 o;
+  o.x = __byte_perm(word_of(in[0], i >> 1), word_of(in[1], i >> 1), sel);
+  o.y = __byte_perm(word_of(in[2], i >> 1), word_of(in[3], i >> 1), sel);
+  o.z = __byte_perm(word_of(in[4], i >> 1), word_of(in[5], i >> 1), sel);
+  o.w = __byte_perm(word_of(in[6], i >> 1), word_of(in[7], i >> 1), sel);
+  return o;
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// Element-wise K-major copy of rows [ra, rb) x columns [ka, kb) of a tile (edges / unaligned tiles).
+__device__ __forceinline__ void pull_t_scalar(const uint8_t* src, uint8_t* dst, uint32_t sp, uint32_t dp,
+                                              uint32_t ra, uint32_t rb, uint32_t ka, uint32_t kb) {
+  const uint32_t nk = kb - ka, total = (rb - ra) * nk;
+  for (uint32_t v = threadIdx.x; v < total; v += kPullThreads) {
+    const uint32_t r = ra + v / nk, k = ka + v % nk;
+    *reinterpret_cast<uint16_t*>(dst + (size_t)k * dp + 2 * (size_t)r) =
+        *reinterpret_cast<const uint16_t*>(src + (size_t)r * sp + 2 * (size_t)k);
+  }
+}
+
+// K-major tile (R16): element k of source row r -> dst + k*dst_pitch + 2r.
+// The kernel is bound by L2 requests (ncu: time tracks lts__t_requests, ~10 ps each, for every variant
+// tried), so both sides must move whole 128-B lines.  Each warp owns 8 KiB of shared memory and walks
+// the tile in 64-row x 64-column blocks:
+//   load   16 x cp.async 16 B per thread, all in flight (no register staging): an instruction reads 4
+//          source rows x one full line into smem row r, 16-B chunk c at chunk position c ^ ((r >> 3) & 7)
+//          (conflict-free on both sides)
+//   store  per thread two 8x8 micro-tiles (source rows 8*(lane%8).., columns 8*(lane/8 + 4h)..):
+//          8 x LDS.128, transpose in registers by byte permutes, 8 x STG.128: an instruction writes
+//          4 destination rows x one full line.
+// Edges (rows or columns not a multiple of 8, unaligned tiles) go element by element.
+constexpr int kTBlk = 64;                                   // block rows = block columns
+constexpr int kTWarpSmem = kTBlk * kTBlk * 2;               // 8 KiB per warp
+constexpr int kPullSmem = kTWarpSmem * (kPullThreads / 32); // 128 KiB per CTA
+
+__device__ __forceinline__ void pull_transposed(const CopyTile& T, const uint8_t* src, uint8_t* dst,
+                                                uint8_t* smem) {
+  const uint32_t R = T.rows, K = T.row_bytes >> 1, sp = T.src_pitch, dp = T.dst_pitch;
+  if ((T.align & 0xFFu) != 16) {
+    pull_t_scalar(src, dst, sp, dp, 0, R, 0, K);
+    return;
+  }
+  const uint32_t RG = R >> 3, KG = K >> 3;                  // whole 8-row / 8-column groups
+  const uint32_t BR = (RG + 7) >> 3, BK = (KG + 7) >> 3;    // 64 x 64 blocks
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint8_t* ws = smem + warp * kTWarpSmem;
+  for (uint32_t blk = warp; blk < BR * BK; blk += kPullThreads / 32) {
+    const uint32_t br = blk % BR, bk = blk / BR;            // walk down the rows first
+    const uint32_t row0 = br * kTBlk, col0 = bk * kTBlk;
+    // ---- load: row = 4k + lane/8, chunk = lane%8
+    const uint32_t lc = lane & 7, lr = lane >> 3;
+    // loads k < kn are in the tile (rows row0 + 4k + lr < 8*RG, column group inside)
+    const int32_t left = (int32_t)(RG * 8 - row0) - (int32_t)lr;
+    const int kn = bk * 8 + lc < KG ? (left > 0 ? min(16, (left + 3) >> 2) : 0) : 0;
+    const uint8_t* p = src + (size_t)(row0 + lr) * sp + 2 * (size_t)(col0 + 8 * lc);
+    const size_t step = 4 * (size_t)sp;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {   // asynchronous global -> smem copies: all 16 in flight
+      const uint32_t r = 4 * k + lr;
+      if (k < kn) cp_async16(ws + r * 128 + 16 * (lc ^ ((r >> 3) & 7)), p + k * step);
+    }
+    cp_async_wait_all();
+    __syncwarp();
+    // ---- store: micro-tile (rows 8*rb.., columns 8*cc..), rb = lane%8, cc = lane/8 + 4h
+    const uint32_t rb = lane & 7;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint32_t cc = (lane >> 3) + 4 * h;
+      if (br * 8 + rb < RG && bk * 8 + cc < KG) {
+        uint4 in[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint32_t r = 8 * rb + j;
+          in[j] = *reinterpret_cast<const uint4*>(ws + r * 128 + 16 * (cc ^ rb));
+        }
+        uint8_t* d0 = dst + (size_t)(col0 + 8 * cc) * dp + 2 * (size_t)(row0 + 8 * rb);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) st_v4(d0 + (size_t)i * dp, transpose_col(in, i));
+      }
+    }
+    __syncwarp();
+  }
+  if (RG * 8 < R) pull_t_scalar(src, dst, sp, dp, RG * 8, R, 0, K);
+  if (KG * 8 < K) pull_t_scalar(src, dst, sp, dp, 0, RG * 8, KG * 8, K);
+}
+
+// Zero-filled block (vocabulary padding rows, R15).
+__device__ __forceinline__ void pull_zero(const CopyTile& T, uint8_t* dst) {
+  const uint32_t a = T.align & 0xFFu;
+  const uint32_t per = T.row_bytes / a, total = per * T.rows;
+  for (uint32_t v = threadIdx.x; v < total; v += kPullThreads) {
+    uint8_t* p = dst + (size_t)(v / per) * T.dst_pitch + (size_t)(v % per) * a;
+    if (a == 16) st_v4(p, make_uint4(0, 0, 0, 0));
+    else if (a == 4) *reinterpret_cast<uint32_t*>(p) = 0;
+    else *reinterpret_cast<uint16_t*>(p) = 0;
+  }
+}
+
+// L2 prefetch of a K-major tile's source rows (whole row runs, so DRAM sees long bursts).
+__device__ __forceinline__ void prefetch_t(const CopyTile& T, const uint8_t* const* rank_base) {
+  if (T.src_rank == LAM_TILE_ZERO || !(T.align & LAM_TILE_TRANSPOSE) || (T.align & 0xFFu) != 16) return;
+  const uint8_t* src = rank_base[T.src_rank] + T.src_off;
+  for (uint32_t r = threadIdx.x; r < T.rows; r += kPullThreads)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src + (size_t)r * T.src_pitch),
+                 "r"(T.row_bytes & ~15u) : "memory");
+}
+
+__global__ void __launch_bounds__(kPullThreads, 1) k_pull(const CopyTile* __restrict__ tiles, uint32_t n_tiles,
+                                                       const uint8_t* const* __restrict__ rank_base, int pf) {
+  extern __shared__ __align__(128) uint8_t pull_smem[];
+  if (pf == 2 && blockIdx.x < n_tiles) prefetch_t(tiles[blockIdx.x], rank_base);
   for (uint32_t ti = blockIdx.x; ti < n_tiles; ti += gridDim.x) {
     const CopyTile T = tiles[ti];
-    const uint8_t* src = rank_base[T.src_rank] + T.src_off;
+    if (pf == 1) prefetch_t(T, rank_base);
+    if (pf == 2 && ti + gridDim.x < n_tiles) prefetch_t(tiles[ti + gridDim.x], rank_base);
     uint8_t* dst = reinterpret_cast<uint8_t*>(T.dst);
+    if (T.src_rank == LAM_TILE_ZERO) {
+      pull_zero(T, dst);
+      continue;
+    }
+    const uint8_t* src = rank_base[T.src_rank] + T.src_off;
+    if (T.align & LAM_TILE_TRANSPOSE) {
+      pull_transposed(T, src, dst, pull_smem);
+      continue;
+    }
     if (T.align == 16) {
       const uint32_t vpr = T.row_bytes >> 4, total = vpr * T.rows;
       if (T.rows == 1) {
@@ -324,9 +456,13 @@ __global__ void __launch_bounds__(kPullThreads) k_pull(const CopyTile* __restric
 
 int launch_pull(const CopyTile* tiles, uint32_t n_tiles, const uint8_t* const* rank_base, int ctas, void* stream) {
   if (n_tiles == 0) return 0;
-  if (ctas <= 0) ctas = resident_ctas(k_pull, kPullThreads);
+  static const bool attr = cudaFuncSetAttribute(k_pull, cudaFuncAttributeMaxDynamicSharedMemorySize, kPullSmem) ==
+                           cudaSuccess;
+  if (!attr) return (int)cudaErrorInvalidValue;
+  if (ctas <= 0) ctas = resident_ctas(k_pull, kPullThreads, kPullSmem);
   unsigned grid = (unsigned)(n_tiles < (uint32_t)ctas ? n_tiles : (uint32_t)ctas);
-  k_pull<<<grid, kPullThreads, 0, (cudaStream_t)stream>>>(tiles, n_tiles, rank_base);
+  static const int pf = getenv("LAM_PULL_PF") ? atoi(getenv("LAM_PULL_PF")) : 0;
+  k_pull<<<grid, kPullThreads, kPullSmem, (cudaStream_t)stream>>>(tiles, n_tiles, rank_base, pf);
   return (int)cudaGetLastError();
 }
 

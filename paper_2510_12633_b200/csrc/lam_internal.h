@@ -16,6 +16,8 @@ constexpr uint64_t kSlotAlign = 2u << 20;
 constexpr uint32_t kPackUnitElems = 32768;     // fp32 elements per pack work unit (128 KiB read)
 constexpr uint32_t kHopTileBytes = 1u << 20;   // bytes per chain-hop tile
 constexpr uint32_t kPullTileBytes = 256u << 10;
+constexpr uint32_t kPullTRows = 256;     // K-major pull tile: source rows ...
+constexpr uint32_t kPullTCols = 512;     // ... x columns (<= 256 KiB per tile)
 // flag = version | kPoison marks a failed chunk.  Bit 62 (not 63) so that a stream memory op waiting
 // for "(int64)(flag - version) >= 0" is released by a poisoned flag as well.
 constexpr uint64_t kPoison = 1ull << 62;
@@ -28,6 +30,7 @@ struct Tensor {
   std::string name;
   int64_t d0, d1;   // d1 = 1 for 1-D tensors
   int ndim;
+  int64_t heads = 0;   // attention heads stacked along dim 0 (q/k/v weights and biases), else 0
   uint64_t numel() const { return (uint64_t)d0 * (uint64_t)d1; }
 };
 std::vector<Tensor> model_tensors(const lam_model_dims& d);
@@ -37,9 +40,11 @@ struct DstPart { uint32_t tensor; int rule; };
 struct VllmDst { std::string name; int64_t rows, cols; std::vector<DstPart> parts; };
 // vLLM Qwen2 destination list for tp; returns false if the dims are not divisible.
 bool vllm_layout(const lam_model_dims& d, int tp, std::vector<VllmDst>* out);
-// Source slice of a part for rank `rank`: rows [r0, r1) x cols [c0, c1) (1-D: cols [0, 1)).
+// Source slice of a part for rank `rank`: rows [r0, r1) x cols [c0, c1) (1-D: cols [0, 1)),
+// followed in the destination by `pad` zero rows (vocabulary padding, LAM_VOCAB_DIM0 only).
+constexpr int64_t kVocabPad = 64;   // vLLM DEFAULT_VOCAB_PADDING_SIZE (R15)
 bool part_slice(const Tensor& t, int rule, int tp, int rank, int64_t* r0, int64_t* r1, int64_t* c0,
-                int64_t* c1);
+                int64_t* c1, int64_t* pad);
 
 // ------------------------------------------------------------------------------- image plan
 struct Segment {
@@ -90,7 +95,11 @@ struct __attribute__((aligned(16))) CopyTile {   // one 2-D block of a pull (res
   uint64_t dst;        // absolute destination address of the first row
   uint32_t src_pitch, dst_pitch;  // bytes
   uint32_t rows, row_bytes;
-  uint32_t src_rank, align;       // align: 16, 4 or 2 — widest access all addresses allow
+  uint32_t src_rank, align;       // align: 16, 4 or 2 — widest access all addresses allow;
+                                  // | LAM_TILE_TRANSPOSE: element k of row r -> dst + k*dst_pitch + 2r;
+                                  // src_rank == LAM_TILE_ZERO: zero-fill, no source
+  bool transposed() const { return (align & LAM_TILE_TRANSPOSE) != 0; }
+  bool zero() const { return src_rank == LAM_TILE_ZERO; }
 };
 
 // Build pack units for actor rank r from the caller's shards; returns false if uncovered.

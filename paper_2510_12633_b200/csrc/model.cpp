@@ -3,10 +3,13 @@
 // Tensor table: Qwen2 state-dict order ("Qwen2.5").  TP rules follow
 // vLLM's Qwen2 convention ("reshards them according to the rollout sharding strategy";
 // SURVEY §8(c) C7): qkv = [q_r; k_r; v_r], gate_up = [gate_r; up_r] (dim-0 shards), o/down split on
-// dim 1, embed/lm_head split by vocab rows, norms replicated.
+// dim 1, embed/lm_head split by padded vocab rows, norms replicated; q/k/v split by whole heads with
+// KV heads replicated when tp > kv_heads (R14, R15).
 #include <math.h>
 #include <stdio.h>
 #include <string.h>
+
+#include <algorithm>
 
 #include "lam_internal.h"
 
@@ -25,12 +28,12 @@ std::vector<Tensor> model_tensors(const lam_model_dims& d) {
   for (int64_t l = 0; l < d.layers; ++l) {
     snprintf(p, sizeof p, "model.layers.%lld.", (long long)l);
     std::string s(p);
-    t.push_back({s + "self_attn.q_proj.weight", q, H, 2});
-    t.push_back({s + "self_attn.q_proj.bias", q, 1, 1});
-    t.push_back({s + "self_attn.k_proj.weight", kv, H, 2});
-    t.push_back({s + "self_attn.k_proj.bias", kv, 1, 1});
-    t.push_back({s + "self_attn.v_proj.weight", kv, H, 2});
-    t.push_back({s + "self_attn.v_proj.bias", kv, 1, 1});
+    t.push_back({s + "self_attn.q_proj.weight", q, H, 2, d.heads});
+    t.push_back({s + "self_attn.q_proj.bias", q, 1, 1, d.heads});
+    t.push_back({s + "self_attn.k_proj.weight", kv, H, 2, d.kv_heads});
+    t.push_back({s + "self_attn.k_proj.bias", kv, 1, 1, d.kv_heads});
+    t.push_back({s + "self_attn.v_proj.weight", kv, H, 2, d.kv_heads});
+    t.push_back({s + "self_attn.v_proj.bias", kv, 1, 1, d.kv_heads});
     t.push_back({s + "self_attn.o_proj.weight", H, q, 2});
     t.push_back({s + "mlp.gate_proj.weight", I, H, 2});
     t.push_back({s + "mlp.up_proj.weight", I, H, 2});
@@ -44,15 +47,39 @@ std::vector<Tensor> model_tensors(const lam_model_dims& d) {
 }
 
 bool part_slice(const Tensor& t, int rule, int tp, int rank, int64_t* r0, int64_t* r1, int64_t* c0,
-                int64_t* c1) {
-  *r0 = 0; *r1 = t.d0; *c0 = 0; *c1 = t.d1;
+                int64_t* c1, int64_t* pad) {
+  *r0 = 0; *r1 = t.d0; *c0 = 0; *c1 = t.d1; *pad = 0;
   switch (rule) {
     case LAM_REPLICATE: return true;
     case LAM_SHARD_DIM0:
-    case LAM_VOCAB_DIM0:
       if (t.d0 % tp) return false;
       *r0 = rank * (t.d0 / tp); *r1 = *r0 + t.d0 / tp;
       return true;
+    case LAM_VOCAB_DIM0: {   // padded rows [rank*n, (rank+1)*n) of Vp; rows >= d0 are zero
+      const int64_t vp = (t.d0 + kVocabPad - 1) / kVocabPad * kVocabPad;
+      if (vp % tp) return false;
+      const int64_t n = vp / tp;
+      *r0 = std::min<int64_t>(rank * n, t.d0);
+      *r1 = std::min<int64_t>((rank + 1) * n, t.d0);
+      *pad = n - (*r1 - *r0);
+      return true;
+    }
+    case LAM_HEAD_DIM0: {    // whole heads; KV heads replicated when tp > heads
+      if (t.heads < 1 || t.d0 % t.heads) return false;
+      const int64_t hd = t.d0 / t.heads;
+      int64_t h0, nh;
+      if (tp <= t.heads) {
+        if (t.heads % tp) return false;
+        nh = t.heads / tp;
+        h0 = rank * nh;
+      } else {
+        if (tp % t.heads) return false;
+        nh = 1;
+        h0 = rank / (tp / t.heads);
+      }
+      *r0 = h0 * hd; *r1 = (h0 + nh) * hd;
+      return true;
+    }
     case LAM_SHARD_DIM1:
       if (t.ndim != 2 || t.d1 % tp) return false;
       *c0 = rank * (t.d1 / tp); *c1 = *c0 + t.d1 / tp;
@@ -68,11 +95,11 @@ bool vllm_layout(const lam_model_dims& d, int tp, std::vector<VllmDst>* out) {
   auto add = [&](const std::string& name, std::vector<DstPart> parts) -> bool {
     VllmDst v{name, 0, 0, parts};
     for (auto& p : parts) {
-      int64_t r0, r1, c0, c1;
-      if (!part_slice(ts[p.tensor], p.rule, tp, 0, &r0, &r1, &c0, &c1)) return false;
+      int64_t r0, r1, c0, c1, pad;
+      if (!part_slice(ts[p.tensor], p.rule, tp, 0, &r0, &r1, &c0, &c1, &pad)) return false;
       if (v.cols && v.cols != c1 - c0) return false;
       v.cols = c1 - c0;
-      v.rows += r1 - r0;
+      v.rows += r1 - r0 + pad;
     }
     out->push_back(v);
     return true;
@@ -86,8 +113,8 @@ bool vllm_layout(const lam_model_dims& d, int tp, std::vector<VllmDst>* out) {
     uint32_t q = id, qb = id + 1, k = id + 2, kb = id + 3, v = id + 4, vb = id + 5, o = id + 6,
              g = id + 7, u = id + 8, dn = id + 9, n1 = id + 10, n2 = id + 11;
     id += 12;
-    ok = ok && add(s + "self_attn.qkv_proj.weight", {{q, LAM_SHARD_DIM0}, {k, LAM_SHARD_DIM0}, {v, LAM_SHARD_DIM0}});
-    ok = ok && add(s + "self_attn.qkv_proj.bias", {{qb, LAM_SHARD_DIM0}, {kb, LAM_SHARD_DIM0}, {vb, LAM_SHARD_DIM0}});
+    ok = ok && add(s + "self_attn.qkv_proj.weight", {{q, LAM_HEAD_DIM0}, {k, LAM_HEAD_DIM0}, {v, LAM_HEAD_DIM0}});
+    ok = ok && add(s + "self_attn.qkv_proj.bias", {{qb, LAM_HEAD_DIM0}, {kb, LAM_HEAD_DIM0}, {vb, LAM_HEAD_DIM0}});
     ok = ok && add(s + "self_attn.o_proj.weight", {{o, LAM_SHARD_DIM1}});
     ok = ok && add(s + "mlp.gate_up_proj.weight", {{g, LAM_SHARD_DIM0}, {u, LAM_SHARD_DIM0}});
     ok = ok && add(s + "mlp.down_proj.weight", {{dn, LAM_SHARD_DIM1}});

@@ -180,6 +180,49 @@ static void emit_block(std::vector<CopyTile>* out, uint32_t rank, uint64_t src_o
   }
 }
 
+// Transposed (K-major) part: source rows [r0, r1) x cols [c0, c1) of tensor t, element (i, c) to
+// dbase + (c - c0) * tpitch + (row0 + i - r0) * 2.  Whole rows inside a segment become tiles of
+// <= kPullTRows rows x kPullTCols columns (the kernel moves them as 8x8 register transposes); rows
+// cut by a segment boundary (FSDP1 flat cuts) become single-row tiles.
+static void emit_transposed_part(std::vector<CopyTile>* out, const ImagePlan& p, const Tensor& t, uint32_t tid,
+                                 int64_t r0, int64_t r1, int64_t c0, int64_t c1, uint64_t dbase, uint64_t row0,
+                                 uint64_t tpitch, uint64_t* bytes) {
+  const uint64_t d1 = (uint64_t)t.d1, w = (uint64_t)(c1 - c0);
+  auto tile = [&](uint32_t rank, uint64_t src_off, uint64_t i, uint64_t col, uint64_t rows, uint64_t cols) {
+    // rows [i, i + rows) (source row numbers), columns [col, col + cols) relative to c0
+    CopyTile x{src_off, dbase + col * tpitch + (row0 + i - (uint64_t)r0) * 2, (uint32_t)(d1 * 2), (uint32_t)tpitch,
+               (uint32_t)rows, (uint32_t)(cols * 2), rank, 0};
+    if (rows == 1) x.src_pitch = 0;
+    x.align = widest_align(x.src_off, x.dst, x.src_pitch, x.dst_pitch, 0) | LAM_TILE_TRANSPOSE;
+    out->push_back(x);
+    *bytes += rows * cols * 2;
+  };
+  for (uint32_t si : p.by_tensor[tid]) {
+    const Segment& s = p.segs[si];
+    const uint64_t e0 = s.elem0, e1 = s.elem0 + s.count;
+    // source rows of the slice that intersect [e0, e1)
+    const uint64_t ia = std::max<uint64_t>((uint64_t)r0, e0 / d1), ib = std::min<uint64_t>((uint64_t)r1, cdiv(e1, d1));
+    uint64_t i = ia;
+    while (i < ib) {
+      const uint64_t a = i * d1 + (uint64_t)c0, b = i * d1 + (uint64_t)c1;
+      const uint64_t lo = std::max(a, e0), hi = std::min(b, e1);
+      if (lo >= hi) { ++i; continue; }
+      if (lo != a || hi != b) {   // row cut by the segment: one row, columns [lo - a, hi - a)
+        tile(s.rank, s.off + (lo - e0) * 2, i, lo - a, 1, hi - lo);
+        ++i;
+        continue;
+      }
+      uint64_t j = i;   // maximal run of whole rows inside the segment
+      while (j < ib && j * d1 + (uint64_t)c0 >= e0 && j * d1 + (uint64_t)c1 <= e1) ++j;
+      for (uint64_t r = i; r < j; r += kPullTRows)
+        for (uint64_t col = 0; col < w; col += kPullTCols)
+          tile(s.rank, s.off + (r * d1 + (uint64_t)c0 + col - e0) * 2, r, col, std::min<uint64_t>(kPullTRows, j - r),
+               std::min<uint64_t>(kPullTCols, w - col));
+      i = j;
+    }
+  }
+}
+
 bool build_copy_tiles(const ImagePlan& p, const std::vector<Tensor>& ts, const lam_tp_layout& L,
                       std::vector<CopyTile>* tiles, uint64_t* bytes, std::string* err) {
   tiles->clear();
@@ -190,31 +233,64 @@ bool build_copy_tiles(const ImagePlan& p, const std::vector<Tensor>& ts, const l
   }
   for (int k = 0; k < L.n_dsts; ++k) {
     const lam_dst& d = L.dsts[k];
-    if (d.transpose) { *err = "transpose destinations are not supported yet"; return false; }
     if (!d.dst || d.n_parts < 1 || !d.parts) { *err = "dst " + std::to_string(k) + ": empty"; return false; }
+    // total destination rows (needed by the K-major pitch) and a check of every part
     int64_t width = -1;
-    uint64_t row0 = 0;   // destination row where the current part starts
+    uint64_t total_rows = 0;
+    bool two_d = false;
     for (int q = 0; q < d.n_parts; ++q) {
       if (d.parts[q].tensor_id >= ts.size()) { *err = "bad tensor id"; return false; }
       const Tensor& t = ts[d.parts[q].tensor_id];
-      int64_t r0, r1, c0, c1;
-      if (!part_slice(t, d.parts[q].rule, L.tp_size, L.tp_rank, &r0, &r1, &c0, &c1)) {
+      int64_t r0, r1, c0, c1, pad;
+      if (!part_slice(t, d.parts[q].rule, L.tp_size, L.tp_rank, &r0, &r1, &c0, &c1, &pad)) {
         *err = "rule not applicable to " + t.name;
         return false;
       }
-      int64_t w = c1 - c0;
-      if (width >= 0 && w != width) { *err = "parts of different widths in one dst"; return false; }
-      width = w;
-      uint64_t dpitch = d.dst_row_pitch_bytes ? (uint64_t)d.dst_row_pitch_bytes : (uint64_t)w * 2;
-      if (dpitch < (uint64_t)w * 2) { *err = "row pitch smaller than the row"; return false; }
-      const uint64_t dbase = (uint64_t)(uintptr_t)d.dst;
+      if (width >= 0 && c1 - c0 != width) { *err = "parts of different widths in one dst"; return false; }
+      width = c1 - c0;
+      two_d = two_d || t.ndim == 2;
+      total_rows += (uint64_t)(r1 - r0 + pad);
+    }
+    const bool transpose = d.transpose && two_d;
+    const uint64_t w = (uint64_t)width;
+    uint64_t dpitch;
+    if (transpose) {
+      dpitch = d.dst_row_pitch_bytes ? (uint64_t)d.dst_row_pitch_bytes : total_rows * 2;
+      if (dpitch < total_rows * 2) { *err = "K-major row pitch smaller than the rows"; return false; }
+    } else {
+      dpitch = d.dst_row_pitch_bytes ? (uint64_t)d.dst_row_pitch_bytes : w * 2;
+      if (dpitch < w * 2) { *err = "row pitch smaller than the row"; return false; }
+    }
+    if (dpitch >= (1ull << 32)) { *err = "row pitch too large"; return false; }
+    const uint64_t dbase = (uint64_t)(uintptr_t)d.dst;
+    uint64_t row0 = 0;   // destination row where the current part starts
+    for (int q = 0; q < d.n_parts; ++q) {
+      const Tensor& t = ts[d.parts[q].tensor_id];
+      int64_t r0, r1, c0, c1, pad;
+      part_slice(t, d.parts[q].rule, L.tp_size, L.tp_rank, &r0, &r1, &c0, &c1, &pad);
+      const uint64_t real = (uint64_t)(r1 - r0);
+      if (pad) {   // vocabulary padding rows: zero-filled by the pull (R15)
+        const size_t first = tiles->size();
+        if (transpose)  // K-major: in every destination row c, the run of pad entries after the real rows
+          emit_block(tiles, LAM_TILE_ZERO, 0, dbase + (row0 + real) * 2, 0, dpitch, w, (uint64_t)pad * 2);
+        else
+          emit_block(tiles, LAM_TILE_ZERO, 0, dbase + (row0 + real) * dpitch, 0, dpitch, (uint64_t)pad, w * 2);
+        for (size_t i = first; i < tiles->size(); ++i) (*tiles)[i].src_pitch = 0;
+        *bytes += (uint64_t)pad * w * 2;
+      }
+      if (transpose) {
+        emit_transposed_part(tiles, p, t, d.parts[q].tensor_id, r0, r1, c0, c1, dbase, row0, dpitch, bytes);
+        row0 += real + (uint64_t)pad;
+        continue;
+      }
       // The slice as runs in the flattened source tensor: run k = [start_k, start_k + run) with
       // start_k = (r0 + k) * d1 + c0; a full-row slice is one contiguous run.
       bool full = (c0 == 0 && c1 == t.d1);
-      uint64_t run = full ? (uint64_t)(r1 - r0) * t.d1 : (uint64_t)w;
-      uint64_t nrun = full ? 1 : (uint64_t)(r1 - r0);
+      uint64_t run = full ? real * t.d1 : w;
+      uint64_t nrun = full ? 1 : real;
       uint64_t first = (uint64_t)r0 * t.d1 + c0, stride = (uint64_t)t.d1;
       for (uint32_t si : p.by_tensor[d.parts[q].tensor_id]) {
+        if (real == 0) break;
         const Segment& s = p.segs[si];
         uint64_t e0 = s.elem0, e1 = s.elem0 + s.count;
         // runs overlapping [e0, e1): start_k + run > e0 and start_k < e1
@@ -226,7 +302,7 @@ bool build_copy_tiles(const ImagePlan& p, const std::vector<Tensor>& ts, const l
           continue;
         }
         auto dst_of = [&](uint64_t k, uint64_t col) {   // dst address of run k, element col
-          return full ? dbase + (row0 * (uint64_t)w + col) * 2  // contiguous: col indexes the run
+          return full ? dbase + (row0 * w + col) * 2  // contiguous: col indexes the run
                       : dbase + (row0 + k) * dpitch + col * 2;
         };
         auto src_of = [&](uint64_t el) { return s.off + (el - e0) * 2; };
@@ -244,7 +320,7 @@ bool build_copy_tiles(const ImagePlan& p, const std::vector<Tensor>& ts, const l
             k = k2;
             continue;
           }
-          if (full && dpitch != (uint64_t)w * 2) {
+          if (full && dpitch != w * 2) {
             // pitched destination with full-row source: emit row by row pieces
             for (uint64_t el = lo; el < hi;) {
               uint64_t row = el / t.d1, col = el % t.d1;
@@ -259,75 +335,90 @@ bool build_copy_tiles(const ImagePlan& p, const std::vector<Tensor>& ts, const l
           ++k;
         }
       }
-      row0 += (uint64_t)(r1 - r0);
+      row0 += real + (uint64_t)pad;
     }
   }
   return true;
 }
 
-// Source chunk of a copy tile (tiles never straddle chunks after split_by_chunk).
+// Source chunk of a copy tile (tiles never straddle chunks after split_by_chunk).  Zero tiles
+// read nothing; split_by_chunk parks the chunk they are launched with in src_off.
 uint32_t chunk_of(const ImagePlan& p, const CopyTile& t) {
+  if (t.zero()) return (uint32_t)t.src_off;
   return (uint32_t)(p.chunk_base[t.src_rank] + t.src_off / p.C);
 }
 
 // Cut copy tiles at source-chunk boundaries (whole rows where possible, a row crossing a boundary
-// is split in two) and order them by chunk, so a pull can be launched chunk by chunk.
+// is split in two) and order them by chunk, so a pull can be launched chunk by chunk.  K-major
+// tiles are cut at 8-row groups so every piece keeps the 16-B destination alignment of the 8x8
+// transposes; a group holding a boundary is cut into single rows.  Zero tiles go first.
 std::vector<CopyTile> split_by_chunk(const ImagePlan& p, const std::vector<CopyTile>& in) {
   const uint64_t C = p.C;
-  std::vector<CopyTile> out;
+  std::vector<CopyTile> out, zeros;
   out.reserve(in.size());
+  auto widest = [](uint64_t x) -> uint32_t { return x % 16 == 0 ? 16 : (x % 4 == 0 ? 4 : 2); };
+  // destination step of one source row / one byte of a row
+  auto row_step = [](const CopyTile& t) -> uint64_t { return t.transposed() ? 2 : t.dst_pitch; };
   auto piece = [&](const CopyTile& t, uint64_t r0, uint64_t nrows) {
     CopyTile u = t;
     u.src_off = t.src_off + r0 * t.src_pitch;
-    u.dst = t.dst + r0 * t.dst_pitch;
+    u.dst = t.dst + r0 * row_step(t);
     u.rows = (uint32_t)nrows;
-    if (nrows == 1) u.src_pitch = u.dst_pitch = 0;
+    if (nrows == 1) {
+      u.src_pitch = 0;
+      if (!t.transposed()) u.dst_pitch = 0;
+    }
     out.push_back(u);
   };
-  for (const CopyTile& t : in) {
-    if (t.rows == 1) {  // cut the row at every chunk boundary it crosses (a row may span many chunks)
-      auto widest = [](uint64_t x) -> uint32_t { return x % 16 == 0 ? 16 : (x % 4 == 0 ? 4 : 2); };
-      uint64_t a = t.src_off, dst = t.dst, left = t.row_bytes;
-      while (left > 0) {
-        const uint64_t n = std::min<uint64_t>(left, (a / C + 1) * C - a);
-        CopyTile u = t;
-        u.src_off = a;
-        u.dst = dst;
-        u.row_bytes = (uint32_t)n;
-        u.src_pitch = u.dst_pitch = 0;
-        u.align = n == t.row_bytes ? t.align : std::min(t.align, widest(u.src_off | u.dst | u.row_bytes));
-        out.push_back(u);
-        a += n;
+  auto cut_row = [&](const CopyTile& t, uint64_t r) {   // one row, cut at every chunk boundary
+    uint64_t a = t.src_off + r * t.src_pitch, dst = t.dst + r * row_step(t), left = t.row_bytes;
+    while (left > 0) {
+      const uint64_t n = std::min<uint64_t>(left, (a / C + 1) * C - a);
+      CopyTile u = t;
+      u.src_off = a;
+      u.dst = dst;
+      u.rows = 1;
+      u.row_bytes = (uint32_t)n;
+      u.src_pitch = 0;
+      if (t.transposed()) {
+        u.align = std::min<uint32_t>(t.align & 0xFF, widest(a | dst)) | LAM_TILE_TRANSPOSE;
+        dst += n / 2 * t.dst_pitch;
+      } else {
+        u.dst_pitch = 0;
+        u.align = n == t.row_bytes && t.rows == 1 ? t.align : std::min(t.align, widest(a | dst | n));
         dst += n;
-        left -= n;
       }
-      continue;
+      out.push_back(u);
+      a += n;
+      left -= n;
     }
+  };
+  for (const CopyTile& t : in) {
+    if (t.zero()) { zeros.push_back(t); continue; }
+    if (t.rows == 1) { cut_row(t, 0); continue; }
+    const uint64_t grp = t.transposed() ? 8 : 1;   // rows cut only at multiples of grp
     uint64_t r0 = 0;
-    for (uint64_t r = 0; r < t.rows; ++r) {
-      const uint64_t a = t.src_off + r * t.src_pitch, b = a + t.row_bytes;
+    for (uint64_t g = 0; g < t.rows; g += grp) {
+      const uint64_t ge = std::min<uint64_t>(t.rows, g + grp);
+      const uint64_t a = t.src_off + g * t.src_pitch, b = t.src_off + (ge - 1) * t.src_pitch + t.row_bytes;
       const bool crosses = a / C != (b - 1) / C;
-      const bool new_chunk = r > r0 && a / C != (t.src_off + r0 * t.src_pitch) / C;
+      const bool new_chunk = g > r0 && a / C != (t.src_off + r0 * t.src_pitch) / C;
       if (new_chunk || crosses) {
-        if (r > r0) piece(t, r0, r - r0);
-        r0 = r;
+        if (g > r0) piece(t, r0, g - r0);
+        r0 = g;
       }
       if (crosses) {
-        CopyTile one = t;
-        one.src_off = a;
-        one.dst = t.dst + r * t.dst_pitch;
-        one.rows = 1;
-        one.src_pitch = one.dst_pitch = 0;
-        std::vector<CopyTile> tmp{one};
-        std::vector<CopyTile> cut = split_by_chunk(p, tmp);
-        out.insert(out.end(), cut.begin(), cut.end());
-        r0 = r + 1;
+        for (uint64_t r = g; r < ge; ++r) cut_row(t, r);
+        r0 = ge;
       }
     }
     if (t.rows > r0) piece(t, r0, t.rows - r0);
   }
   std::stable_sort(out.begin(), out.end(),
                    [&](const CopyTile& x, const CopyTile& y) { return chunk_of(p, x) < chunk_of(p, y); });
+  const uint64_t first = out.empty() ? 0 : chunk_of(p, out.front());
+  for (CopyTile& z : zeros) z.src_off = first;
+  out.insert(out.begin(), zeros.begin(), zeros.end());
   return out;
 }
 

@@ -849,6 +849,7 @@ lam_status get_plan(lam_ctx* c, const lam_rollout_desc& ro, const lam_tp_layout&
   }
   pp.chunk_begin.push_back((uint32_t)tiles.size());
   for (const CopyTile& t : tiles) {
+    if (t.zero()) continue;   // padding rows: written, nothing read
     const Part& q = c->parts[c->node_rank_part[ro.node][t.src_rank]];
     (q.device == ro.device ? pp.local_bytes : pp.remote_bytes) += (uint64_t)t.rows * t.row_bytes;
   }
@@ -1159,6 +1160,8 @@ extern "C" lam_status lam_subscribe(lam_ctx* c, int32_t rid, const lam_tp_layout
     for (int q = 0; q < d.n_parts; ++q) {
       const uint32_t t = d.parts[q].tensor_id;
       if (t >= c->ts.size() || tdst[t]) return LAM_EINVAL;
+      // vocabulary padding rows would have to be zero-filled: not a plain image of the tensor
+      if (d.parts[q].rule == LAM_VOCAB_DIM0 && c->ts[t].d0 % kVocabPad) return LAM_EINVAL;
       if (d.dst_row_pitch_bytes && (uint64_t)d.dst_row_pitch_bytes != 2 * (uint64_t)c->ts[t].d1) return LAM_EINVAL;
       tdst[t] = (uint64_t)(uintptr_t)d.dst + off;
       off += 2 * c->ts[t].numel();

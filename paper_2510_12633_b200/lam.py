@@ -20,7 +20,8 @@ LAM_OK, LAM_ENOVERSION, LAM_IDLE = 0, 1, 2
 LAM_EINVAL, LAM_ESTALE, LAM_ECUDA, LAM_ECHECKSUM, LAM_ENOMEM = -1, -2, -3, -4, -5
 LAM_ESHUTDOWN, LAM_EBUSY, LAM_ETIMEOUT, LAM_EIPC = -6, -7, -8, -9
 LAM_FSDP2_DIM0, LAM_FSDP1_FLAT = 0, 1
-LAM_REPLICATE, LAM_SHARD_DIM0, LAM_SHARD_DIM1, LAM_VOCAB_DIM0 = 0, 1, 2, 3
+LAM_REPLICATE, LAM_SHARD_DIM0, LAM_SHARD_DIM1, LAM_VOCAB_DIM0, LAM_HEAD_DIM0 = 0, 1, 2, 3, 4
+LAM_TILE_TRANSPOSE, LAM_TILE_ZERO = 0x100, 0xFFFFFFFF
 LAM_HOP_KERNEL, LAM_HOP_COPY_ENGINE = 0, 1
 
 
@@ -207,12 +208,15 @@ def vllm_layout(d: lam_model_dims, tp: int) -> list[VllmDst]:
 class TPLayout:
     """A rollout TP rank's destination buffers (keeps the ctypes arrays alive)."""
 
-    def __init__(self, tp_size: int, tp_rank: int, dsts: list[tuple[list[tuple[int, int]], int, int]]):
-        """dsts: list of (parts [(tensor_id, rule)], device pointer, row pitch bytes or 0)."""
-        self._parts = [(lam_part * len(p))(*[lam_part(t, r) for t, r in p]) for p, _, _ in dsts]
+    def __init__(self, tp_size: int, tp_rank: int, dsts: list[tuple], transpose: bool = False):
+        """dsts: list of (parts [(tensor_id, rule)], device pointer, row pitch bytes or 0[, transpose]);
+        `transpose` is the default K-major flag of entries without their own."""
+        self._parts = [(lam_part * len(d[0]))(*[lam_part(t, r) for t, r in d[0]]) for d in dsts]
         self._dsts = (lam_dst * max(1, len(dsts)))()
-        for i, (p, ptr, pitch) in enumerate(dsts):
-            self._dsts[i] = lam_dst(C.cast(self._parts[i], C.POINTER(lam_part)), len(p), 0, ptr, pitch)
+        for i, d in enumerate(dsts):
+            p, ptr, pitch = d[:3]
+            tr = d[3] if len(d) > 3 else transpose
+            self._dsts[i] = lam_dst(C.cast(self._parts[i], C.POINTER(lam_part)), len(p), int(bool(tr)), ptr, pitch)
         self.c = lam_tp_layout(tp_size, tp_rank, C.cast(self._dsts, C.POINTER(lam_dst)), len(dsts))
 
 

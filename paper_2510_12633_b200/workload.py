@@ -85,15 +85,17 @@ class ActorShard:
 class RolloutBuffers:
     """bf16 destination buffers of one rollout TP rank in the vLLM Qwen2 convention."""
 
-    def __init__(self, model: lam.lam_model_dims, tp: int, rank: int, device: int):
+    def __init__(self, model: lam.lam_model_dims, tp: int, rank: int, device: int, transpose: bool = False):
+        """`transpose`: every 2-D buffer K-major, i.e. shaped (cols, rows) (R16)."""
         self.layout = lam.vllm_layout(model, tp)
         self.bufs = {}
         dsts = []
         for d in self.layout:
-            shape = (d.rows, d.cols) if d.cols > 1 else (d.rows,)
+            two_d = d.cols > 1   # (a rows x 1 matrix has the same bytes either way)
+            shape = ((d.cols, d.rows) if transpose else (d.rows, d.cols)) if two_d else (d.rows,)
             t = torch.empty(shape, dtype=torch.bfloat16, device=f"cuda:{device}")
             self.bufs[d.name] = t
-            dsts.append((d.parts, t.data_ptr(), 0))
+            dsts.append((d.parts, t.data_ptr(), 0, transpose and two_d))
         self.tp = lam.TPLayout(tp, rank, dsts)
         self.bytes = sum(t.numel() * 2 for t in self.bufs.values())
 

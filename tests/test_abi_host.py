@@ -39,12 +39,13 @@ def test_no_gpu_fails_loudly():
     assert e.value.status == lam.LAM_ECUDA
 
 
-@pytest.mark.parametrize("name", ["tiny", "7b", "32b", "72b"])
+@pytest.mark.parametrize("name", ["tiny", "7b", "32b", "72b", "odd"])
 def test_model_table_matches_oracle(name):
     assert lam.model_tensors(MODELS[name]) == otensors(OMODELS[name])
 
 
-@pytest.mark.parametrize("name,tp", [("tiny", 1), ("tiny", 4), ("7b", 2), ("72b", 8)])
+@pytest.mark.parametrize("name,tp", [("tiny", 1), ("tiny", 4), ("tiny", 8), ("7b", 2), ("72b", 8), ("odd", 1),
+                                     ("odd", 4), ("odd", 8)])
 def test_vllm_layout_matches_oracle(name, tp):
     ours = lam.vllm_layout(MODELS[name], tp)
     ref = vllm_dsts(OMODELS[name], tp)
@@ -79,32 +80,50 @@ def _execute_plan(tiles, img_rank_base, img, out_base, out):
     """numpy executor of the library's copy plan (test-only: checks the plan's arithmetic)."""
     for t in tiles:
         for r in range(t.rows):
+            if t.src_rank == lam.LAM_TILE_ZERO:
+                d = t.dst - out_base + r * t.dst_pitch
+                out[d:d + t.row_bytes] = 0
+                continue
             s = img_rank_base[t.src_rank] + t.src_off + r * t.src_pitch
+            if t.align & lam.LAM_TILE_TRANSPOSE:   # element k of row r -> dst + k*dst_pitch + 2r
+                d = t.dst - out_base + 2 * r
+                for k in range(t.row_bytes // 2):
+                    out[d + k * t.dst_pitch:d + k * t.dst_pitch + 2] = img[s + 2 * k:s + 2 * k + 2]
+                continue
             d = t.dst - out_base + r * t.dst_pitch
             out[d:d + t.row_bytes] = img[s:s + t.row_bytes]
 
 
-@pytest.mark.parametrize("layout,N,C,tp", [(FSDP2_DIM0, 1, 1 << 20, 1), (FSDP2_DIM0, 4, 1 << 18, 2),
-                                           (FSDP1_FLAT, 3, 1 << 18, 4), (FSDP2_DIM0, 8, 4096 * 5, 4),
-                                           (FSDP1_FLAT, 8, 4096, 8), (FSDP2_DIM0, 3, 4096 * 3, 2)])
-def test_copy_plan_reproduces_oracle_pull(layout, N, C, tp):
-    d = OMODELS["tiny"]
+@pytest.mark.parametrize("model,layout,N,C,tp,tr", [
+    ("tiny", FSDP2_DIM0, 1, 1 << 20, 1, False), ("tiny", FSDP2_DIM0, 4, 1 << 18, 2, False),
+    ("tiny", FSDP1_FLAT, 3, 1 << 18, 4, False), ("tiny", FSDP2_DIM0, 8, 4096 * 5, 4, False),
+    ("tiny", FSDP1_FLAT, 8, 4096, 8, False), ("tiny", FSDP2_DIM0, 3, 4096 * 3, 2, False),
+    ("odd", FSDP2_DIM0, 1, 4096, 8, False), ("odd", FSDP1_FLAT, 3, 4096, 4, False),
+    ("tiny", FSDP2_DIM0, 1, 1 << 18, 1, True), ("tiny", FSDP1_FLAT, 3, 4096 * 3, 2, True),
+    ("odd", FSDP1_FLAT, 3, 4096, 8, True), ("odd", FSDP2_DIM0, 4, 4096 * 2, 4, True)])
+def test_copy_plan_reproduces_oracle_pull(model, layout, N, C, tp, tr):
+    """The library's pull plan, executed by numpy, reproduces the oracle's pull: fused qkv/gate_up,
+    dim-1 slices, KV-head replication, vocabulary padding (zero tiles), K-major destinations."""
+    d = OMODELS[model]
     plan = image_plan([s for _, s in otensors(d)], N, C, layout)
     img, _ = publish(plan, SEED, 4, specials=True)
     rank_base = [plan.chunk_base[r] * C for r in range(N)]
+    layout_c = lam.vllm_layout(MODELS[model], tp)
     for rank in range(tp):
-        want = direct_pull(d, tp, rank, SEED, 4, specials=True)
-        layout_c = lam.vllm_layout(MODELS["tiny"], tp)
+        want = direct_pull(d, tp, rank, SEED, 4, specials=True, transpose=tr)
         base, offs, o = 1 << 40, {}, 0
         for x in layout_c:
             offs[x.name] = o
             o += -(-x.rows * x.cols * 2 // 256) * 256
-        tpl = lam.TPLayout(tp, rank, [(x.parts, base + offs[x.name], 0) for x in layout_c])
-        tiles = lam.plan_copy_tiles(MODELS["tiny"], LAYOUT[layout], N, C, tpl)
+        tpl = lam.TPLayout(tp, rank, [(x.parts, base + offs[x.name], 0) for x in layout_c], transpose=tr)
+        tiles = lam.plan_copy_tiles(MODELS[model], LAYOUT[layout], N, C, tpl)
         # streaming pulls launch tiles chunk by chunk: every tile must lie inside one source chunk,
-        # and tiles must come in chunk order
+        # and tiles must come in chunk order (zero tiles first: they read nothing)
         chunks = []
         for t in tiles:
+            if t.src_rank == lam.LAM_TILE_ZERO:
+                assert not chunks
+                continue
             lo = t.src_off
             hi = t.src_off + (t.rows - 1) * t.src_pitch + t.row_bytes
             assert lo // C == (hi - 1) // C, (t.src_rank, lo, hi, C)

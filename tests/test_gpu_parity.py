@@ -52,14 +52,14 @@ def check_image(ctx, node, v, oimg, ohdr, C):
         assert a == b, (node, g, a, b)
 
 
-def check_pull(ctx, rid, tp, rank, dev, v, specials, odims):
-    rb = RolloutBuffers(MODELS_BY_DIMS[id(odims)], tp, rank, dev)
+def check_pull(ctx, rid, tp, rank, dev, v, specials, odims, transpose=False):
+    rb = RolloutBuffers(MODELS_BY_DIMS[id(odims)], tp, rank, dev, transpose=transpose)
     rb.fill_(0xFFFF)
     s = torch.cuda.Stream(device=dev)
     got_v = ctx.pull(rid, rb.tp, s.cuda_stream)
     assert got_v == v
     s.synchronize()
-    want = direct_pull(odims, tp, rank, SEED, v, specials=specials)
+    want = direct_pull(odims, tp, rank, SEED, v, specials=specials, transpose=transpose)
     for name, t in rb.bufs.items():
         g = t.view(torch.int16).cpu().numpy().view(np.uint16)
         assert np.array_equal(g, want[name].reshape(g.shape)), (name, rank)
@@ -112,6 +112,49 @@ def test_tiny_publish_pull_single_gpu(layout, N, C, tp):
     check_image(ctx, 0, 1, oimg, ohdr, C)
     for r in range(tp):
         check_pull(ctx, 0, tp, r, 0, 1, True, od)
+    ctx.close()
+
+
+@pytest.mark.parametrize("model,layout,N,C,tps", [
+    ("odd", lam.LAM_FSDP2_DIM0, 1, 4096, (1, 2, 4, 8)),      # KV-head replication, vocab padding
+    ("odd", lam.LAM_FSDP1_FLAT, 3, 4096, (2, 8)),            # ... with mid-row FSDP1 cuts
+    ("tiny", lam.LAM_FSDP2_DIM0, 4, 3 * 4096, (8,)),         # nkv = 4 < tp = 8
+    ("tiny", lam.LAM_FSDP1_FLAT, 3, 1 << 18, (1, 2))])
+@pytest.mark.parametrize("transpose", [False, True])
+def test_pull_rules_and_k_major(model, layout, N, C, tps, transpose):
+    """A6 beyond the configs (R14-R16): HEAD_DIM0 with KV heads replicated when tp > nkv,
+    zero-filled vocabulary padding rows, and K-major (transposed) destinations — full comparison."""
+    od = OMODELS[model]
+    ctx = make_ctx(model, N, [0] * N, [], [(0, 0)], layout=layout, C=C)
+    shards = [ActorShard(MODELS[model], N, r, 0, layout, misalign=(layout == lam.LAM_FSDP1_FLAT)) for r in range(N)]
+    publish_all(ctx, shards, 2, True)
+    until_idle(ctx)
+    for tp in tps:
+        for r in range(tp):
+            check_pull(ctx, 0, tp, r, 0, 2, True, od, transpose=transpose)
+    ctx.close()
+
+
+def test_7b_k_major_tp2_sampled():
+    """K-major TP=2 pull of the 7B bench workload: sampled elements of every destination vs the oracle."""
+    od = OMODELS["7b"]
+    ctx = make_ctx("7b", 1, [0], [], [(0, 0)], C=64 << 20)
+    shard = ActorShard(MODELS["7b"], 1, 0, 0)
+    publish_all(ctx, [shard], 4, False)
+    until_idle(ctx)
+    del shard
+    torch.cuda.empty_cache()
+    rng = np.random.default_rng(1)
+    for rank in range(2):
+        rb = RolloutBuffers(MODELS["7b"], 2, rank, 0, transpose=True)
+        rb.fill_(0xFFFF)
+        assert ctx.pull(0, rb.tp, 0) == 4
+        torch.cuda.synchronize()
+        for name, t in rb.bufs.items():
+            idx = rng.integers(0, t.numel(), 512)
+            got = t.view(-1).view(torch.int16).cpu().numpy().view(np.uint16)[idx]
+            assert np.array_equal(got, dst_elements(od, 2, rank, name, idx, SEED, 4, transpose=True)), name
+        del rb
     ctx.close()
 
 

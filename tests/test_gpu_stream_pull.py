@@ -61,6 +61,45 @@ def test_stream_pull_tiny_chain(tp):
     ctx.close()
 
 
+@pytest.mark.parametrize("model,tp,rank", [("odd", 8, 7), ("odd", 4, 1), ("tiny", 2, 0)])
+def test_stream_pull_k_major(model, tp, rank):
+    """Streaming pull into K-major buffers with zero-filled vocabulary padding and replicated KV heads:
+    transposed tiles are cut at chunk boundaries in 8-row groups, zero tiles go with the first chunk."""
+    n = torch.cuda.device_count()
+    dev = 1 % n
+    od = OMODELS[model]
+    ctx = lam.Context(lam.Config(model=MODELS[model], fsdp_size=3, actor_devices=[0, 0, 0],
+                                 actor_layout=lam.LAM_FSDP1_FLAT, relays=[[dev] * 3],
+                                 rollouts=[(1, dev)], chunk_bytes=4096))
+    shards = [ActorShard(MODELS[model], 3, r, 0, lam.LAM_FSDP1_FLAT) for r in range(3)]
+    rb = RolloutBuffers(MODELS[model], tp, rank, dev, transpose=True)
+    s = torch.cuda.Stream(device=dev)
+    for v in (1, 2):
+        for sh in shards:
+            sh.fill(SEED, v, specials=True)
+        rb.fill_(0xFFFF)
+        torch.cuda.synchronize()
+        for r, sh in enumerate(shards):
+            assert ctx.publish(v, r, sh.shards()) == lam.LAM_OK
+        got = 0
+        t0 = time.time()
+        while got == 0:
+            ctx.relay_step()
+            got = ctx.pull_stream(0, rb.tp, s.cuda_stream, None, v)
+            assert time.time() - t0 < 60
+        assert got == v
+        assert drive(ctx, 0) == (v, 0)
+        s.synchronize()
+        want = direct_pull(od, tp, rank, SEED, v, specials=True, transpose=True)
+        for name, t in rb.bufs.items():
+            g = t.view(torch.int16).cpu().numpy().view(np.uint16)
+            assert np.array_equal(g, want[name].reshape(g.shape)), (v, name)
+        for _ in range(100000):
+            if ctx.relay_step()[0] == lam.LAM_IDLE:
+                break
+    ctx.close()
+
+
 def test_stream_pull_from_master_while_packing():
     od = OMODELS["7b"]
     ctx = lam.Context(lam.Config(model=MODELS["7b"], rollouts=[(0, 0)], chunk_bytes=128 << 20))
