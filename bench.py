@@ -45,8 +45,11 @@ def parse():
     ap.add_argument("--hop-ctas", type=int, default=0)
     ap.add_argument("--hop-mode", default="kernel", choices=["kernel", "ce"],
                     help="relay hop: TMA kernel or copy engines + k_verify")
-    ap.add_argument("--no-stream-pull", action="store_true",
-                    help="rollouts pull only after their relay committed (no chunk-by-chunk reshard)")
+    ap.add_argument("--stream-pull", default="auto", choices=["auto", "on", "off"],
+                    help="on: rollouts reshard chunk by chunk while their relay receives (lam_pull_stream); "
+                         "off: pull once the relay committed (lam_pull); auto: on for chain / relay-tp, off for "
+                         "colocated (there the pull competes with the pack for HBM and gains nothing)")
+    ap.add_argument("--no-stream-pull", action="store_true", help="same as --stream-pull off")
     ap.add_argument("--no-subscribe", action="store_true",
                     help="colocated rollouts pull after the pack instead of being written by it")
     ap.add_argument("--pack-ctas", type=int, default=0)
@@ -215,6 +218,8 @@ def topology(config: str, N: int, tp_arg: int):
 
 def main():
     args = parse()
+    if args.no_stream_pull or args.stream_pull == "off" or (args.stream_pull == "auto" and args.config == "colocated"):
+        args.no_stream_pull = True
     if args.impl == "reference":
         return run_reference(args)
     if os.environ.get("LAM_BENCH_WATCHDOG"):      # debugging aid: dump every thread's stack, then exit

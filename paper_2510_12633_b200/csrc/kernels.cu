@@ -372,33 +372,29 @@ __device__ __forceinline__ void pull_zero(const CopyTile& T, uint8_t* dst) {
   }
 }
 
-// L2 prefetch of a K-major tile's source rows (whole row runs, so DRAM sees long bursts).
-__device__ __forceinline__ void prefetch_t(const CopyTile& T, const uint8_t* const* rank_base) {
-  if (T.src_rank == LAM_TILE_ZERO || !(T.align & LAM_TILE_TRANSPOSE) || (T.align & 0xFFu) != 16) return;
-  const uint8_t* src = rank_base[T.src_rank] + T.src_off;
-  for (uint32_t r = threadIdx.x; r < T.rows; r += kPullThreads)
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src + (size_t)r * T.src_pitch),
-                 "r"(T.row_bytes & ~15u) : "memory");
-}
-
-__global__ void __launch_bounds__(kPullThreads, 1) k_pull(const CopyTile* __restrict__ tiles, uint32_t n_tiles,
-                                                       const uint8_t* const* __restrict__ rank_base, int pf) {
+// K-major tiles only (one CTA per SM: 128 KiB of staging smem); other tiles are skipped.
+__global__ void __launch_bounds__(kPullThreads, 1) k_pull_t(const CopyTile* __restrict__ tiles, uint32_t n_tiles,
+                                                         const uint8_t* const* __restrict__ rank_base) {
   extern __shared__ __align__(128) uint8_t pull_smem[];
-  if (pf == 2 && blockIdx.x < n_tiles) prefetch_t(tiles[blockIdx.x], rank_base);
   for (uint32_t ti = blockIdx.x; ti < n_tiles; ti += gridDim.x) {
     const CopyTile T = tiles[ti];
-    if (pf == 1) prefetch_t(T, rank_base);
-    if (pf == 2 && ti + gridDim.x < n_tiles) prefetch_t(tiles[ti + gridDim.x], rank_base);
+    if (T.src_rank == LAM_TILE_ZERO || !(T.align & LAM_TILE_TRANSPOSE)) continue;
+    pull_transposed(T, rank_base[T.src_rank] + T.src_off, reinterpret_cast<uint8_t*>(T.dst), pull_smem);
+  }
+}
+
+// Row-major and zero tiles (no shared memory: co-resides with k_hop); K-major tiles are skipped.
+__global__ void __launch_bounds__(kPullThreads) k_pull(const CopyTile* __restrict__ tiles, uint32_t n_tiles,
+                                                       const uint8_t* const* __restrict__ rank_base) {
+  for (uint32_t ti = blockIdx.x; ti < n_tiles; ti += gridDim.x) {
+    const CopyTile T = tiles[ti];
     uint8_t* dst = reinterpret_cast<uint8_t*>(T.dst);
     if (T.src_rank == LAM_TILE_ZERO) {
       pull_zero(T, dst);
       continue;
     }
+    if (T.align & LAM_TILE_TRANSPOSE) continue;
     const uint8_t* src = rank_base[T.src_rank] + T.src_off;
-    if (T.align & LAM_TILE_TRANSPOSE) {
-      pull_transposed(T, src, dst, pull_smem);
-      continue;
-    }
     if (T.align == 16) {
       const uint32_t vpr = T.row_bytes >> 4, total = vpr * T.rows;
       if (T.rows == 1) {
@@ -454,15 +450,27 @@ __global__ void __launch_bounds__(kPullThreads, 1) k_pull(const CopyTile* __rest
   }
 }
 
-int launch_pull(const CopyTile* tiles, uint32_t n_tiles, const uint8_t* const* rank_base, int ctas, void* stream) {
+int launch_pull(const CopyTile* tiles, uint32_t n_tiles, const uint8_t* const* rank_base, int ctas, void* stream,
+                uint32_t kinds) {
   if (n_tiles == 0) return 0;
-  static const bool attr = cudaFuncSetAttribute(k_pull, cudaFuncAttributeMaxDynamicSharedMemorySize, kPullSmem) ==
-                           cudaSuccess;
-  if (!attr) return (int)cudaErrorInvalidValue;
-  if (ctas <= 0) ctas = resident_ctas(k_pull, kPullThreads, kPullSmem);
-  unsigned grid = (unsigned)(n_tiles < (uint32_t)ctas ? n_tiles : (uint32_t)ctas);
-  static const int pf = getenv("LAM_PULL_PF") ? atoi(getenv("LAM_PULL_PF")) : 0;
-  k_pull<<<grid, kPullThreads, kPullSmem, (cudaStream_t)stream>>>(tiles, n_tiles, rank_base, pf);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (kinds & kPullKMajor) {
+    static uint32_t attr_set = 0;   // per device: k_pull_t's dynamic shared memory limit
+    if (!(attr_set & (1u << dev))) {
+      cudaError_t e = cudaFuncSetAttribute(k_pull_t, cudaFuncAttributeMaxDynamicSharedMemorySize, kPullSmem);
+      if (e != cudaSuccess) return (int)e;
+      attr_set |= 1u << dev;
+    }
+    const int n = ctas > 0 ? ctas : resident_ctas(k_pull_t, kPullThreads, kPullSmem);
+    const unsigned grid = (unsigned)std::min<uint32_t>(n_tiles, (uint32_t)n);
+    k_pull_t<<<grid, kPullThreads, kPullSmem, (cudaStream_t)stream>>>(tiles, n_tiles, rank_base);
+  }
+  if (kinds & kPullRowMajor) {
+    const int n = ctas > 0 ? ctas : resident_ctas(k_pull, kPullThreads);
+    const unsigned grid = (unsigned)std::min<uint32_t>(n_tiles, (uint32_t)n);
+    k_pull<<<grid, kPullThreads, 0, (cudaStream_t)stream>>>(tiles, n_tiles, rank_base);
+  }
   return (int)cudaGetLastError();
 }
 

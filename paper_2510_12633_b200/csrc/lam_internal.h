@@ -114,7 +114,12 @@ bool build_copy_tiles(const ImagePlan& p, const std::vector<Tensor>& ts, const l
                       std::vector<CopyTile>* tiles, uint64_t* bytes, std::string* err);
 // Source chunk of a tile; cut tiles at source-chunk boundaries and order them by chunk.
 uint32_t chunk_of(const ImagePlan& p, const CopyTile& t);
-std::vector<CopyTile> split_by_chunk(const ImagePlan& p, const std::vector<CopyTile>& in);
+uint64_t chunk_order(const ImagePlan& p, uint32_t g, int rot);
+std::vector<CopyTile> split_by_chunk(const ImagePlan& p, const std::vector<CopyTile>& in, int rot);
+// Rank rotation of a TP rank's pull: spreads the TP ranks over the source rank regions.
+inline int pull_rotation(const ImagePlan& p, const lam_tp_layout& L) {
+  return L.tp_size > 0 ? (int)((int64_t)L.tp_rank * p.N / L.tp_size) : 0;
+}
 
 // ------------------------------------------------------------------------------ kernel entry
 struct ChunkMeta {          // device view of one slot's metadata in a node part
@@ -132,8 +137,9 @@ int launch_pack(const PackUnit* units, uint32_t n_units, const float* const* sha
 int launch_hop(const HopTile* tiles, uint32_t n_tiles, const RankLink* links, ChunkMeta meta,
                const uint32_t* tiles_per_chunk, uint64_t version, uint32_t* err_word,
                uint64_t timeout_ns, int ctas, void* stream);
+constexpr uint32_t kPullRowMajor = 1, kPullKMajor = 2;   // tile kinds present in a pull (launch_pull)
 int launch_pull(const CopyTile* tiles, uint32_t n_tiles, const uint8_t* const* rank_base, int ctas,
-                void* stream);
+                void* stream, uint32_t kinds);
 // Diagnostics (LAM_HOP_PROF=1): 7 per-device cycle counters accumulated by k_hop's thread 0.
 int hop_set_profile(unsigned long long* buf);
 // One-thread kernel: spin until (int64)(*flag - v) >= 0 or timeout (fallback for stream memory ops).

@@ -144,9 +144,11 @@ void build_hop_tiles(const ImagePlan& p, const std::vector<int>& ranks, std::vec
       }
     }
   }
-  // order tiles by chunk so the pipeline advances chunk by chunk across all ranks of the part
-  std::stable_sort(tiles->begin(), tiles->end(),
-                   [](const HopTile& a, const HopTile& b) { return a.chunk < b.chunk; });
+  // order tiles so the pipeline advances chunk by chunk across all ranks of the part: chunk j of
+  // every rank region before chunk j + 1 of any (the regions are produced side by side)
+  std::stable_sort(tiles->begin(), tiles->end(), [&](const HopTile& a, const HopTile& b) {
+    return chunk_order(p, a.chunk, 0) < chunk_order(p, b.chunk, 0);
+  });
 }
 
 static uint32_t widest_align(uint64_t a, uint64_t b, uint64_t c, uint64_t d, uint64_t e) {
@@ -214,8 +216,8 @@ static void emit_transposed_part(std::vector<CopyTile>* out, const ImagePlan& p,
       }
       uint64_t j = i;   // maximal run of whole rows inside the segment
       while (j < ib && j * d1 + (uint64_t)c0 >= e0 && j * d1 + (uint64_t)c1 <= e1) ++j;
-      for (uint64_t r = i; r < j; r += kPullTRows)
-        for (uint64_t col = 0; col < w; col += kPullTCols)
+      for (uint64_t col = 0; col < w; col += kPullTCols)
+        for (uint64_t r = i; r < j; r += kPullTRows)
           tile(s.rank, s.off + (r * d1 + (uint64_t)c0 + col - e0) * 2, r, col, std::min<uint64_t>(kPullTRows, j - r),
                std::min<uint64_t>(kPullTCols, w - col));
       i = j;
@@ -348,11 +350,21 @@ uint32_t chunk_of(const ImagePlan& p, const CopyTile& t) {
   return (uint32_t)(p.chunk_base[t.src_rank] + t.src_off / p.C);
 }
 
+// Launch order of source chunks for a pull: chunk j of every rank region before chunk j + 1 of any
+// (FSDP ranks pack, and relays receive, their regions side by side, so the j-th chunks become
+// available together), ranks rotated by `rot` so that concurrent pullers read from different GPUs
+// (sorting rank-major made every TP rank read the same peer at once: 4 x slower NVLink gathers).
+uint64_t chunk_order(const ImagePlan& p, uint32_t g, int rot) {
+  const uint32_t r = p.chunk_rank[g];
+  const uint64_t j = g - p.chunk_base[r];
+  return j * (uint64_t)p.N + (uint64_t)((r + p.N - (uint32_t)(rot % p.N)) % p.N);
+}
+
 // Cut copy tiles at source-chunk boundaries (whole rows where possible, a row crossing a boundary
-// is split in two) and order them by chunk, so a pull can be launched chunk by chunk.  K-major
+// is split in two) and order them by chunk_order, so a pull can be launched chunk by chunk.  K-major
 // tiles are cut at 8-row groups so every piece keeps the 16-B destination alignment of the 8x8
 // transposes; a group holding a boundary is cut into single rows.  Zero tiles go first.
-std::vector<CopyTile> split_by_chunk(const ImagePlan& p, const std::vector<CopyTile>& in) {
+std::vector<CopyTile> split_by_chunk(const ImagePlan& p, const std::vector<CopyTile>& in, int rot) {
   const uint64_t C = p.C;
   std::vector<CopyTile> out, zeros;
   out.reserve(in.size());
@@ -414,8 +426,9 @@ std::vector<CopyTile> split_by_chunk(const ImagePlan& p, const std::vector<CopyT
     }
     if (t.rows > r0) piece(t, r0, t.rows - r0);
   }
-  std::stable_sort(out.begin(), out.end(),
-                   [&](const CopyTile& x, const CopyTile& y) { return chunk_of(p, x) < chunk_of(p, y); });
+  std::stable_sort(out.begin(), out.end(), [&](const CopyTile& x, const CopyTile& y) {
+    return chunk_order(p, chunk_of(p, x), rot) < chunk_order(p, chunk_of(p, y), rot);
+  });
   const uint64_t first = out.empty() ? 0 : chunk_of(p, out.front());
   for (CopyTile& z : zeros) z.src_off = first;
   out.insert(out.begin(), zeros.begin(), zeros.end());
@@ -450,7 +463,7 @@ extern "C" int64_t lam_plan_copy_tiles(const lam_model_dims* d, int32_t layout, 
   uint64_t bytes = 0;
   std::string err;
   if (!build_copy_tiles(p, ts, *L, &tiles, &bytes, &err)) return LAM_EINVAL;
-  tiles = split_by_chunk(p, tiles);
+  tiles = split_by_chunk(p, tiles, pull_rotation(p, *L));
   if (out) {
     for (size_t i = 0; i < tiles.size() && (int64_t)i < cap; ++i) {
       const CopyTile& t = tiles[i];

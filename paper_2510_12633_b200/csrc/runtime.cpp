@@ -102,6 +102,7 @@ struct PullPlan {
   CopyTile* d_tiles = nullptr;        // ordered by source chunk
   uint32_t n_tiles = 0;
   uint64_t bytes = 0, local_bytes = 0, remote_bytes = 0;
+  uint32_t kinds = 0;                 // kPullRowMajor (row-major / zero tiles) | kPullKMajor
   std::vector<uint32_t> chunk_ids;    // source chunks in order
   std::vector<uint32_t> chunk_begin;  // [chunk_ids.size() + 1] tile ranges per chunk
 };
@@ -154,6 +155,7 @@ struct lam_ctx {
     uint32_t next = 0;                // next chunk (index into plan->chunk_ids) to launch
     cudaStream_t stream = nullptr;
     cudaEvent_t done = nullptr;
+    cudaEvent_t last = nullptr;       // recorded after the latest reshard launch (on the rollout's device)
   };
   std::vector<StreamPull> streams;    // [n_rollouts]
   // kernel timing (lam_set_profiling)
@@ -689,6 +691,7 @@ lam_status launch_hop_part(lam_ctx* c, Part& p, int s, bool* launched) {
 
 // Streaming pull progress (lam_pull_stream): launch the reshard of every newly verified chunk (the
 // producers mirror chunk flags into the shared control block), then close with the done event.
+constexpr uint32_t kStreamBatches = 8;
 lam_status stream_progress(lam_ctx* c, int rid, int* transitions) {
   lam_ctx::StreamPull& sp = c->streams[rid];
   if (!sp.active) return LAM_OK;
@@ -703,12 +706,22 @@ lam_status stream_progress(lam_ctx* c, int rid, int* transitions) {
     while (sp.next < n && (sl.state == S_COMPLETE ||
                            __atomic_load_n(mir + sp.plan->chunk_ids[sp.next], __ATOMIC_ACQUIRE) == sp.v))
       ++sp.next;
+    // While the previous reshard launch is still running, wait for a batch of >= n/8 chunks (or the
+    // rest): launches on one stream serialise and each pays a tail of straggling tiles, so hundreds of
+    // one-chunk launches behind each other cost more than they overlap.  An idle stream (the usual
+    // case behind a chain hop, where chunks arrive slower than they reshard) launches at once.
+    const uint32_t min_batch = std::max<uint32_t>(1, (n + kStreamBatches - 1) / kStreamBatches);
+    if (sp.next > first && sp.next - first < min_batch && sp.next < n && sl.state != S_COMPLETE && sp.last &&
+        cudaEventQuery(sp.last) == cudaErrorNotReady)
+      sp.next = first;
     if (sp.next > first) {
       auto rb = c->d_rank_base.find({sp.node * LAM_MAX_SLOTS + sp.slot, sp.device});
       const uint32_t b = sp.plan->chunk_begin[first], e = sp.plan->chunk_begin[sp.next];
       cudaEvent_t t0 = prof_begin(c, sp.device, sp.stream);
-      if (launch_pull(sp.plan->d_tiles + b, e - b, rb->second, c->pull_ctas, sp.stream)) return LAM_ECUDA;
+      if (launch_pull(sp.plan->d_tiles + b, e - b, rb->second, c->pull_ctas, sp.stream, sp.plan->kinds)) return LAM_ECUDA;
       prof_end(c, 2, sp.device, sp.stream, t0);
+      if (!sp.last) CK(cudaEventCreateWithFlags(&sp.last, cudaEventDisableTiming));
+      CK(cudaEventRecord(sp.last, sp.stream));
       (*transitions)++;
     }
     if (sp.next < n) return LAM_OK;
@@ -836,7 +849,12 @@ lam_status get_plan(lam_ctx* c, const lam_rollout_desc& ro, const lam_tp_layout&
     fprintf(stderr, "liblam: lam_pull: %s\n", err.c_str());
     return LAM_EINVAL;
   }
-  tiles = split_by_chunk(c->plan, tiles);
+  // start with the rank region stored on the rollout's own GPU (colocated FSDP shards): pullers then
+  // walk the source GPUs as a permutation at every step instead of queueing on the same peer
+  int rot = pull_rotation(c->plan, L);
+  for (int r = 0; r < c->cfg.fsdp_size; ++r)
+    if (c->parts[c->node_rank_part[ro.node][r]].device == ro.device) { rot = r; break; }
+  tiles = split_by_chunk(c->plan, tiles, rot);
   PullPlan pp;
   pp.n_tiles = (uint32_t)tiles.size();
   pp.bytes = bytes;
@@ -849,6 +867,7 @@ lam_status get_plan(lam_ctx* c, const lam_rollout_desc& ro, const lam_tp_layout&
   }
   pp.chunk_begin.push_back((uint32_t)tiles.size());
   for (const CopyTile& t : tiles) {
+    pp.kinds |= t.transposed() ? kPullKMajor : kPullRowMajor;
     if (t.zero()) continue;   // padding rows: written, nothing read
     const Part& q = c->parts[c->node_rank_part[ro.node][t.src_rank]];
     (q.device == ro.device ? pp.local_bytes : pp.remote_bytes) += (uint64_t)t.rows * t.row_bytes;
@@ -1226,7 +1245,7 @@ extern "C" lam_status lam_pull(lam_ctx* c, int32_t rid, const lam_tp_layout* L, 
     return LAM_EINVAL;
   }
   cudaEvent_t t0 = prof_begin(c, ro.device, (cudaStream_t)stream);
-  int rc = launch_pull(pp->d_tiles, pp->n_tiles, rb->second, c->pull_ctas, stream);
+  int rc = launch_pull(pp->d_tiles, pp->n_tiles, rb->second, c->pull_ctas, stream, pp->kinds);
   if (rc) {
     ctl::unpin(c->shm, ro.node, s);
     fprintf(stderr, "liblam: pull launch failed: %s\n", cudaGetErrorString((cudaError_t)rc));

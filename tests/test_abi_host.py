@@ -118,7 +118,10 @@ def test_copy_plan_reproduces_oracle_pull(model, layout, N, C, tp, tr):
         tpl = lam.TPLayout(tp, rank, [(x.parts, base + offs[x.name], 0) for x in layout_c], transpose=tr)
         tiles = lam.plan_copy_tiles(MODELS[model], LAYOUT[layout], N, C, tpl)
         # streaming pulls launch tiles chunk by chunk: every tile must lie inside one source chunk,
-        # and tiles must come in chunk order (zero tiles first: they read nothing)
+        # and tiles must come in launch order — chunk j of every rank before chunk j + 1, ranks
+        # rotated by tp_rank * N / tp (zero tiles first: they read nothing)
+        rot = rank * N // tp
+        order = lambda g: (g - plan.chunk_base[plan.chunk_rank(g)], (plan.chunk_rank(g) - rot) % N)
         chunks = []
         for t in tiles:
             if t.src_rank == lam.LAM_TILE_ZERO:
@@ -128,7 +131,7 @@ def test_copy_plan_reproduces_oracle_pull(model, layout, N, C, tp, tr):
             hi = t.src_off + (t.rows - 1) * t.src_pitch + t.row_bytes
             assert lo // C == (hi - 1) // C, (t.src_rank, lo, hi, C)
             chunks.append(plan.chunk_base[t.src_rank] + lo // C)
-        assert chunks == sorted(chunks)
+        assert chunks == sorted(chunks, key=order)
         out = np.full(o, 0xAB, dtype=np.uint8)
         _execute_plan(tiles, rank_base, img, base, out)
         for x in layout_c:
