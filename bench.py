@@ -38,8 +38,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="lam", choices=["lam", "reference"])
     ap.add_argument("--model", default="7b")
-    ap.add_argument("--config", default="chain", choices=["chain", "colocated", "relay-tp"],
-                    help="placement: chain (config 2), colocated (config 4), relay-tp (config 3)")
+    ap.add_argument("--config", default="chain", choices=["chain", "colocated", "relay-tp", "host"],
+                    help="placement: chain (config 2), colocated (config 4), relay-tp (config 3), "
+                         "host (NEXT-3: the paper's host-memory relay tier)")
     ap.add_argument("--tp", type=int, default=0, help="rollout TP size (colocated / relay-tp)")
     ap.add_argument("--chunk-mb", type=int, default=0, help="chunk size; 0 = Appendix D k*")
     ap.add_argument("--hop-ctas", type=int, default=0)
@@ -188,6 +189,17 @@ class Clocks:
 # -------------------------------------------------------------------------------- GPU leg
 def topology(config: str, N: int, tp_arg: int):
     """Placement of actor ranks, relay nodes and rollouts on N GPUs (BASELINE.json configs)."""
+    if config == "host":
+        # NEXT-3 (PAPER L396-418, L637-646): actor FSDP-1 on GPU 0 -> one relay node in pinned host
+        # memory (received by GPU min(1, N-1) over PCIe) -> TP rollouts on GPUs 1..N-1 (GPU 0 at N=1)
+        # pull from host memory over their own PCIe links
+        g = min(1, N - 1)
+        tp = tp_arg or 1
+        gpus = list(range(g, N))
+        ro = [(1, gpus[k * tp + j], tp, j) for k in range(len(gpus) // tp) for j in range(tp)]
+        return dict(fsdp=1, actors=[0], relays=[[g]], host_relays=[1], rollouts=ro,
+                    desc=f"actor FSDP-1 on GPU0 -> host-memory relay (received by GPU{g}) -> "
+                         f"{len(ro) // tp} TP={tp} rollout(s) on GPUs {g}..{N - 1} pulling over PCIe")
     if config == "chain" or N == 1:
         # config 2: actor FSDP-1 on GPU 0 -> chain of relays on GPUs 1..N-1, one TP=1 rollout each
         if N == 1:
@@ -256,7 +268,8 @@ def main():
                      proc_rank=rank, n_procs=N, proc_of_device={d: d for d in range(N)},
                      shm_name=f"lam_bench_{port}_{os.getppid()}", hop_ctas=args.hop_ctas,
                      pack_ctas=args.pack_ctas, pull_ctas=args.pull_ctas,
-                     hop_mode=lam.LAM_HOP_COPY_ENGINE if args.hop_mode == "ce" else lam.LAM_HOP_KERNEL)
+                     hop_mode=lam.LAM_HOP_COPY_ENGINE if args.hop_mode == "ce" else lam.LAM_HOP_KERNEL,
+                     host_relays=T.get("host_relays", []))
     ctx = lam.Context(cfg)
     if N > 1:
         blobs = [None] * N
@@ -363,6 +376,11 @@ def main():
     ms_max = allmax(ms)
     launches_all = int(allsum(launches))
     avg = {k: (v / n if n else None) for k, (v, n) in kt.items()}
+    # a streamed pull is many k_pull launches (one batch per arriving chunk): per pull = the sum of
+    # this rank's pull launches / (timed steps x rollouts pulled here)
+    n_pulled = len([rid for rid in mine if rid not in subs])
+    if kt["pull"][1] and n_pulled:
+        avg["pull"] = kt["pull"][0] / (args.steps * n_pulled)
     # per-rank roofline candidates of this rank's dominant kernel work
     cand = []
     if avg["pack"]:
@@ -370,12 +388,14 @@ def main():
         b = (8.0 if subs else 6.0) * sum(sh.numel for sh in shards.values())
         cand.append(dict(kernel="k_pack" + ("+subscriber" if subs else ""), ms=avg["pack"], bound="hbm", bytes=b))
     if avg["hop"]:
-        part_bytes = sum(info.snapshot_bytes for _ in [0]) if args.config == "chain" else M / max(1, T["fsdp"])
-        cand.append(dict(kernel="k_hop", ms=avg["hop"], bound="nvlink", bytes=float(part_bytes)))
+        part_bytes = M if args.config in ("chain", "host") else M / max(1, T["fsdp"])
+        cand.append(dict(kernel="k_hop", ms=avg["hop"], bound="pcie" if args.config == "host" else "nvlink",
+                         bytes=float(part_bytes)))
     if avg["pull"] and mine:
         loc, rem = pull_bytes[mine[0]]
         if rem > 0:
-            cand.append(dict(kernel="k_pull", ms=avg["pull"], bound="nvlink", bytes=float(rem), local=loc, remote=rem))
+            cand.append(dict(kernel="k_pull", ms=avg["pull"], bound="pcie" if args.config == "host" else "nvlink",
+                             bytes=float(rem), local=loc, remote=rem))
         else:
             cand.append(dict(kernel="k_pull", ms=avg["pull"], bound="hbm", bytes=2.0 * loc, local=loc, remote=rem))
     per_rank = [None] * N
@@ -387,6 +407,7 @@ def main():
         per_rank = [mine_info]
 
     kmax = {k: allmax(v or 0.0) for k, v in avg.items()}   # collective: every rank, outside rank-0 code
+    pcie_peak = measure_pcie(torch) if args.config == "host" and rank == 0 else None
     e2e = None
     if not args.quick and not args.no_e2e:
         e2e = run_e2e(args, N, shards, bufs, mine, step, barrier, allmax, torch)
@@ -404,14 +425,17 @@ def main():
         dom = max(allc, key=lambda c: c["ms"]) if allc else None
         roof = None
         if dom:
-            peak = hbm_peak if dom["bound"] == "hbm" else nvl_peak
+            if dom["bound"] == "pcie":
+                peak, src = pcie_peak
+            else:
+                peak = hbm_peak if dom["bound"] == "hbm" else nvl_peak
+                src = ("MEASURED_PEAKS.json hbm_gbs (burst copy)" if dom["bound"] == "hbm" and "hbm_gbs" in peaks
+                       else "fallback 6.65 TB/s" if dom["bound"] == "hbm"
+                       else "B200_PROFILING.md measured peer copy 770 GB/s/dir (nominal 900)")
             ach = dom["bytes"] / (dom["ms"] / 1e3) / 1e9
             roof = dict(bound=dom["bound"], kernel=dom["kernel"], achieved=ach, peak=peak, unit="GB/s",
                         frac=ach / peak, traffic=traffic_of(dom["kernel"], args.model, N, args.config),
-                        algorithmic_bytes_per_launch=dom["bytes"], launch_ms=dom["ms"],
-                        peak_source=("MEASURED_PEAKS.json hbm_gbs (burst copy)" if dom["bound"] == "hbm" and "hbm_gbs" in peaks
-                                     else "fallback 6.65 TB/s" if dom["bound"] == "hbm"
-                                     else "B200_PROFILING.md measured peer copy 770 GB/s/dir (nominal 900)"))
+                        algorithmic_bytes_per_launch=dom["bytes"], launch_ms=dom["ms"], peak_source=src)
         cpu = None
         if N == 1 and not args.quick and not args.no_cpu_baseline:
             _, cpu = oracle_sample(args.model, args.cpu_seconds)
@@ -438,6 +462,28 @@ def main():
         dist.barrier(group=gloo)
         dist.destroy_process_group()
     return 0
+
+
+def measure_pcie(torch):
+    """Host-tier roofline: this box's pinned copy bandwidth, measured here (best of 5, 1 GiB each way);
+    the host relay's dominant direction decides (receive = D2H, pull = H2D), so report the max."""
+    n = 1 << 30
+    h = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(n, dtype=torch.uint8, device="cuda")
+    best = {}
+    for name, (dst, src) in {"h2d": (d, h), "d2h": (h, d)}.items():
+        t = []
+        for _ in range(5):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            dst.copy_(src, non_blocking=True)
+            b.record()
+            b.synchronize()
+            t.append(a.elapsed_time(b))
+        best[name] = n / (min(t) / 1e3) / 1e9
+    del h, d
+    return max(best.values()), "measured in this run: pinned cudaMemcpy 1 GiB, H2D %.1f / D2H %.1f GB/s" % (
+        best["h2d"], best["d2h"])
 
 
 def traffic_of(kernel, model, N, config):

@@ -92,9 +92,16 @@ typedef struct {
 
 /* A relay node ("one relay per rollout machine"): for each actor rank r, the CUDA
  * device that stores rank r's region of the bucket image in this node.  All entries equal = the
- * node holds the full image on one GPU; different entries = range-sharded over several GPUs. */
+ * node holds the full image on one GPU; different entries = range-sharded over several GPUs.
+ * host_memory = 1 (the paper's own relay tier: "relay workers … store the
+ * latest model weights in CPU memory"): the node's ring slots
+ * live in pinned, device-mapped host memory (shared between rank processes through a memfd) instead
+ * of HBM; part_device[r] is then the GPU whose SMs receive rank r's region into it over PCIe and
+ * whose pulls read it from there.  Chunk headers, flags and counters stay in that GPU's HBM.  Zero
+ * extra GPU memory; bandwidth is PCIe's.  Node 0 (the actor's slots) is always HBM. */
 typedef struct {
   int32_t part_device[LAM_MAX_RANKS];
+  int32_t host_memory;
 } lam_node_desc;
 
 /* A rollout: the node it pulls from (0 = the master/publish node) and the GPU its pull runs on. */
@@ -190,6 +197,9 @@ typedef struct {
 } lam_stats;
 
 /* ---- lifecycle ------------------------------------------------------------------------- */
+/* sizeof(lam_config) as this library was compiled: bindings compare it with their own struct
+ * layout before the first call (a stale build fails loudly instead of misreading the config). */
+size_t lam_config_size(void);
 /* Validates cfg, builds the image plan, allocates this process's ring slots (S per node part on
  * its devices, zero-filled) and the control block.  n_procs > 1: rank 0 creates the shm block
  * `shm_name`, the others attach (waiting up to 60 s); then exchange handles with lam_export_ipc /
@@ -282,8 +292,9 @@ lam_status lam_read_headers(lam_ctx*, int32_t node, uint64_t version, lam_chunk_
 lam_status lam_set_profiling(lam_ctx*, int32_t on);
 lam_status lam_kernel_times(lam_ctx*, double ms_out[3], uint64_t count_out[3]);
 
-/* Bytes a pull of `layout` at rollout `rollout_id` reads from the rollout's own GPU (local) and from
- * other GPUs over NVLink (remote); builds/caches the copy plan.  For roofline accounting. */
+/* Bytes a pull of `layout` at rollout `rollout_id` reads from the rollout's own GPU's HBM (local) and
+ * from elsewhere (remote: other GPUs over NVLink, or a host-memory relay node over PCIe); builds/caches
+ * the copy plan.  For roofline accounting. */
 lam_status lam_pull_bytes(lam_ctx*, int32_t rollout_id, const lam_tp_layout* layout, uint64_t* local_bytes,
                           uint64_t* remote_bytes);
 

@@ -50,6 +50,13 @@ struct Part {
   bool local = false;
   uint8_t* base = nullptr;           // valid in this process (own allocation or IPC mapping)
   bool ipc_opened = false;
+  uint8_t* data = nullptr;           // slot 0's data (HBM: base; host tier: pinned host mapping)
+  uint8_t* meta = nullptr;           // slot 0's metadata block (always HBM of `device`)
+  // host-memory tier (lam_node_desc.host_memory, NEXT-3): slot data in a memfd mapping
+  bool host = false;
+  int host_fd = -1;                  // memfd (owner) or /proc/<pid>/fd reopen (other processes)
+  size_t host_bytes = 0;
+  bool host_registered = false;
   // local-only
   cudaStream_t stream = nullptr;
   cudaEvent_t done_ev[LAM_MAX_SLOTS] = {};
@@ -218,7 +225,7 @@ void prof_end(lam_ctx* c, int kind, int dev, cudaStream_t st, cudaEvent_t a) {
 }
 
 ChunkMeta meta_of(const lam_ctx* c, const Part& p, int slot) {
-  uint8_t* m = p.base + p.meta_base + (uint64_t)slot * p.meta_stride;
+  uint8_t* m = p.meta + (uint64_t)slot * p.meta_stride;
   ChunkMeta cm;
   cm.flags = reinterpret_cast<uint64_t*>(m + c->sm.flags);
   cm.hdr = reinterpret_cast<lam_chunk_header*>(m + c->sm.hdr);
@@ -228,7 +235,30 @@ ChunkMeta meta_of(const lam_ctx* c, const Part& p, int slot) {
   return cm;
 }
 
-uint8_t* slot_data(const Part& p, int slot) { return p.base + (uint64_t)slot * p.slot_stride; }
+uint8_t* slot_data(const Part& p, int slot) { return p.data + (uint64_t)slot * p.slot_stride; }
+
+// Host-memory tier: map `bytes` of the memfd `fd` and pin it for every device (mapped, portable).
+lam_status map_host_part(Part& p, int fd, size_t bytes) {
+  void* h = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+  if (h == MAP_FAILED) {
+    fprintf(stderr, "liblam: mmap of the host relay part (%.2f GB) failed: %s\n", bytes / 1e9, strerror(errno));
+    return LAM_ENOMEM;
+  }
+  p.host_fd = fd;
+  p.host_bytes = bytes;
+  cudaError_t e = cudaHostRegister(h, bytes, cudaHostRegisterMapped | cudaHostRegisterPortable);
+  if (e != cudaSuccess) {
+    fprintf(stderr, "liblam: cudaHostRegister(%.2f GB) failed: %s\n", bytes / 1e9, cudaGetErrorString(e));
+    munmap(h, bytes);
+    return LAM_ENOMEM;
+  }
+  p.host_registered = true;
+  void* d = nullptr;
+  if (cudaHostGetDevicePointer(&d, h, 0) != cudaSuccess) return LAM_ECUDA;
+  p.data = (uint8_t*)d;
+  p.base = (uint8_t*)h;   // host address (munmap / unregister)
+  return LAM_OK;
+}
 
 lam_status validate(const lam_config& c, std::string* why) {
   auto bad = [&](const std::string& s) { *why = s; return LAM_EINVAL; };
@@ -288,6 +318,7 @@ lam_status alloc_parts(lam_ctx* c) {
         p.pos = (int)c->node_parts[node].size();
         p.rank_off.assign(N, -1);
         p.local = owns(c, d);
+        p.host = node > 0 && c->cfg.relay[node - 1].host_memory != 0;
         by_dev[d] = p.index;
         c->node_parts[node].push_back(p.index);
         c->parts.push_back(p);
@@ -307,11 +338,28 @@ lam_status alloc_parts(lam_ctx* c) {
     p.alloc_bytes = p.meta_base + p.meta_stride * S;
     if (!p.local) continue;
     CK(cudaSetDevice(p.device));
-    if (cudaMalloc(&p.base, p.alloc_bytes) != cudaSuccess) {
-      fprintf(stderr, "liblam: cudaMalloc(%.2f GB) failed on device %d\n", p.alloc_bytes / 1e9, p.device);
-      return LAM_ENOMEM;
+    if (p.host) {
+      // slot data in pinned host memory (zero-filled by the kernel), metadata in HBM
+      const size_t hb = (size_t)p.slot_stride * S;
+      int fd = (int)memfd_create("lam_host_relay", 0);
+      if (fd < 0 || ftruncate(fd, (off_t)hb) != 0) {
+        fprintf(stderr, "liblam: memfd for the host relay part (%.2f GB) failed: %s\n", hb / 1e9, strerror(errno));
+        if (fd >= 0) close(fd);
+        return LAM_ENOMEM;
+      }
+      lam_status hs = map_host_part(p, fd, hb);
+      if (hs != LAM_OK) return hs;
+      if (cudaMalloc(&p.meta, (size_t)p.meta_stride * S) != cudaSuccess) return LAM_ENOMEM;
+      CK(cudaMemset(p.meta, 0, (size_t)p.meta_stride * S));
+    } else {
+      if (cudaMalloc(&p.base, p.alloc_bytes) != cudaSuccess) {
+        fprintf(stderr, "liblam: cudaMalloc(%.2f GB) failed on device %d\n", p.alloc_bytes / 1e9, p.device);
+        return LAM_ENOMEM;
+      }
+      CK(cudaMemset(p.base, 0, p.alloc_bytes));
+      p.data = p.base;
+      p.meta = p.base + p.meta_base;
     }
-    CK(cudaMemset(p.base, 0, p.alloc_bytes));
     int lo = 0, hi = 0;
     CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     CK(cudaStreamCreateWithPriority(&p.stream, cudaStreamNonBlocking, lo));  // lowest priority: SM-light
@@ -383,7 +431,7 @@ lam_status connect_links(lam_ctx* c) {
       }
   }
   for (auto& p : c->parts)
-    if (!p.base) {
+    if (!p.data || !p.meta) {
       fprintf(stderr, "liblam: part of node %d on device %d not mapped (missing lam_import_ipc?)\n", p.node, p.device);
       return LAM_EIPC;
     }
@@ -486,7 +534,7 @@ lam_status ce_topup(lam_ctx* c, Part& p) {
     uint8_t* dst = slot_data(p, s) + p.rank_off[r] + off;
     lam_status st = stream_wait_flag(c, p.stream, qm.flags + g, u);
     if (st != LAM_OK) return st;
-    CK(cudaMemcpyAsync(dst, src, len, cudaMemcpyDeviceToDevice, p.stream));
+    CK(cudaMemcpyAsync(dst, src, len, cudaMemcpyDefault, p.stream));
     CK(cudaEventRecord(p.chunk_ev[i], p.stream));
     CK(cudaStreamWaitEvent(p.vstream, p.chunk_ev[i], 0));
     if (launch_verify(dst, g, len, qm.flags, qm.hdr, m, u, p.err_dev + s, p.d_my_chunks, i, n, 32, p.vstream))
@@ -870,7 +918,8 @@ lam_status get_plan(lam_ctx* c, const lam_rollout_desc& ro, const lam_tp_layout&
     pp.kinds |= t.transposed() ? kPullKMajor : kPullRowMajor;
     if (t.zero()) continue;   // padding rows: written, nothing read
     const Part& q = c->parts[c->node_rank_part[ro.node][t.src_rank]];
-    (q.device == ro.device ? pp.local_bytes : pp.remote_bytes) += (uint64_t)t.rows * t.row_bytes;
+    // local = this GPU's HBM; remote = a peer's HBM over NVLink, or the host tier over PCIe
+    (q.device == ro.device && !q.host ? pp.local_bytes : pp.remote_bytes) += (uint64_t)t.rows * t.row_bytes;
   }
   CK(cudaMalloc(&pp.d_tiles, sizeof(CopyTile) * std::max<size_t>(tiles.size(), 1)));
   if (!tiles.empty()) CK(cudaMemcpy(pp.d_tiles, tiles.data(), sizeof(CopyTile) * tiles.size(), cudaMemcpyHostToDevice));
@@ -894,6 +943,8 @@ std::string layout_key(int node, const lam_tp_layout& L) {
 }  // namespace
 
 // ===================================================================================== C ABI
+extern "C" size_t lam_config_size(void) { return sizeof(lam_config); }
+
 extern "C" const char* lam_strerror(lam_status s) {
   switch (s) {
     case LAM_OK: return "ok";
@@ -994,7 +1045,9 @@ extern "C" lam_status lam_init(const lam_config* cfg, lam_ctx** out) {
 
 struct IpcEntry {
   int32_t part, device;
-  cudaIpcMemHandle_t h;
+  cudaIpcMemHandle_t h;          // HBM part: the whole allocation; host part: the metadata block
+  int32_t host, pid, fd, _pad;   // host part: memfd of the slot data, reopened via /proc/<pid>/fd/<fd>
+  uint64_t host_bytes;
 };
 
 extern "C" lam_status lam_export_ipc(lam_ctx* c, void* buf, size_t cap, size_t* len) {
@@ -1002,9 +1055,9 @@ extern "C" lam_status lam_export_ipc(lam_ctx* c, void* buf, size_t cap, size_t* 
   std::vector<IpcEntry> v;
   for (Part& p : c->parts)
     if (p.local) {
-      IpcEntry e{p.index, p.device, {}};
+      IpcEntry e{p.index, p.device, {}, p.host ? 1 : 0, (int32_t)getpid(), p.host_fd, 0, p.host_bytes};
       cudaSetDevice(p.device);
-      CK(cudaIpcGetMemHandle(&e.h, p.base));
+      CK(cudaIpcGetMemHandle(&e.h, p.host ? p.meta : p.base));
       v.push_back(e);
     }
   size_t need = sizeof(int32_t) + v.size() * sizeof(IpcEntry);
@@ -1032,15 +1085,30 @@ extern "C" lam_status lam_import_ipc(lam_ctx* c, int32_t proc, const void* buf, 
     memcpy(&e, (const char*)buf + sizeof n + (size_t)i * sizeof(IpcEntry), sizeof e);
     if (e.part < 0 || e.part >= (int)c->parts.size()) return LAM_EINVAL;
     Part& p = c->parts[e.part];
-    if (p.local || p.base) continue;
+    if (p.local || p.meta) continue;
     void* ptr = nullptr;
     cudaError_t err = cudaIpcOpenMemHandle(&ptr, e.h, cudaIpcMemLazyEnablePeerAccess);
     if (err != cudaSuccess) {
       fprintf(stderr, "liblam: cudaIpcOpenMemHandle(part %d, dev %d): %s\n", e.part, e.device, cudaGetErrorString(err));
       return LAM_EIPC;
     }
-    p.base = (uint8_t*)ptr;
     p.ipc_opened = true;
+    if (e.host) {
+      p.meta = (uint8_t*)ptr;
+      char path[64];
+      snprintf(path, sizeof path, "/proc/%d/fd/%d", e.pid, e.fd);
+      int fd = open(path, O_RDWR);
+      if (fd < 0) {
+        fprintf(stderr, "liblam: open(%s) for the host relay part failed: %s\n", path, strerror(errno));
+        return LAM_EIPC;
+      }
+      lam_status hs = map_host_part(p, fd, e.host_bytes);
+      if (hs != LAM_OK) return hs;
+    } else {
+      p.base = (uint8_t*)ptr;
+      p.data = p.base;
+      p.meta = p.base + p.meta_base;
+    }
   }
   return LAM_OK;
 }
@@ -1440,7 +1508,7 @@ extern "C" lam_status lam_debug_region(lam_ctx* c, int32_t node, uint64_t v, int
   if (s < 0) s = find_slot(n, c->S, v, S_FILLING);
   if (s < 0) return LAM_ENOVERSION;
   const Part& p = c->parts[c->node_rank_part[node][rank]];
-  if (!p.base) return LAM_EINVAL;
+  if (!p.data) return LAM_EINVAL;
   *ptr = slot_data(p, s) + p.rank_off[rank];
   return LAM_OK;
 }
@@ -1448,7 +1516,7 @@ extern "C" lam_status lam_debug_region(lam_ctx* c, int32_t node, uint64_t v, int
 extern "C" void lam_destroy(lam_ctx* c) {
   if (!c) return;
   for (Part& p : c->parts) {
-    if (p.local && p.base) {
+    if (p.local && p.meta) {
       cudaSetDevice(p.device);
       cudaDeviceSynchronize();
     }
@@ -1475,7 +1543,16 @@ extern "C" void lam_destroy(lam_ctx* c) {
       if (rp.ev[s]) cudaEventDestroy(rp.ev[s]);
   }
   for (Part& p : c->parts) {
-    if (p.ipc_opened && p.base) cudaIpcCloseMemHandle(p.base);
+    if (p.host) {
+      if (p.host_registered) cudaHostUnregister(p.base);
+      if (p.base) munmap(p.base, p.host_bytes);
+      if (p.host_fd >= 0) close(p.host_fd);
+      if (p.ipc_opened) cudaIpcCloseMemHandle(p.meta);
+      else if (p.local && p.meta) { cudaSetDevice(p.device); cudaFree(p.meta); }
+      p.base = nullptr;
+    } else if (p.ipc_opened && p.base) {
+      cudaIpcCloseMemHandle(p.base);
+    }
     if (!p.local) continue;
     cudaSetDevice(p.device);
     if (p.d_tiles) cudaFree(p.d_tiles);

@@ -31,7 +31,7 @@ class lam_model_dims(C.Structure):
 
 
 class lam_node_desc(C.Structure):
-    _fields_ = [("part_device", C.c_int32 * LAM_MAX_RANKS)]
+    _fields_ = [("part_device", C.c_int32 * LAM_MAX_RANKS), ("host_memory", C.c_int32)]
 
 
 class lam_rollout_desc(C.Structure):
@@ -142,11 +142,15 @@ def load() -> C.CDLL:
     for name, (res, args) in sig.items():
         f = getattr(L, name)
         f.restype, f.argtypes = res, args
+    L.lam_config_size.restype, L.lam_config_size.argtypes = C.c_size_t, []
+    if L.lam_config_size() != C.sizeof(lam_config):
+        raise RuntimeError(f"{LIB_PATH} was built for sizeof(lam_config) = {L.lam_config_size()}, the binding has "
+                           f"{C.sizeof(lam_config)}: stale build, run __graft_entry__.build()")
     _LIB = L
     return L
 
 
-EXPORTED = ["lam_init", "lam_export_ipc", "lam_import_ipc", "lam_connect", "lam_destroy", "lam_strerror",
+EXPORTED = ["lam_config_size", "lam_init", "lam_export_ipc", "lam_import_ipc", "lam_connect", "lam_destroy", "lam_strerror",
             "lam_publish", "lam_relay_step", "lam_pull", "lam_latest", "lam_get_plan_info", "lam_get_stats",
             "lam_read_image", "lam_read_headers", "lam_debug_region", "lam_set_profiling", "lam_kernel_times", "lam_pull_bytes", "lam_model_n_tensors", "lam_model_tensor", "lam_vllm_layout",
             "lam_plan_segments", "lam_plan_copy_tiles", "lam_optimal_chunks", "lam_chain_latency"]
@@ -243,6 +247,7 @@ class Config:
     spin_timeout_s: float = 0.0
     hop_mode: int = LAM_HOP_KERNEL
     heartbeat_timeout_s: float = 0.0
+    host_relays: list[int] = field(default_factory=list)     # relay nodes (1-based) kept in host memory
 
     def to_c(self) -> lam_config:
         c = lam_config()
@@ -254,6 +259,7 @@ class Config:
         for i, node in enumerate(self.relays):
             for r, d in enumerate(node):
                 c.relay[i].part_device[r] = d
+            c.relay[i].host_memory = int(i + 1 in self.host_relays)
         c.chunk_bytes, c.t_start_s, c.t_byte_s = self.chunk_bytes, self.t_start_s, self.t_byte_s
         c.n_rollouts = len(self.rollouts)
         for i, (node, dev) in enumerate(self.rollouts):

@@ -52,7 +52,7 @@ def main():
                      rollouts=[(n, d) for n, d, _, _ in ro], chunk_bytes=a.chunk_kb << 10, proc_rank=rank,
                      n_procs=N, proc_of_device={d: d for d in range(N)},
                      shm_name=f"lam_mp_{os.environ.get('MASTER_PORT', '0')}_{os.getppid()}", spin_timeout_s=60,
-                     hop_mode=a.hop_mode)
+                     hop_mode=a.hop_mode, host_relays=T.get("host_relays", []))
     ctx = lam.Context(cfg)
     blobs = [None] * N
     dist.all_gather_object(blobs, ctx.export_ipc())

@@ -39,6 +39,9 @@ CASES = [  # (min GPUs, args)
     (4, ["--config", "colocated", "--model", "tiny", "--tp", "4", "--stream"]),
     (4, ["--config", "relay-tp", "--model", "tiny", "--tp", "2", "--stream"]),
     (2, ["--config", "chain", "--model", "7b", "--chunk-kb", str(128 << 10), "--stream"]),
+    (2, ["--config", "host", "--model", "tiny", "--versions", "3"]),                 # NEXT-3 host tier
+    (4, ["--config", "host", "--model", "tiny", "--tp", "2", "--stream"]),
+    (4, ["--config", "host", "--model", "tiny", "--versions", "2", "--hop-mode", "1"]),
 ]
 
 

@@ -184,6 +184,50 @@ def test_tiny_three_versions_chain_on_one_gpu(hop_mode):
 
 
 @pytest.mark.parametrize("hop_mode", HOP_MODES)
+def test_tiny_host_memory_relay_tier(hop_mode):
+    """NEXT-3: relay node 1 keeps its ring in pinned host memory (received by
+    GPU 0's SMs or copy engines over PCIe), node 2 (HBM) is fed from it — its hop reads host memory —
+    and rollouts pull from both; two versions, everything compared in full with the oracle."""
+    od = OMODELS["tiny"]
+    C = 16 * 4096
+    ctx = make_ctx("tiny", 1, [0], [[0], [0]], [(1, 0), (2, 0)], C=C, hop_mode=hop_mode, host_relays=[1])
+    shard = ActorShard(MODELS["tiny"], 1, 0, 0)
+    plan = image_plan([s for _, s in otensors(od)], 1, C)
+    for v in (1, 2):
+        publish_all(ctx, [shard], v, True)
+        until_idle(ctx)
+        oimg, ohdr = publish(plan, SEED, v, specials=True)
+        for node in (0, 1, 2):
+            assert ctx.latest(node) == v
+            check_image(ctx, node, v, oimg, ohdr, C)
+        for r in range(2):
+            check_pull(ctx, 0, 2, r, 0, v, True, od)            # TP=2 reshard straight from host memory
+        check_pull(ctx, 1, 1, 0, 0, v, True, od)
+    assert ctx.pull_bytes(0, RolloutBuffers(MODELS["tiny"], 1, 0, 0).tp)[0] == 0  # nothing from local HBM
+    ctx.close()
+
+
+def test_tiny_host_relay_read_by_other_gpus():
+    """Host tier across devices: GPU 1 receives node 1 into host memory; GPU 0 pulls from it (portable
+    registration) and node 2 on GPU 0 chains from it."""
+    if ngpu() < 2:
+        pytest.skip("needs >= 2 GPUs")
+    od = OMODELS["tiny"]
+    C = 8 * 4096
+    ctx = make_ctx("tiny", 1, [0], [[1], [0]], [(1, 0), (2, 1)], C=C, host_relays=[1])
+    shard = ActorShard(MODELS["tiny"], 1, 0, 0)
+    plan = image_plan([s for _, s in otensors(od)], 1, C)
+    publish_all(ctx, [shard], 1, True)
+    until_idle(ctx)
+    oimg, ohdr = publish(plan, SEED, 1, specials=True)
+    for node in (1, 2):
+        check_image(ctx, node, 1, oimg, ohdr, C)
+    check_pull(ctx, 0, 1, 0, 0, 1, True, od)
+    check_pull(ctx, 1, 2, 1, 1, 1, True, od)
+    ctx.close()
+
+
+@pytest.mark.parametrize("hop_mode", HOP_MODES)
 def test_tiny_chain_across_gpus(hop_mode):
     n = ngpu()
     if n < 2:
