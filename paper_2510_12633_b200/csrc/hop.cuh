@@ -4,27 +4,37 @@
 //
 // Receiver-driven.  The NVLink pull is the latency-bound part, so it goes to TMA (bulk copies reach
 // ~785 GB/s with 32 CTAs where 16-B peer loads need ~148 — tools/p2p_bench.cu); the local part is
-// done by the threads that read the stage anyway:
-//   producer (thread 0): before the first sub-block of a new chunk, check the predecessor's chunk
-//     flag (ld.acquire.sys over NVLink); cp.async.bulk peer global -> smem stage, completion on an
-//     mbarrier (expect_tx).  Refills are non-blocking, so the chunk in hand is never held behind the
-//     wait for the next one; only an empty pipeline makes it spin.
-//   all 512 threads, per 32 KiB stage: 16-B shared loads -> streaming 16-B stores to local HBM +
-//     checksum (S1, S2); one __syncthreads, after which the stage is refilled immediately.
-//   A CTA folds its share of a chunk into the chunk header once, after its last tile of that chunk
-//     (fence, 3 atomics); the CTA completing the chunk compares with the predecessor's header and
-//     releases the flag (st.release.sys) — or poisons it on mismatch so the successor aborts too
-//     (SPEC L643).
-// Cycle accounting of the previous design (128 threads, TMA store per stage; LAM_HOP_PROF): thread 0
-// spent only 11-23 % waiting for data and ~80 % in the checksum pass and in waiting for its store to
-// release the stage.
+// done by the threads that read the stage anyway.  Warp-specialised (v4):
+//   producer warp (lane 0): walks the CTA's tiles; before the first sub-block of a new chunk, checks
+//     the predecessor's chunk flag (ld.acquire.sys over NVLink); waits for the stage to be empty
+//     (mbarrier, one arrival per consumer warp) and issues cp.async.bulk peer global -> smem with
+//     completion on the stage's full mbarrier (expect_tx).  It runs up to kHopStages ahead and never
+//     waits on the consumers' per-stage work.
+//   16 consumer warps, per 32 KiB stage: wait full -> 16-B shared loads -> streaming 16-B stores to
+//     local HBM (or a host-memory relay) + checksum (S1, S2) -> __syncwarp, lane 0 arrives on empty.
+//     No CTA-wide barrier per stage: v3 (one __syncthreads per stage, thread 0 both producer and
+//     consumer) left thread 0 ~50 % in the copy, ~21 % in dependent tile/link loads of the refill and
+//     only 11-16 % waiting for data (LAM_HOP_PROF, chain N=4), i.e. the refill latency sat on every
+//     stage's critical path.
+//   flusher warp (lane 0): a CTA folds its share of a chunk into the chunk header once, after its
+//     last tile of that chunk: each consumer warp fences its stores, reduces its sums by shuffles and
+//     lane 0 deposits them (double-buffered) and arrives on the chunk's flush mbarrier; the flusher
+//     sums the 16 partials and does the 3 atomics; the CTA completing the chunk compares with the
+//     predecessor's header and releases the flag (st.release.sys) — or poisons it on mismatch so the
+//     successor aborts too.  v4 did this on consumer thread 0 between two CTA-wide
+//     named barriers: ~10 % of the consumers' time (remote header loads, system fences).
+//   Failure (predecessor poisoned, abort, timeout): the producer records the job index it stopped
+//     at and arrives (without bytes) on that stage's full barrier; consumers finish every earlier
+//     stage (all of them real, in-flight TMA) and stop there, so no copy is left landing in smem.
 
-// Optional per-CTA cycle accounting of thread 0 (LAM_HOP_PROF=1; diagnostics only):
-// [0] data wait, [1] copy + checksum, [2] barrier, [3] chunk flush, [4] refill, [5] empty-pipeline spin, [6] total
+// Optional per-CTA cycle accounting (LAM_HOP_PROF=1; diagnostics only):
+// [0] consumer data wait, [1] consumer copy + checksum, [2] producer empty-stage wait, [3] chunk
+// flush, [4] producer issue (tile/link loads + TMA), [5] producer flag spin, [6] consumer total
 __device__ unsigned long long* g_hop_prof = nullptr;
 
-constexpr int kHopThreads = 512;
-constexpr int kHopStages = 6;
+constexpr int kHopConsumers = 512;                 // 16 consumer warps
+constexpr int kHopThreads = kHopConsumers + 64;    // + producer warp + flusher warp
+constexpr int kHopStages = 7;                      // 7 x 32 KiB = 224 KiB of the 227 KiB
 constexpr uint32_t kHopSub = 32768;  // bytes per pipeline stage
 constexpr size_t kHopSmem = (size_t)kHopStages * kHopSub;
 
@@ -97,60 +107,118 @@ __global__ void __launch_bounds__(kHopThreads, 1)
     k_hop(const HopTile* __restrict__ tiles, uint32_t n_tiles, const RankLink* __restrict__ links, ChunkMeta meta,
           const uint32_t* __restrict__ tiles_per_chunk, uint64_t version, uint32_t* err_word, uint64_t timeout_ns) {
   extern __shared__ __align__(1024) uint8_t stage_buf[];
-  __shared__ __align__(8) uint64_t bar[kHopStages];
-  __shared__ uint64_t red[2][kHopThreads / 32];
-  __shared__ int s_status;
-  __shared__ uint32_t s_fail_chunk;
+  __shared__ __align__(8) uint64_t full[kHopStages], empty[kHopStages];
+  __shared__ __align__(8) uint64_t fl_full[2], fl_free[2];   // flush hand-off, double-buffered
+  __shared__ uint64_t red[2][2][kHopConsumers / 32];         // [buffer][s1|s2][consumer warp]
+  __shared__ uint32_t s_fail_job;
+  __shared__ int s_consumers_failed;
 
   const uint32_t my_tiles = blockIdx.x < n_tiles ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  uint32_t total = 0;  // jobs of this CTA (every thread knows the job list)
-  for (uint32_t m = 0; m < my_tiles; ++m) total += (tiles[blockIdx.x + m * gridDim.x].bytes + kHopSub - 1) / kHopSub;
-
-  // producer cursor (thread 0 only)
-  uint32_t p_tile = 0, p_sub = 0, waited = 0xFFFFFFFFu, issued = 0;
-  const uint64_t deadline = globaltimer() + timeout_ns;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned long long* prof = g_hop_prof;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kHopStages; ++s) mbar_init(&bar[s], 1);
+    for (int s = 0; s < kHopStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kHopConsumers / 32);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&fl_full[b], kHopConsumers / 32);
+      mbar_init(&fl_free[b], 1);
+    }
+    s_consumers_failed = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    s_status = kHopOk;
+    s_fail_job = 0xFFFFFFFFu;
   }
   __syncthreads();
 
-  // thread 0: issue the next job if its chunk is available; block=true spins until it is.
-  auto try_issue = [&](bool block) -> bool {
-    if (issued >= total || s_status != kHopOk) return false;
-    const HopTile T = tiles[blockIdx.x + p_tile * gridDim.x];
-    const RankLink& L = links[T.rank];
-    if (T.chunk != waited) {
-      for (uint32_t spin = 0;; ++spin) {
-        const uint64_t f = ld_acquire_sys(L.src_flags + T.chunk);
-        if (f == version) break;
-        if (f == (version | kPoison)) { s_fail_chunk = T.chunk; s_status = kHopPoison; return false; }
-        if (!block) return false;
-        if (*(volatile int32_t*)meta.abort_flag) { s_fail_chunk = T.chunk; s_status = kHopAbort; return false; }
-        if ((spin & 63) == 63 && globaltimer() > deadline) { s_fail_chunk = T.chunk; s_status = kHopTimeout; return false; }
-        __nanosleep(spin < 64 ? 100 : 1000);
+  if (warp == kHopConsumers / 32) {
+    // ------------------------------------------------------------------ producer (one lane)
+    if (lane != 0) return;
+    unsigned long long pc[3] = {}, t_a = clock64(), t_b;
+    const uint64_t deadline = globaltimer() + timeout_ns;
+    uint32_t job = 0, waited = 0xFFFFFFFFu, fail_chunk = 0;
+    int status = kHopOk;
+    for (uint32_t m = 0; m < my_tiles && status == kHopOk; ++m) {
+      const HopTile T = tiles[blockIdx.x + m * gridDim.x];
+      const uint8_t* src = links[T.rank].src + T.region_off;
+      if (T.chunk != waited) {
+        const uint64_t* flag = links[T.rank].src_flags + T.chunk;
+        if (prof) { t_b = clock64(); pc[1] += t_b - t_a; t_a = t_b; }
+        for (uint32_t spin = 0;; ++spin) {
+          const uint64_t f = ld_acquire_sys(flag);
+          if (f == version) break;
+          if (f == (version | kPoison)) { status = kHopPoison; break; }
+          if (*(volatile int32_t*)meta.abort_flag) { status = kHopAbort; break; }
+          if ((spin & 63) == 63 && globaltimer() > deadline) { status = kHopTimeout; break; }
+          __nanosleep(spin < 64 ? 100 : 1000);
+        }
+        if (prof) { t_b = clock64(); pc[2] += t_b - t_a; t_a = t_b; }
+        if (status != kHopOk) { fail_chunk = T.chunk; break; }
+        waited = T.chunk;
       }
-      waited = T.chunk;
+      for (uint32_t off = 0; off < T.bytes; off += kHopSub, ++job) {
+        const uint32_t st = job % kHopStages;
+        if (job >= (uint32_t)kHopStages) {
+          if (prof) { t_b = clock64(); pc[1] += t_b - t_a; t_a = t_b; }
+          mbar_wait(&empty[st], ((job / kHopStages) + 1) & 1u);
+          if (prof) { t_b = clock64(); pc[0] += t_b - t_a; t_a = t_b; }
+        }
+        const uint32_t bytes = min(kHopSub, T.bytes - off);
+        mbar_expect_tx(&full[st], bytes);
+        bulk_g2s(stage_buf + (size_t)st * kHopSub, src + off, bytes, &full[st]);
+      }
     }
-    const uint32_t st = issued % kHopStages;
-    const uint32_t off = p_sub * kHopSub;
-    const uint32_t bytes = min(kHopSub, T.bytes - off);
-    mbar_expect_tx(&bar[st], bytes);
-    bulk_g2s(stage_buf + (size_t)st * kHopSub, L.src + T.region_off + off, bytes, &bar[st]);
-    if (off + bytes >= T.bytes) { p_sub = 0; ++p_tile; } else { ++p_sub; }
-    ++issued;
-    return true;
-  };
-
-  if (threadIdx.x == 0 && total > 0) {
-    try_issue(true);
-    while (issued < kHopStages && try_issue(false)) {}
+    if (status != kHopOk) {
+      // release the consumers at the stage this job would have used; every earlier stage is a real
+      // copy they will wait for, so nothing is still landing in shared memory when they stop
+      const uint32_t st = job % kHopStages;
+      if (job >= (uint32_t)kHopStages) mbar_wait(&empty[st], ((job / kHopStages) + 1) & 1u);
+      *(volatile uint32_t*)&s_fail_job = job;
+      mbar_arrive(&full[st]);
+      // abort flag 2 = superseded by a chain rebuild (the runtime restarts the fill): exit quietly,
+      // keep the verified chunks and do not poison the successor
+      if (!(status == kHopAbort && *(volatile int32_t*)meta.abort_flag == 2))
+        hop_fail(meta, err_word, fail_chunk, version, status == kHopTimeout ? kHopTimeout : kHopPoison);
+    }
+    if (prof) {
+      t_b = clock64();
+      pc[1] += t_b - t_a;
+      atomicAdd(prof + 2, pc[0]);
+      atomicAdd(prof + 4, pc[1]);
+      atomicAdd(prof + 5, pc[2]);
+    }
+    return;
   }
 
-  unsigned long long* prof = g_hop_prof;
-  unsigned long long pc[7] = {}, t_a = clock64(), t_b;
+  if (warp == kHopConsumers / 32 + 1) {
+    // ------------------------------------------------------------------- flusher (one lane)
+    if (lane != 0) return;
+    unsigned long long t_f = 0, t0;
+    uint32_t q = 0, n_in_chunk = 0;
+    for (uint32_t m = 0; m < my_tiles; ++m) {
+      const HopTile T = tiles[blockIdx.x + m * gridDim.x];
+      ++n_in_chunk;
+      if (!(m + 1 >= my_tiles || tiles[blockIdx.x + (m + 1) * gridDim.x].chunk != T.chunk)) continue;
+      const uint32_t b = q & 1u;
+      mbar_wait(&fl_full[b], (q >> 1) & 1u);
+      if (*(volatile int*)&s_consumers_failed) break;
+      t0 = prof ? clock64() : 0;
+      uint64_t a = 0, c = 0;
+#pragma unroll
+      for (int i = 0; i < kHopConsumers / 32; ++i) { a += red[b][0][i]; c += red[b][1][i]; }
+      mbar_arrive(&fl_free[b]);
+      hop_flush(meta, links[T.rank], tiles_per_chunk, T.chunk, n_in_chunk, a, c, version, err_word);
+      if (prof) t_f += clock64() - t0;
+      n_in_chunk = 0;
+      ++q;
+    }
+    if (prof) atomicAdd(prof + 3, t_f);
+    return;
+  }
+
+  // -------------------------------------------------------------------- consumers (16 warps)
+  unsigned long long pc[3] = {}, t_a = clock64(), t_b;
   const unsigned long long t_start = t_a;
 #define HOP_LAP(i)                            \
   if (prof && threadIdx.x == 0) {             \
@@ -158,73 +226,63 @@ __global__ void __launch_bounds__(kHopThreads, 1)
     pc[i] += t_b - t_a;                       \
     t_a = t_b;                                \
   }
-  // consumer cursor (all threads); per-chunk accumulation of this CTA's checksum share
-  uint32_t c_tile = 0, c_sub = 0, phases = 0, k = 0, n_in_chunk = 0;
+  uint32_t job = 0, q = 0;   // q: this CTA's chunk-end count (flush buffer q & 1)
   uint64_t s1 = 0, s2 = 0;
-  for (; k < total; ++k) {
-    const uint32_t st = k % kHopStages;
-    if (threadIdx.x == 0 && issued <= k) {        // pipeline empty: wait for the predecessor
-      if (!try_issue(true)) mbar_arrive(&bar[st]);  // failure: release the waiters, exit below
-    }
-    HOP_LAP(5)
-    mbar_wait(&bar[st], (phases >> st) & 1u);
-    phases ^= 1u << st;
-    HOP_LAP(0)
-    const HopTile T = tiles[blockIdx.x + c_tile * gridDim.x];
-    const uint32_t off = c_sub * kHopSub;
-    const uint32_t bytes = min(kHopSub, T.bytes - off);
-    const uint8_t* sb = stage_buf + (size_t)st * kHopSub;
-    const RankLink& L = links[T.rank];
-    uint8_t* dst = L.dst + T.region_off + off;
-    const uint64_t w0 = (uint64_t)T.word0 + off / 4;
-    if (s_status == kHopOk) {                      // (on failure the stage holds nothing valid)
-      for (uint32_t v = threadIdx.x; v < bytes / 16; v += kHopThreads) {
+  bool failed = false;
+  for (uint32_t m = 0; m < my_tiles && !failed; ++m) {
+    const HopTile T = tiles[blockIdx.x + m * gridDim.x];
+    uint8_t* dst = links[T.rank].dst + T.region_off;
+    for (uint32_t off = 0; off < T.bytes; off += kHopSub, ++job) {
+      const uint32_t st = job % kHopStages;
+      mbar_wait(&full[st], (job / kHopStages) & 1u);
+      HOP_LAP(0)
+      if (*(volatile uint32_t*)&s_fail_job == job) { failed = true; break; }
+      const uint32_t bytes = min(kHopSub, T.bytes - off);
+      const uint8_t* sb = stage_buf + (size_t)st * kHopSub;
+      const uint64_t w0 = (uint64_t)T.word0 + off / 4;
+      for (uint32_t v = threadIdx.x; v < bytes / 16; v += kHopConsumers) {
         const uint4 w = lds128(sb + 16 * v);
-        st_v4(dst + 16 * (size_t)v, w);
+        st_v4(dst + off + 16 * (size_t)v, w);
         cks4(w0 + 4ull * v, w, s1, s2);
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+      HOP_LAP(1)
     }
-    HOP_LAP(1)
-    __syncthreads();                               // stage fully read; s_status uniform from here
-    HOP_LAP(2)
-    if (s_status != kHopOk) break;
-    if (threadIdx.x == 0)                          // refill: every stage but the ones in flight is free
-      while (issued < k + 1 + kHopStages && try_issue(false)) {}
-    HOP_LAP(4)
-    if (off + bytes >= T.bytes) {                  // tile end
-      ++n_in_chunk;
-      ++c_tile;
-      c_sub = 0;
-      const bool chunk_end = c_tile >= my_tiles || tiles[blockIdx.x + c_tile * gridDim.x].chunk != T.chunk;
-      if (chunk_end) {                             // this CTA's last tile of the chunk: flush its share
-        __threadfence_system();                    // this thread's stores before the header / flag
-        block_reduce2<kHopThreads>(s1, s2, red);
-        if (threadIdx.x == 0) hop_flush(meta, L, tiles_per_chunk, T.chunk, n_in_chunk, s1, s2, version, err_word);
-        __syncthreads();                           // red[] reuse
-        s1 = s2 = 0;
-        n_in_chunk = 0;
+    if (failed) break;
+    const bool chunk_end = m + 1 >= my_tiles || tiles[blockIdx.x + (m + 1) * gridDim.x].chunk != T.chunk;
+    if (chunk_end) {                               // this CTA's last tile of the chunk: hand its share over
+      __threadfence_system();                      // this thread's stores before the header / flag
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+        s2 += __shfl_xor_sync(0xffffffffu, s2, o);
       }
-      HOP_LAP(3)
-    } else {
-      ++c_sub;
+      if (lane == 0) {
+        const uint32_t b = q & 1u;
+        if (q >= 2) mbar_wait(&fl_free[b], ((q >> 1) + 1) & 1u);   // the flusher took chunk q-2's sums
+        red[b][0][warp] = s1;
+        red[b][1][warp] = s2;
+        mbar_arrive(&fl_full[b]);
+      }
+      ++q;
+      s1 = s2 = 0;
+      HOP_LAP(2)
     }
+  }
+  if (failed && lane == 0) {                       // wake the flusher at the chunk that never ended
+    if (threadIdx.x == 0) *(volatile int*)&s_consumers_failed = 1;   // before warp 0's arrival below
+    const uint32_t b = q & 1u;
+    if (q >= 2) mbar_wait(&fl_free[b], ((q >> 1) + 1) & 1u);
+    mbar_arrive(&fl_full[b]);
   }
   if (prof && threadIdx.x == 0) {
-    pc[6] = clock64() - t_start;
-    for (int i = 0; i < 7; ++i) atomicAdd(prof + i, pc[i]);
+    atomicAdd(prof + 0, pc[0]);
+    atomicAdd(prof + 1, pc[1]);
+    atomicAdd(prof + 3, pc[2]);
+    atomicAdd(prof + 6, clock64() - t_start);
   }
 #undef HOP_LAP
-  if (threadIdx.x == 0 && s_status != kHopOk) {
-    for (uint32_t j = k + 1; j < issued; ++j) {    // drain loads still landing in shared memory
-      const uint32_t st = j % kHopStages;
-      mbar_wait(&bar[st], (phases >> st) & 1u);
-      phases ^= 1u << st;
-    }
-    // abort flag 2 = superseded by a chain rebuild (runtime restarts the fill): exit quietly, keep
-    // the verified chunks and do not poison the successor
-    if (!(s_status == kHopAbort && *(volatile int32_t*)meta.abort_flag == 2))
-      hop_fail(meta, err_word, s_fail_chunk, version, s_status == kHopTimeout ? kHopTimeout : kHopPoison);
-  }
 }
 
 // LAM_HOP_PROF diagnostics: point g_hop_prof of the current device at a 7-counter buffer (or null).

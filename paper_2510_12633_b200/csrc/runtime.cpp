@@ -722,7 +722,9 @@ lam_status launch_hop_part(lam_ctx* c, Part& p, int s, bool* launched) {
       links = p.d_links_dyn;
     }
     int rc = launch_hop(tiles, n_tiles, links, m, p.d_tiles_per_chunk, u, p.err_dev + s, c->timeout_ns,
-                        c->hop_ctas, p.stream);
+                        // host-tier destination: PCIe stores need more CTAs in flight (v6 box run:
+                        // 32 CTAs 29 GB/s, 148 CTAs 47 GB/s but starved the concurrent pulls)
+                        p.host && c->cfg.hop_ctas <= 0 ? 96 : c->hop_ctas, p.stream);
     if (rc) {
       fprintf(stderr, "liblam: hop launch failed: %s\n", cudaGetErrorString((cudaError_t)rc));
       return LAM_ECUDA;
@@ -821,8 +823,8 @@ lam_status step_locked(lam_ctx* c, int* transitions, bool* busy) {
       if (p.prof_host) {
         const unsigned long long* q = p.prof_host;
         const double tot = (double)(q[6] ? q[6] : 1);
-        fprintf(stderr, "k_hop node %d dev %d: wait %.1f%% cks %.1f%% bar %.1f%% tile %.1f%% refill %.1f%% spin %.1f%% (%.2f Gcyc)\n",
-                p.node, p.device, 100 * q[0] / tot, 100 * q[1] / tot, 100 * q[2] / tot, 100 * q[3] / tot,
+        fprintf(stderr, "k_hop node %d dev %d: consumer wait %.1f%% copy+cks %.1f%% flush %.1f%% | producer empty-wait %.1f%% issue %.1f%% flag-spin %.1f%% (%.2f Gcyc)\n",
+                p.node, p.device, 100 * q[0] / tot, 100 * q[1] / tot, 100 * q[3] / tot, 100 * q[2] / tot,
                 100 * q[4] / tot, 100 * q[5] / tot, tot / 1e9);
         memset(p.prof_host, 0, 64);
       }
@@ -987,14 +989,15 @@ extern "C" lam_status lam_init(const lam_config* cfg, lam_ctx** out) {
   uint64_t C = cfg->chunk_bytes;
   if (C == 0) {
     double tb = cfg->t_byte_s > 0 ? cfg->t_byte_s : 1.0 / 750e9;
-    // T_start calibrated on B200 (bench --chunk-mb sweep at N=4: 64 MB 38.0 ms, 138 MB 34.2 ms,
-    // 256 MB 33.1 ms): per-chunk flag propagation + pipeline refill is ~20 us, not RDMA's ~5 us
-    double tsu = cfg->t_start_s > 0 ? cfg->t_start_s : 20e-6;
+    // T_start calibrated on B200: per-chunk flag propagation + pipeline refill.  k_hop v3 (bench
+    // --chunk-mb sweep at N=4: 64 MB 38.0 ms, 138 MB 34.2 ms, 256 MB 33.1 ms) implied ~20 us; with the
+    // flusher warp (v5) 128 MB beats 256 MB at N=4 (25.5 vs 25.9 ms): ~10 us
+    double tsu = cfg->t_start_s > 0 ? cfg->t_start_s : 10e-6;
     // the pack is one more pipeline stage ahead of the chain (reading R12)
     int64_t k = lam_optimal_chunks(c->n_nodes + 1, 2.0 * (double)c->params, tb, tsu, 1024);
     C = align_up(cdiv(2 * c->params, (uint64_t)k), kChunkAlign);
     // practical cap: the chunk is also the checksum / completion-signal unit
-    C = std::min<uint64_t>(C, 256ull << 20);
+    C = std::min<uint64_t>(C, 128ull << 20);
   }
   if (!build_image_plan(c->ts, cfg->fsdp_size, cfg->actor_layout, C, &c->plan)) return LAM_EINVAL;
   int sms = 148;
