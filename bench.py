@@ -294,11 +294,12 @@ def main():
     actor_stream = torch.cuda.Stream()
     torch.cuda.synchronize()
     state = {"v": 0}
+    pub_host = []                                   # host seconds inside lam_publish (actor stall part 1)
 
     # colocated rollouts (node 0, an actor GPU, TP=1) are written by the pack itself (lam_subscribe)
     subs = [] if args.no_subscribe else [rid for rid in mine if rollouts[rid][0] == 0 and rollouts[rid][2] == 1
                                           and rollouts[rid][1] in T["actors"]]
-    sub_done = {rid: torch.cuda.Event() for rid in subs}
+    sub_done = {rid: live_event(torch) for rid in subs}
 
     def step(h2d=None, d2h=None):
         state["v"] += 1
@@ -309,8 +310,10 @@ def main():
             if h2d is not None:                        # e2e: the step's inputs arrive from host memory
                 with torch.cuda.stream(actor_stream):
                     shards[r].buf.copy_(h2d[r], non_blocking=True)
+            t_pub = time.perf_counter()
             while ctx.publish(v, r, shards[r].shards(), actor_stream.cuda_stream) == lam.LAM_EBUSY:
                 ctx.relay_step()
+            pub_host.append(time.perf_counter() - t_pub)
         pending, streaming = [rid for rid in mine if rid not in subs], list(subs)
         while True:
             ctx.relay_step()
@@ -341,6 +344,7 @@ def main():
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    pub_host.clear()
     ctx.kernel_times()
     ctx.set_profiling(True)
     st0 = ctx.stats()
@@ -408,9 +412,17 @@ def main():
 
     kmax = {k: allmax(v or 0.0) for k, v in avg.items()}   # collective: every rank, outside rank-0 code
     pcie_peak = measure_pcie(torch) if args.config == "host" and rank == 0 else None
+    pub_timed = sorted(pub_host)
     e2e = None
     if not args.quick and not args.no_e2e:
         e2e = run_e2e(args, N, shards, bufs, mine, step, barrier, allmax, torch)
+    stall = None
+    if N == 1 and not args.quick and my_ranks:
+        stall = actor_stall(ctx, lam, shards, state, actor_stream, torch)
+    if stall is not None or pub_timed:
+        stall = dict(stall or {}, publish_host_us=dict(
+            p50=round(pub_timed[len(pub_timed) // 2] * 1e6, 1) if pub_timed else None,
+            max=round(pub_timed[-1] * 1e6, 1) if pub_timed else None, n=len(pub_timed)))
 
     if rank == 0:
         peaks = {}
@@ -452,7 +464,7 @@ def main():
             kernels_ms=kmax, per_rank=per_rank,
             host_latency_ms=dict(p50=lat[len(lat) // 2] * 1e3, max=lat[-1] * 1e3),
             paper_context="actor stall 0.64 s (32B) / 1.40 s (72B); 72B to 127 relays < 1.6 s on 128x8 H800 + RDMA",
-            cpu_baseline=cpu, e2e=e2e, gpu_launches=launches_all,
+            cpu_baseline=cpu, e2e=e2e, gpu_launches=launches_all, actor_stall=stall,
             stats=dict(publishes=st1["publishes"] - st0["publishes"], hops=st1["hops_launched"] - st0["hops_launched"],
                        pulls=st1["pulls"] - st0["pulls"], skipped=st1["versions_skipped"] - st0["versions_skipped"]),
             clocks=None if args.quick else clk.summary())
@@ -462,6 +474,85 @@ def main():
         dist.barrier(group=gloo)
         dist.destroy_process_group()
     return 0
+
+
+def live_event(torch, timing=False):
+    """A torch CUDA event with its handle created (torch creates it lazily at the first record; until
+    then .cuda_event is 0 and liblam would be handed a NULL event)."""
+    e = torch.cuda.Event(enable_timing=timing)
+    e.record()
+    return e
+
+
+def actor_stall(ctx, lam, shards, state, actor_stream, torch, reps=5, target_ms=25.0):
+    """Actor stall per publish, the trainer's view of step 5 ("pushes the new
+    actor weights to the master relay and immediately resumes its next training iteration"):
+      reads_done_wait_ms  actor-stream wait on reads_done before the next optimizer step, when that step
+                          comes one synthetic training step after the publish;
+      inflation_ms        that training step's slowdown from the concurrent pack (SM / HBM contention,
+                          PAPER L401-402): synthetic step = a bf16 GEMM loop of ~target_ms on the actor
+                          stream (torch/cuBLAS: it stands in for the trainer, it is not the path).
+    Pack-only publishes (no subscriber), each committed before the next; medians over `reps`."""
+    n = 8192
+    a = torch.randn(n, n, device="cuda", dtype=torch.bfloat16)
+    b = torch.randn(n, n, device="cuda", dtype=torch.bfloat16)
+    c = torch.empty(n, n, device="cuda", dtype=torch.bfloat16)
+    ev = lambda: torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(actor_stream):
+        for _ in range(3):
+            torch.mm(a, b, out=c)
+        e0, e1 = ev(), ev()
+        e0.record()
+        for _ in range(10):
+            torch.mm(a, b, out=c)
+        e1.record()
+    e1.synchronize()
+    iters = max(1, int(target_ms / (e0.elapsed_time(e1) / 10)))
+
+    def train_step():
+        with torch.cuda.stream(actor_stream):
+            for _ in range(iters):
+                torch.mm(a, b, out=c)
+
+    alone, total, wait, busy = [], [], [], []
+    for _ in range(reps):
+        with torch.cuda.stream(actor_stream):
+            s0, s1 = ev(), ev()
+            s0.record()
+        train_step()
+        with torch.cuda.stream(actor_stream):
+            s1.record()
+        s1.synchronize()
+        alone.append(s0.elapsed_time(s1))
+    for _ in range(reps):
+        state["v"] += 1
+        v = state["v"]
+        rd = {r: live_event(torch, timing=True) for r in shards}
+        with torch.cuda.stream(actor_stream):
+            t0, t_mid, t1 = ev(), ev(), ev()
+            t0.record()
+        for r, sh in shards.items():
+            while ctx.publish(v, r, sh.shards(), actor_stream.cuda_stream, rd[r].cuda_event) == lam.LAM_EBUSY:
+                ctx.relay_step()
+        train_step()                                   # the next training iteration, concurrent with the pack
+        with torch.cuda.stream(actor_stream):
+            t_mid.record()
+            for e in rd.values():
+                actor_stream.wait_event(e)             # before the optimizer overwrites the fp32 masters
+            t1.record()
+        t1.synchronize()
+        while ctx.relay_step()[0] != lam.LAM_IDLE:
+            pass
+        total.append(t0.elapsed_time(t_mid))
+        wait.append(t_mid.elapsed_time(t1))
+        busy.append(max(t0.elapsed_time(e) for e in rd.values()))
+    med = lambda x: sorted(x)[len(x) // 2]
+    del a, b, c
+    return dict(step_ms_alone=round(med(alone), 3), step_ms_with_publish=round(med(total), 3),
+                inflation_ms=round(med(total) - med(alone), 3),
+                inflation_frac=round(med(total) / med(alone) - 1, 4),
+                reads_done_wait_ms=round(med(wait), 4), masters_busy_ms=round(med(busy), 3),
+                actor_step=f"bf16 GEMM {n}^3 x {iters} on the actor stream (~{target_ms:.0f} ms)", reps=reps)
 
 
 def measure_pcie(torch):

@@ -109,6 +109,7 @@ def test_stream_pull_from_master_while_packing():
     torch.cuda.synchronize()
     s = torch.cuda.Stream()
     done = torch.cuda.Event()
+    done.record()                      # create the handle (torch makes it lazily)
     assert ctx.publish(4, 0, shard.shards()) == lam.LAM_OK
     assert ctx.pull_stream(0, rb.tp, s.cuda_stream, done.cuda_event, 4) == 4   # FILLING at node 0
     assert drive(ctx, 0) == (4, 0)
@@ -137,6 +138,7 @@ def test_colocated_subscription(model, N):
         rb.fill_(0xFFFF)
         torch.cuda.synchronize()
         done = torch.cuda.Event()
+        done.record()                  # create the handle (torch makes it lazily)
         ctx.subscribe(0, rb.tp, done.cuda_event)
         assert ctx.pull_state(0)[1] == 1
         for r, sh in enumerate(shards):

@@ -63,6 +63,7 @@ def test_stress_invariants(seed):
             torch.cuda._sleep(rng.choice([0, 100_000, 2_000_000]))
         shard.fill(SEED, v, specials=True, stream=actor.cuda_stream)
         ev = torch.cuda.Event()
+        ev.record(actor)                   # create the handle (torch makes it lazily)
         t0 = time.perf_counter()
         st = ctx.publish(v, 0, shard.shards(), actor.cuda_stream, ev.cuda_event)
         stalls.append(time.perf_counter() - t0)
