@@ -137,3 +137,46 @@ def test_copy_plan_reproduces_oracle_pull(model, layout, N, C, tp, tr):
         for x in layout_c:
             got = out[offs[x.name]:offs[x.name] + x.rows * x.cols * 2].view(np.uint16)
             assert np.array_equal(got, want[x.name].ravel()), (x.name, rank)
+
+
+def test_config_struct_size_matches_library():
+    """The binding's lam_config layout is the library's (a stale .so fails loudly in lam.load)."""
+    import ctypes
+    L = lam.load()
+    assert L.lam_config_size() == ctypes.sizeof(lam.lam_config)
+    assert ctypes.sizeof(lam.lam_node_desc) == 4 * (lam.LAM_MAX_RANKS + 1)   # part_device[] + host_memory
+
+
+@pytest.mark.parametrize("config,tp", [("chain", 0), ("colocated", 0), ("colocated", 2), ("relay-tp", 2),
+                                       ("relay-tp", 1), ("host", 1), ("host", 2)])
+@pytest.mark.parametrize("N", [1, 2, 4, 8])
+def test_bench_placements_are_valid(config, tp, N):
+    """bench.py placements at every N the driver's scaling run uses: devices in range, every rollout
+    rank r of a TP group present exactly once, relays hold every actor rank, and the 7B chain fits HBM."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("bench", os.path.join(os.path.dirname(__file__), "..", "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    if (config == "relay-tp" and (N < 2 or tp > N // 2) or config == "colocated" and tp and N % tp
+            or config == "host" and tp > max(1, N - 1)):
+        return                                   # not a placement the bench offers at this N
+    T = bench.topology(config, N, tp)
+    assert len(T["actors"]) == T["fsdp"] and all(0 <= d < N for d in T["actors"])
+    for node in T["relays"]:
+        assert len(node) == T["fsdp"] and all(0 <= d < N for d in node)
+    assert set(T.get("host_relays", [])) <= set(range(1, len(T["relays"]) + 1))
+    assert T["rollouts"], "every placement has at least one rollout"
+    for node, dev, tpr, rank in T["rollouts"]:
+        assert 0 <= node <= len(T["relays"]) and 0 <= dev < N and 0 <= rank < tpr
+    ranks = sorted(r for _, _, _, r in T["rollouts"])
+    tpr = T["rollouts"][0][2]
+    assert ranks == sorted(list(range(tpr)) * (len(ranks) // tpr))
+    if config == "chain":
+        P = sum(int(np.prod(s)) for _, s in otensors(OMODELS["7b"]))
+        per_gpu = {d: 0 for d in range(N)}
+        per_gpu[0] += 4 * P + 2 * 2 * P                      # fp32 masters + 2 master slots
+        for node in T["relays"]:
+            per_gpu[node[0]] += 2 * 2 * P                    # 2 relay slots (full image)
+        for _, dev, tpr, _ in T["rollouts"]:
+            per_gpu[dev] += 2 * P // tpr                     # rollout buffers
+        assert max(per_gpu.values()) < 180e9
