@@ -135,8 +135,9 @@ def run_reference(args):
     out = dict(metric=METRIC, value=value, unit=UNIT, impl="reference", n_gpus=args.gpus, steps=args.steps,
                warmup=args.warmup, ms_per_step=value * 1e3, higher_is_better=False, scaling="weak",
                vs_baseline=None, dtype="bf16", data="synthetic",
-               config=dict(workload=f"{args.model}: oracle publish+pull, bounded sample scaled to one step",
-                           model=f"Qwen2.5-{args.model.upper()}-shaped"),
+               config=dict(workload=f"{args.model} [{args.config}]: " + topology(args.config, args.gpus, args.tp)["desc"],
+                           model=f"Qwen2.5-{args.model.upper()}-shaped",
+                           reference="CPU oracle publish + TP=1 pull, bounded sample scaled to one step"),
                cpu_baseline=dict(info, value=value, host_cpus=cpu, wall_s=wall),
                e2e=dict(value=value, unit=UNIT, h2d_bytes_per_step=0, d2h_bytes_per_step=0))
     print(json.dumps(out))
