@@ -34,9 +34,9 @@ __device__ unsigned long long* g_hop_prof = nullptr;
 
 constexpr int kHopConsumers = 512;                 // 16 consumer warps
 constexpr int kHopThreads = kHopConsumers + 64;    // + producer warp + flusher warp
-constexpr int kHopStages = 7;                      // 7 x 32 KiB = 224 KiB of the 227 KiB
-constexpr uint32_t kHopSub = 32768;  // bytes per pipeline stage
-constexpr size_t kHopSmem = (size_t)kHopStages * kHopSub;
+// Pipeline geometry: kHopStages x kHopSub bytes of staging = 224 KiB of the 227 KiB.  Two instantiations:
+// 7 x 32 KiB (default) and 14 x 16 KiB (LAM_HOP_STAGE_KB=16: finer-grained hand-off, same bytes in flight).
+constexpr size_t kHopSmem = (size_t)7 * 32768;
 
 enum : int { kHopOk = 0, kHopPoison = 1, kHopAbort = 2, kHopTimeout = 3 };
 
@@ -103,6 +103,7 @@ __device__ void hop_flush(ChunkMeta meta, const RankLink& L, const uint32_t* til
   }
 }
 
+template <int kHopStages, uint32_t kHopSub>
 __global__ void __launch_bounds__(kHopThreads, 1)
     k_hop(const HopTile* __restrict__ tiles, uint32_t n_tiles, const RankLink* __restrict__ links, ChunkMeta meta,
           const uint32_t* __restrict__ tiles_per_chunk, uint64_t version, uint32_t* err_word, uint64_t timeout_ns) {
@@ -294,15 +295,24 @@ int launch_hop(const HopTile* tiles, uint32_t n_tiles, const RankLink* links, Ch
                const uint32_t* tiles_per_chunk, uint64_t version, uint32_t* err_word, uint64_t timeout_ns,
                int ctas, void* stream) {
   if (n_tiles == 0) return 0;
+  static const bool fine = [] {
+    const char* e = getenv("LAM_HOP_STAGE_KB");
+    return e && atoi(e) == 16;
+  }();
   static bool attr[64] = {};  // the attribute is per device
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 64 && !attr[dev]) {
-    cudaFuncSetAttribute(k_hop, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kHopSmem);
+    cudaFuncSetAttribute(k_hop<7, 32768>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kHopSmem);
+    cudaFuncSetAttribute(k_hop<14, 16384>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kHopSmem);
     attr[dev] = true;
   }
   unsigned grid = (unsigned)(n_tiles < (uint32_t)ctas ? n_tiles : (uint32_t)ctas);
-  k_hop<<<grid, kHopThreads, kHopSmem, (cudaStream_t)stream>>>(tiles, n_tiles, links, meta, tiles_per_chunk, version,
-                                                              err_word, timeout_ns);
+  if (fine)
+    k_hop<14, 16384><<<grid, kHopThreads, kHopSmem, (cudaStream_t)stream>>>(tiles, n_tiles, links, meta,
+                                                                         tiles_per_chunk, version, err_word, timeout_ns);
+  else
+    k_hop<7, 32768><<<grid, kHopThreads, kHopSmem, (cudaStream_t)stream>>>(tiles, n_tiles, links, meta,
+                                                                        tiles_per_chunk, version, err_word, timeout_ns);
   return (int)cudaGetLastError();
 }
