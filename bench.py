@@ -446,8 +446,9 @@ def main():
                        else "fallback 6.65 TB/s" if dom["bound"] == "hbm"
                        else "B200_PROFILING.md measured peer copy 770 GB/s/dir (nominal 900)")
             ach = dom["bytes"] / (dom["ms"] / 1e3) / 1e9
+            nominal = {"hbm": 8000.0, "nvlink": 900.0}.get(dom["bound"])
             roof = dict(bound=dom["bound"], kernel=dom["kernel"], achieved=ach, peak=peak, unit="GB/s",
-                        frac=ach / peak, traffic=traffic_of(dom["kernel"], args.model, N, args.config),
+                        frac=ach / peak, frac_of_nominal=(ach / nominal if nominal else None), traffic=traffic_of(dom["kernel"], args.model, N, args.config),
                         algorithmic_bytes_per_launch=dom["bytes"], launch_ms=dom["ms"], peak_source=src)
         cpu = None
         if N == 1 and not args.quick and not args.no_cpu_baseline:

@@ -121,6 +121,7 @@ struct PendingPull {
 
 struct DevLocal {
   uint64_t* d_chunk_len = nullptr;   // per device: [total_chunks]
+  uint32_t* d_pack_work = nullptr;   // k_pack's dynamic unit counter (packs are serialised on `side`)
   cudaStream_t side = nullptr;
 };
 
@@ -374,6 +375,7 @@ lam_status alloc_parts(lam_ctx* c) {
       CK(cudaMalloc(&dl.d_chunk_len, 8 * std::max<uint64_t>(total, 1)));
       if (total) CK(cudaMemcpy(dl.d_chunk_len, len.data(), 8 * total, cudaMemcpyHostToDevice));
       CK(cudaStreamCreateWithPriority(&dl.side, cudaStreamNonBlocking, lo));
+      CK(cudaMalloc(&dl.d_pack_work, sizeof(uint32_t)));
       c->dev[p.device] = dl;
     }
     if (p.node > 0) {
@@ -1210,7 +1212,8 @@ extern "C" lam_status lam_publish(lam_ctx* c, uint64_t v, int32_t rank, const la
     sub = rp.d_sub;
   }
   int rc = launch_pack(rp.d_units, rp.n_units, rp.d_ptrs, slot_data(p, s), m, rp.d_units_per_chunk, v,
-                       c->plan.total_chunks, c->dev[dev].d_chunk_len, c->pack_ctas, side, sub);
+                       c->plan.total_chunks, c->dev[dev].d_chunk_len, c->pack_ctas, side, sub,
+                       c->dev[dev].d_pack_work);
   if (rc) {
     fprintf(stderr, "liblam: pack launch failed: %s\n", cudaGetErrorString((cudaError_t)rc));
     return LAM_ECUDA;
@@ -1528,6 +1531,7 @@ extern "C" void lam_destroy(lam_ctx* c) {
     cudaSetDevice(kv.first);
     cudaDeviceSynchronize();
     if (kv.second.d_chunk_len) cudaFree(kv.second.d_chunk_len);
+    if (kv.second.d_pack_work) cudaFree(kv.second.d_pack_work);
     if (kv.second.side) cudaStreamDestroy(kv.second.side);
   }
   for (auto& kv : c->plans) {
