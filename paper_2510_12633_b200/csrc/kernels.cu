@@ -385,26 +385,29 @@ __device__ __forceinline__ void pull_zero(const CopyTile& T, uint8_t* dst) {
 
 // K-major tiles only (one CTA per SM: 128 KiB of staging smem); other tiles are skipped.
 __global__ void __launch_bounds__(kPullThreads, 1) k_pull_t(const CopyTile* __restrict__ tiles, uint32_t n_tiles,
-                                                         const uint8_t* const* __restrict__ rank_base) {
+                                                         const uint8_t* const* __restrict__ rank_base,
+                                                         uint32_t* __restrict__ work) {
   extern __shared__ __align__(128) uint8_t pull_smem[];
-  for (uint32_t ti = blockIdx.x; ti < n_tiles; ti += gridDim.x) {
+  __shared__ uint32_t s_next[2];
+  uint32_t it = 0;
+  for (uint32_t ti = blockIdx.x; ti < n_tiles; ++it) {
+    if (threadIdx.x == 0) s_next[it & 1] = gridDim.x + atomicAdd(work, 1u);   // next tile, fetched ahead
     const CopyTile T = tiles[ti];
-    if (T.src_rank == LAM_TILE_ZERO || !(T.align & LAM_TILE_TRANSPOSE)) continue;
-    pull_transposed(T, rank_base[T.src_rank] + T.src_off, reinterpret_cast<uint8_t*>(T.dst), pull_smem);
+    if (T.src_rank != LAM_TILE_ZERO && (T.align & LAM_TILE_TRANSPOSE))
+      pull_transposed(T, rank_base[T.src_rank] + T.src_off, reinterpret_cast<uint8_t*>(T.dst), pull_smem);
+    __syncthreads();
+    ti = s_next[it & 1];   // double-buffered: rewritten only after the next barrier
   }
 }
 
-// Row-major and zero tiles (no shared memory: co-resides with k_hop); K-major tiles are skipped.
-__global__ void __launch_bounds__(kPullThreads) k_pull(const CopyTile* __restrict__ tiles, uint32_t n_tiles,
-                                                       const uint8_t* const* __restrict__ rank_base) {
-  for (uint32_t ti = blockIdx.x; ti < n_tiles; ti += gridDim.x) {
-    const CopyTile T = tiles[ti];
+__device__ __forceinline__ void pull_tile(const CopyTile& T, const uint8_t* const* __restrict__ rank_base) {
+  {
     uint8_t* dst = reinterpret_cast<uint8_t*>(T.dst);
     if (T.src_rank == LAM_TILE_ZERO) {
       pull_zero(T, dst);
-      continue;
+      return;
     }
-    if (T.align & LAM_TILE_TRANSPOSE) continue;
+    if (T.align & LAM_TILE_TRANSPOSE) return;
     const uint8_t* src = rank_base[T.src_rank] + T.src_off;
     if (T.align == 16) {
       const uint32_t vpr = T.row_bytes >> 4, total = vpr * T.rows;
@@ -461,9 +464,31 @@ __global__ void __launch_bounds__(kPullThreads) k_pull(const CopyTile* __restric
   }
 }
 
+// Row-major and zero tiles (no shared memory: co-resides with k_hop); K-major tiles are skipped.
+// Tiles are distributed dynamically (first tile = blockIdx.x, then a per-stream work counter zeroed
+// before the launch, fetched one tile ahead): the static round-robin left ncu's per-SM active cycles
+// at min 3.45 M / avg 4.36 M / max 4.96 M of 4.96 M elapsed (r1d, 7B TP=2) — the same imbalance the
+// pack had.
+__global__ void __launch_bounds__(kPullThreads) k_pull(const CopyTile* __restrict__ tiles, uint32_t n_tiles,
+                                                       const uint8_t* const* __restrict__ rank_base,
+                                                       uint32_t* __restrict__ work) {
+  __shared__ uint32_t s_next[2];
+  uint32_t it = 0;
+  for (uint32_t ti = blockIdx.x; ti < n_tiles; ++it) {
+    if (threadIdx.x == 0) s_next[it & 1] = gridDim.x + atomicAdd(work, 1u);   // next tile, fetched ahead
+    pull_tile(tiles[ti], rank_base);
+    __syncthreads();
+    ti = s_next[it & 1];   // double-buffered: rewritten only after the next barrier
+  }
+}
+
+
 int launch_pull(const CopyTile* tiles, uint32_t n_tiles, const uint8_t* const* rank_base, int ctas, void* stream,
-                uint32_t kinds) {
+                uint32_t kinds, uint32_t* work) {
   if (n_tiles == 0) return 0;
+  // work[0]: k_pull_t's tile counter, work[1]: k_pull's (both kernels run in order on `stream`)
+  cudaError_t me = cudaMemsetAsync(work, 0, 2 * sizeof(uint32_t), (cudaStream_t)stream);
+  if (me != cudaSuccess) return (int)me;
   int dev = 0;
   cudaGetDevice(&dev);
   if (kinds & kPullKMajor) {
@@ -475,12 +500,12 @@ int launch_pull(const CopyTile* tiles, uint32_t n_tiles, const uint8_t* const* r
     }
     const int n = ctas > 0 ? ctas : resident_ctas(k_pull_t, kPullThreads, kPullSmem);
     const unsigned grid = (unsigned)std::min<uint32_t>(n_tiles, (uint32_t)n);
-    k_pull_t<<<grid, kPullThreads, kPullSmem, (cudaStream_t)stream>>>(tiles, n_tiles, rank_base);
+    k_pull_t<<<grid, kPullThreads, kPullSmem, (cudaStream_t)stream>>>(tiles, n_tiles, rank_base, work);
   }
   if (kinds & kPullRowMajor) {
     const int n = ctas > 0 ? ctas : resident_ctas(k_pull, kPullThreads);
     const unsigned grid = (unsigned)std::min<uint32_t>(n_tiles, (uint32_t)n);
-    k_pull<<<grid, kPullThreads, 0, (cudaStream_t)stream>>>(tiles, n_tiles, rank_base);
+    k_pull<<<grid, kPullThreads, 0, (cudaStream_t)stream>>>(tiles, n_tiles, rank_base, work + 1);
   }
   return (int)cudaGetLastError();
 }

@@ -142,6 +142,7 @@ struct lam_ctx {
   std::vector<RankPub> pubs;                  // [N]; local ranks only used
   std::map<int, DevLocal> dev;                // devices owned by this process
   std::map<std::string, PullPlan> plans;
+  std::map<std::pair<int, void*>, uint32_t*> pull_work;  // (device, stream) -> k_pull's 2 tile counters
   std::map<std::pair<int, int>, const uint8_t**> d_rank_base;  // (node*S+slot, device) -> device array
   std::vector<PendingPull> pending;
   std::map<int, std::vector<cudaEvent_t>> ev_pool;  // per device
@@ -259,6 +260,18 @@ lam_status map_host_part(Part& p, int fd, size_t bytes) {
   p.data = (uint8_t*)d;
   p.base = (uint8_t*)h;   // host address (munmap / unregister)
   return LAM_OK;
+}
+
+// Tile counters of the pull kernels' dynamic distribution: one pair per (device, stream) — launches
+// on one stream run in order, launches on different streams never share a counter.
+uint32_t* pull_counter(lam_ctx* c, int dev, void* stream) {
+  const auto key = std::make_pair(dev, stream);
+  auto it = c->pull_work.find(key);
+  if (it != c->pull_work.end()) return it->second;
+  uint32_t* p = nullptr;
+  if (cudaMalloc(&p, 2 * sizeof(uint32_t)) != cudaSuccess) return nullptr;
+  c->pull_work[key] = p;
+  return p;
 }
 
 lam_status validate(const lam_config& c, std::string* why) {
@@ -770,7 +783,10 @@ lam_status stream_progress(lam_ctx* c, int rid, int* transitions) {
       auto rb = c->d_rank_base.find({sp.node * LAM_MAX_SLOTS + sp.slot, sp.device});
       const uint32_t b = sp.plan->chunk_begin[first], e = sp.plan->chunk_begin[sp.next];
       cudaEvent_t t0 = prof_begin(c, sp.device, sp.stream);
-      if (launch_pull(sp.plan->d_tiles + b, e - b, rb->second, c->pull_ctas, sp.stream, sp.plan->kinds)) return LAM_ECUDA;
+      uint32_t* work = pull_counter(c, sp.device, sp.stream);
+      if (!work) return LAM_ENOMEM;
+      if (launch_pull(sp.plan->d_tiles + b, e - b, rb->second, c->pull_ctas, sp.stream, sp.plan->kinds, work))
+        return LAM_ECUDA;
       prof_end(c, 2, sp.device, sp.stream, t0);
       if (!sp.last) CK(cudaEventCreateWithFlags(&sp.last, cudaEventDisableTiming));
       CK(cudaEventRecord(sp.last, sp.stream));
@@ -1319,7 +1335,9 @@ extern "C" lam_status lam_pull(lam_ctx* c, int32_t rid, const lam_tp_layout* L, 
     return LAM_EINVAL;
   }
   cudaEvent_t t0 = prof_begin(c, ro.device, (cudaStream_t)stream);
-  int rc = launch_pull(pp->d_tiles, pp->n_tiles, rb->second, c->pull_ctas, stream, pp->kinds);
+  uint32_t* work = pull_counter(c, ro.device, stream);
+  int rc = work ? launch_pull(pp->d_tiles, pp->n_tiles, rb->second, c->pull_ctas, stream, pp->kinds, work)
+                : (int)cudaErrorMemoryAllocation;
   if (rc) {
     ctl::unpin(c->shm, ro.node, s);
     fprintf(stderr, "liblam: pull launch failed: %s\n", cudaGetErrorString((cudaError_t)rc));
@@ -1536,6 +1554,10 @@ extern "C" void lam_destroy(lam_ctx* c) {
   }
   for (auto& kv : c->plans) {
     cudaFree(kv.second.d_tiles);
+  }
+  for (auto& kv : c->pull_work) {
+    cudaSetDevice(kv.first.first);
+    cudaFree(kv.second);
   }
   for (auto& kv : c->d_rank_base) {
     cudaSetDevice(kv.first.second);
