@@ -465,8 +465,8 @@ __device__ __forceinline__ void pull_tile(const CopyTile& T, const uint8_t* cons
 }
 
 // Row-major and zero tiles (no shared memory: co-resides with k_hop); K-major tiles are skipped.
-// Tiles are distributed dynamically (first tile = blockIdx.x, then a per-stream work counter zeroed
-// before the launch, fetched one tile ahead): the static round-robin left ncu's per-SM active cycles
+// Tiles are distributed dynamically (first tile = blockIdx.x, then a per-launch work counter zeroed
+// on the launch stream, fetched one tile ahead): the static round-robin left ncu's per-SM active cycles
 // at min 3.45 M / avg 4.36 M / max 4.96 M of 4.96 M elapsed (r1d, 7B TP=2) — the same imbalance the
 // pack had.
 __global__ void __launch_bounds__(kPullThreads) k_pull(const CopyTile* __restrict__ tiles, uint32_t n_tiles,

@@ -139,7 +139,7 @@ int launch_hop(const HopTile* tiles, uint32_t n_tiles, const RankLink* links, Ch
                uint64_t timeout_ns, int ctas, void* stream);
 constexpr uint32_t kPullRowMajor = 1, kPullKMajor = 2;   // tile kinds present in a pull (launch_pull)
 int launch_pull(const CopyTile* tiles, uint32_t n_tiles, const uint8_t* const* rank_base, int ctas,
-                void* stream, uint32_t kinds, uint32_t* work);  // work: 2 counters owned by `stream`
+                void* stream, uint32_t kinds, uint32_t* work);  // work: 2 counters, zeroed on `stream` here
 // Diagnostics (LAM_HOP_PROF=1): 7 per-device cycle counters accumulated by k_hop's thread 0.
 int hop_set_profile(unsigned long long* buf);
 // One-thread kernel: spin until (int64)(*flag - v) >= 0 or timeout (fallback for stream memory ops).

@@ -142,7 +142,8 @@ struct lam_ctx {
   std::vector<RankPub> pubs;                  // [N]; local ranks only used
   std::map<int, DevLocal> dev;                // devices owned by this process
   std::map<std::string, PullPlan> plans;
-  std::map<std::pair<int, void*>, uint32_t*> pull_work;  // (device, stream) -> k_pull's 2 tile counters
+  struct PullRing { uint32_t* d = nullptr; uint32_t next = 0; };
+  std::map<int, PullRing> pull_work;  // per device: ring of k_pull tile-counter pairs
   std::map<std::pair<int, int>, const uint8_t**> d_rank_base;  // (node*S+slot, device) -> device array
   std::vector<PendingPull> pending;
   std::map<int, std::vector<cudaEvent_t>> ev_pool;  // per device
@@ -262,16 +263,17 @@ lam_status map_host_part(Part& p, int fd, size_t bytes) {
   return LAM_OK;
 }
 
-// Tile counters of the pull kernels' dynamic distribution: one pair per (device, stream) — launches
-// on one stream run in order, launches on different streams never share a counter.
-uint32_t* pull_counter(lam_ctx* c, int dev, void* stream) {
-  const auto key = std::make_pair(dev, stream);
-  auto it = c->pull_work.find(key);
-  if (it != c->pull_work.end()) return it->second;
-  uint32_t* p = nullptr;
-  if (cudaMalloc(&p, 2 * sizeof(uint32_t)) != cudaSuccess) return nullptr;
-  c->pull_work[key] = p;
-  return p;
+// Tile counters of the pull kernels' dynamic distribution: every launch takes the next pair of a
+// per-device ring (zeroed by launch_pull on the launch's own stream), so launches in flight on
+// different streams never share a counter unless kPullRing of them are queued at once.
+constexpr uint32_t kPullRing = 4096;
+uint32_t* pull_counter(lam_ctx* c, int dev) {
+  lam_ctx::PullRing& r = c->pull_work[dev];
+  if (!r.d && cudaMalloc(&r.d, 2 * sizeof(uint32_t) * kPullRing) != cudaSuccess) {
+    r.d = nullptr;
+    return nullptr;
+  }
+  return r.d + 2 * (r.next++ % kPullRing);
 }
 
 lam_status validate(const lam_config& c, std::string* why) {
@@ -783,7 +785,7 @@ lam_status stream_progress(lam_ctx* c, int rid, int* transitions) {
       auto rb = c->d_rank_base.find({sp.node * LAM_MAX_SLOTS + sp.slot, sp.device});
       const uint32_t b = sp.plan->chunk_begin[first], e = sp.plan->chunk_begin[sp.next];
       cudaEvent_t t0 = prof_begin(c, sp.device, sp.stream);
-      uint32_t* work = pull_counter(c, sp.device, sp.stream);
+      uint32_t* work = pull_counter(c, sp.device);
       if (!work) return LAM_ENOMEM;
       if (launch_pull(sp.plan->d_tiles + b, e - b, rb->second, c->pull_ctas, sp.stream, sp.plan->kinds, work))
         return LAM_ECUDA;
@@ -1335,7 +1337,7 @@ extern "C" lam_status lam_pull(lam_ctx* c, int32_t rid, const lam_tp_layout* L, 
     return LAM_EINVAL;
   }
   cudaEvent_t t0 = prof_begin(c, ro.device, (cudaStream_t)stream);
-  uint32_t* work = pull_counter(c, ro.device, stream);
+  uint32_t* work = pull_counter(c, ro.device);
   int rc = work ? launch_pull(pp->d_tiles, pp->n_tiles, rb->second, c->pull_ctas, stream, pp->kinds, work)
                 : (int)cudaErrorMemoryAllocation;
   if (rc) {
@@ -1556,8 +1558,8 @@ extern "C" void lam_destroy(lam_ctx* c) {
     cudaFree(kv.second.d_tiles);
   }
   for (auto& kv : c->pull_work) {
-    cudaSetDevice(kv.first.first);
-    cudaFree(kv.second);
+    cudaSetDevice(kv.first);
+    if (kv.second.d) cudaFree(kv.second.d);
   }
   for (auto& kv : c->d_rank_base) {
     cudaSetDevice(kv.first.second);
