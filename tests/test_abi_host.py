@@ -180,3 +180,28 @@ def test_bench_placements_are_valid(config, tp, N):
         for _, dev, tpr, _ in T["rollouts"]:
             per_gpu[dev] += 2 * P // tpr                     # rollout buffers
         assert max(per_gpu.values()) < 180e9
+
+
+@pytest.mark.parametrize("config,model,tp", [("colocated", "32b", 2),     # the 32B x 8 reading
+                                              ("colocated", "72b", 8), ("colocated", "72b", 4),   # config 4
+                                              ("relay-tp", "32b", 2)])   # config 3
+def test_full_size_8gpu_placements_fit_hbm(config, model, tp):
+    """The full-size 8-GPU configurations (only their 4-GPU scalings could be measured) fit 180 GB per
+    GPU: fp32 master shards + 2 ring slots of every part a GPU stores + its rollout's TP buffers."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("bench", os.path.join(os.path.dirname(__file__), "..", "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    N = 8
+    T = bench.topology(config, N, tp)
+    P = sum(int(np.prod(s)) for _, s in otensors(OMODELS[model]))
+    n = T["fsdp"]
+    per_gpu = {d: 0.0 for d in range(N)}
+    for d in T["actors"]:
+        per_gpu[d] += 4 * P / n + 2 * (2 * P / n)            # fp32 shard + 2 master slots of its bf16 region
+    for node in T["relays"]:
+        for d in node:
+            per_gpu[d] += 2 * (2 * P / n)                    # 2 relay slots of one rank region
+    for _, dev, tpr, _ in T["rollouts"]:
+        per_gpu[dev] += 2 * P / tpr
+    assert max(per_gpu.values()) < 180e9, per_gpu
