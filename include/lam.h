@@ -255,7 +255,8 @@ lam_status lam_pull_stream(lam_ctx*, int32_t rollout_id, const lam_tp_layout* la
  * bf16 bytes go to the master slot and to the rollout: 8 instead of 4 + 6 B/param of HBM traffic).
  * `done_event` (caller-created, may be NULL) is recorded after that pack; lam_pull_state then
  * reports (version, 0).  One-shot: subscribe again for the next version.  LAM_EINVAL if the rollout
- * or layout does not qualify (use lam_pull / lam_pull_stream instead). */
+ * or layout does not qualify (use lam_pull / lam_pull_stream instead) — in particular unless EVERY
+ * actor rank is packed on the rollout's GPU (the pack only writes the shards it packs there). */
 lam_status lam_subscribe(lam_ctx*, int32_t rollout_id, const lam_tp_layout* layout, void* done_event);
 
 /* State of the rollout's streaming pull: 1 = chunks still arriving, 0 = all enqueued (or none),

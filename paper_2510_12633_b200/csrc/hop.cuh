@@ -156,6 +156,9 @@ __global__ void __launch_bounds__(kHopThreads, 1)
         }
         if (prof) { t_b = clock64(); pc[2] += t_b - t_a; t_a = t_b; }
         if (status != kHopOk) { fail_chunk = T.chunk; break; }
+        // the flag was acquired by a generic-proxy load; the chunk's bytes are read by the async
+        // proxy (cp.async.bulk): order those reads after the acquire
+        asm volatile("fence.proxy.async.global;" ::: "memory");
         waited = T.chunk;
       }
       for (uint32_t off = 0; off < T.bytes; off += kHopSub, ++job) {

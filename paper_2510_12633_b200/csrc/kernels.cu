@@ -556,24 +556,28 @@ __global__ void __launch_bounds__(kVerifyThreads) k_verify(const uint8_t* __rest
     __threadfence_system();
     publish_flag(meta, chunk, version);
   } else {
+    // failure stays local: poison our own flag (the successor aborts) and raise our abort flag, which
+    // the flag waits queued for this part's later chunks poll (k_wait_flag) — never write into the
+    // predecessor's flags (its state is its own)
     atomicCAS(err_word, 0u, (uint32_t)(-LAM_ECHECKSUM));
+    atomicExch(meta.abort_flag, 1);
     publish_flag(meta, chunk, version | kPoison);
-    for (uint32_t j = pos + 1; j < n_my; ++j) st_release_sys(pred_flags + my_chunks[j], version | kPoison);
     __threadfence_system();
   }
 }
 
-__global__ void k_wait_flag(const uint64_t* flag, uint64_t v, uint64_t timeout_ns) {
+__global__ void k_wait_flag(const uint64_t* flag, uint64_t v, uint64_t timeout_ns, const int32_t* abort_flag) {
   const uint64_t deadline = globaltimer() + timeout_ns;
   for (uint32_t spin = 0;; ++spin) {
     if ((int64_t)(ld_acquire_sys(flag) - v) >= 0) return;
+    if (abort_flag && *(volatile const int32_t*)abort_flag) return;   // this part failed / was superseded
     if ((spin & 63) == 63 && globaltimer() > deadline) return;  // k_verify then reports the failure
     __nanosleep(200);
   }
 }
 
-int launch_wait_flag(const uint64_t* flag, uint64_t v, uint64_t timeout_ns, void* stream) {
-  k_wait_flag<<<1, 1, 0, (cudaStream_t)stream>>>(flag, v, timeout_ns);
+int launch_wait_flag(const uint64_t* flag, uint64_t v, uint64_t timeout_ns, const int32_t* abort_flag, void* stream) {
+  k_wait_flag<<<1, 1, 0, (cudaStream_t)stream>>>(flag, v, timeout_ns, abort_flag);
   return (int)cudaGetLastError();
 }
 

@@ -142,12 +142,13 @@ int launch_pull(const CopyTile* tiles, uint32_t n_tiles, const uint8_t* const* r
                 void* stream, uint32_t kinds, uint32_t* work);  // work: 2 counters, zeroed on `stream` here
 // Diagnostics (LAM_HOP_PROF=1): 7 per-device cycle counters accumulated by k_hop's thread 0.
 int hop_set_profile(unsigned long long* buf);
-// One-thread kernel: spin until (int64)(*flag - v) >= 0 or timeout (fallback for stream memory ops).
-int launch_wait_flag(const uint64_t* flag, uint64_t v, uint64_t timeout_ns, void* stream);
+// One-thread kernel: spin until (int64)(*flag - v) >= 0, *abort_flag != 0 or timeout (fallback for
+// stream memory ops).
+int launch_wait_flag(const uint64_t* flag, uint64_t v, uint64_t timeout_ns, const int32_t* abort_flag,
+                     void* stream);
 // Copy-engine hop: verify chunk `chunk` (len bytes at `data`, already copied from the predecessor)
-// against the predecessor's header; publish the header and flag — or poison it and also poison the
-// predecessor flags of this part's later chunks (my_chunks[pos+1 .. n_my)) so that the stream's
-// remaining flag waits fall through and the hop terminates.
+// against the predecessor's header; publish the header and flag — or poison our own flag and raise our
+// abort flag, so that the part's remaining flag waits fall through (the runtime also stops enqueuing).
 int launch_verify(const uint8_t* data, uint32_t chunk, uint64_t len, uint64_t* pred_flags,
                   const lam_chunk_header* pred_hdr, ChunkMeta meta, uint64_t version, uint32_t* err_word,
                   const uint32_t* my_chunks, uint32_t pos, uint32_t n_my, int ctas, void* stream);

@@ -112,7 +112,12 @@ struct PullPlan {
   uint32_t kinds = 0;                 // kPullRowMajor (row-major / zero tiles) | kPullKMajor
   std::vector<uint32_t> chunk_ids;    // source chunks in order
   std::vector<uint32_t> chunk_begin;  // [chunk_ids.size() + 1] tile ranges per chunk
+  int device = 0;
+  uint64_t last_use = 0;              // LRU stamp (bounded cache, kMaxPlans)
+  cudaEvent_t last_ev = nullptr;      // recorded after the latest launch reading d_tiles
 };
+
+constexpr size_t kMaxPlans = 64;   // pull-plan cache bound (LRU)
 
 struct PendingPull {
   cudaEvent_t ev;
@@ -142,7 +147,8 @@ struct lam_ctx {
   std::vector<RankPub> pubs;                  // [N]; local ranks only used
   std::map<int, DevLocal> dev;                // devices owned by this process
   std::map<std::string, PullPlan> plans;
-  struct PullRing { uint32_t* d = nullptr; uint32_t next = 0; };
+  uint64_t plan_clock = 0;
+  struct PullRing { uint32_t* d = nullptr; uint32_t next = 0; std::vector<cudaEvent_t> ev; };
   std::map<int, PullRing> pull_work;  // per device: ring of k_pull tile-counter pairs
   std::map<std::pair<int, int>, const uint8_t**> d_rank_base;  // (node*S+slot, device) -> device array
   std::vector<PendingPull> pending;
@@ -265,15 +271,27 @@ lam_status map_host_part(Part& p, int fd, size_t bytes) {
 
 // Tile counters of the pull kernels' dynamic distribution: every launch takes the next pair of a
 // per-device ring (zeroed by launch_pull on the launch's own stream), so launches in flight on
-// different streams never share a counter unless kPullRing of them are queued at once.
-constexpr uint32_t kPullRing = 4096;
-uint32_t* pull_counter(lam_ctx* c, int dev) {
+// different streams never share a counter.  Each entry carries the event recorded after its last
+// launch; an entry whose launch has not completed is waited for before reuse (only possible with
+// kPullRing launches queued at once).  The caller records *ev after its launch.
+constexpr uint32_t kPullRing = 1024;
+uint32_t* pull_counter(lam_ctx* c, int dev, cudaEvent_t* ev) {
   lam_ctx::PullRing& r = c->pull_work[dev];
-  if (!r.d && cudaMalloc(&r.d, 2 * sizeof(uint32_t) * kPullRing) != cudaSuccess) {
-    r.d = nullptr;
+  if (!r.d) {
+    if (cudaMalloc(&r.d, 2 * sizeof(uint32_t) * kPullRing) != cudaSuccess) {
+      r.d = nullptr;
+      return nullptr;
+    }
+    r.ev.assign(kPullRing, nullptr);
+  }
+  const uint32_t i = r.next++ % kPullRing;
+  if (!r.ev[i]) {
+    if (cudaEventCreateWithFlags(&r.ev[i], cudaEventDisableTiming) != cudaSuccess) return nullptr;
+  } else if (cudaEventSynchronize(r.ev[i]) != cudaSuccess) {   // normally long complete: returns at once
     return nullptr;
   }
-  return r.d + 2 * (r.next++ % kPullRing);
+  *ev = r.ev[i];
+  return r.d + 2 * i;
 }
 
 lam_status validate(const lam_config& c, std::string* why) {
@@ -513,13 +531,13 @@ WaitValue64Fn wait_value_fn() {
 
 // Stream waits until (int64)(*flag - v) >= 0 (flag == v, or v | kPoison): a front-end stream memory
 // operation when the driver supports it, else a one-thread polling kernel.
-lam_status stream_wait_flag(lam_ctx* c, cudaStream_t st, const uint64_t* flag, uint64_t v) {
+lam_status stream_wait_flag(lam_ctx* c, cudaStream_t st, const uint64_t* flag, uint64_t v, const int32_t* abort_flag) {
   // Stream memory ops on CUDA-IPC-mapped peer memory never released in multi-process runs on
   // B200 / driver 580 (observed hang); there, poll with a one-thread kernel instead.
   WaitValue64Fn fn = c->cfg.n_procs == 1 ? wait_value_fn() : nullptr;
   if (fn && fn((void*)st, (unsigned long long)(uintptr_t)flag, v, 0x0 /*CU_STREAM_WAIT_VALUE_GEQ*/) == 0)
     return LAM_OK;
-  if (launch_wait_flag(flag, v, c->timeout_ns, st)) return LAM_ECUDA;
+  if (launch_wait_flag(flag, v, c->timeout_ns, abort_flag, st)) return LAM_ECUDA;
   return LAM_OK;
 }
 
@@ -537,6 +555,10 @@ lam_status ce_topup(lam_ctx* c, Part& p) {
   const uint32_t n = (uint32_t)p.my_chunks.size();
   CK(cudaSetDevice(p.device));
   for (uint32_t i = p.ce_next; i < n; i = ++p.ce_next) {
+    if (*(volatile uint32_t*)&p.err_host[s]) {   // a chunk failed verification: enqueue nothing more, close the hop
+      p.ce_next = n;
+      break;
+    }
     if (i >= kCeWindow) {
       cudaError_t q = cudaEventQuery(p.chunk_ev[i - kCeWindow]);
       if (q == cudaErrorNotReady) return LAM_OK;
@@ -549,7 +571,7 @@ lam_status ce_topup(lam_ctx* c, Part& p) {
     const uint64_t off = (g - c->plan.chunk_base[r]) * c->plan.C, len = c->plan.chunk_len(g);
     const uint8_t* src = slot_data(q, ps) + q.rank_off[r] + off;
     uint8_t* dst = slot_data(p, s) + p.rank_off[r] + off;
-    lam_status st = stream_wait_flag(c, p.stream, qm.flags + g, u);
+    lam_status st = stream_wait_flag(c, p.stream, qm.flags + g, u, m.abort_flag);
     if (st != LAM_OK) return st;
     CK(cudaMemcpyAsync(dst, src, len, cudaMemcpyDefault, p.stream));
     CK(cudaEventRecord(p.chunk_ev[i], p.stream));
@@ -785,10 +807,13 @@ lam_status stream_progress(lam_ctx* c, int rid, int* transitions) {
       auto rb = c->d_rank_base.find({sp.node * LAM_MAX_SLOTS + sp.slot, sp.device});
       const uint32_t b = sp.plan->chunk_begin[first], e = sp.plan->chunk_begin[sp.next];
       cudaEvent_t t0 = prof_begin(c, sp.device, sp.stream);
-      uint32_t* work = pull_counter(c, sp.device);
+      cudaEvent_t wev = nullptr;
+      uint32_t* work = pull_counter(c, sp.device, &wev);
       if (!work) return LAM_ENOMEM;
       if (launch_pull(sp.plan->d_tiles + b, e - b, rb->second, c->pull_ctas, sp.stream, sp.plan->kinds, work))
         return LAM_ECUDA;
+      CK(cudaEventRecord(wev, sp.stream));
+      CK(cudaEventRecord(sp.plan->last_ev, sp.stream));
       prof_end(c, 2, sp.device, sp.stream, t0);
       if (!sp.last) CK(cudaEventCreateWithFlags(&sp.last, cudaEventDisableTiming));
       CK(cudaEventRecord(sp.last, sp.stream));
@@ -909,8 +934,30 @@ lam_status get_plan(lam_ctx* c, const lam_rollout_desc& ro, const lam_tp_layout&
   auto it = c->plans.find(key);
   if (it != c->plans.end()) {
     c->shm->stats.plan_cache_hits++;
+    it->second.last_use = ++c->plan_clock;
     *out = &it->second;
     return LAM_OK;
+  }
+  // bounded cache (keys hold destination addresses, which callers may reallocate): evict the least
+  // recently used plan no streaming pull is using, once its last launch has completed
+  if (c->plans.size() >= kMaxPlans) {
+    auto victim = c->plans.end();
+    for (auto jt = c->plans.begin(); jt != c->plans.end(); ++jt) {
+      bool busy = false;
+      for (const auto& sp : c->streams) busy |= sp.active && sp.plan == &jt->second;
+      if (!busy && (victim == c->plans.end() || jt->second.last_use < victim->second.last_use)) victim = jt;
+    }
+    if (victim != c->plans.end()) {
+      PullPlan& v = victim->second;
+      CK(cudaSetDevice(v.device));
+      if (v.last_ev) {
+        CK(cudaEventSynchronize(v.last_ev));
+        cudaEventDestroy(v.last_ev);
+      }
+      cudaFree(v.d_tiles);
+      c->plans.erase(victim);
+      CK(cudaSetDevice(ro.device));
+    }
   }
   std::vector<CopyTile> tiles;
   uint64_t bytes = 0;
@@ -945,6 +992,9 @@ lam_status get_plan(lam_ctx* c, const lam_rollout_desc& ro, const lam_tp_layout&
   }
   CK(cudaMalloc(&pp.d_tiles, sizeof(CopyTile) * std::max<size_t>(tiles.size(), 1)));
   if (!tiles.empty()) CK(cudaMemcpy(pp.d_tiles, tiles.data(), sizeof(CopyTile) * tiles.size(), cudaMemcpyHostToDevice));
+  CK(cudaEventCreateWithFlags(&pp.last_ev, cudaEventDisableTiming));
+  pp.device = ro.device;
+  pp.last_use = ++c->plan_clock;
   *out = &c->plans.emplace(key, pp).first->second;
   c->shm->stats.plan_cache_misses++;
   return LAM_OK;
@@ -1280,12 +1330,15 @@ extern "C" lam_status lam_subscribe(lam_ctx* c, int32_t rid, const lam_tp_layout
   }
   for (uint64_t a : tdst)
     if (!a) return LAM_EINVAL;
+  // the pack writes only the shards packed on the rollout's own GPU: every actor rank must be there,
+  // otherwise the rollout would see a partial version (pull the others with lam_pull instead)
+  for (int r = 0; r < c->cfg.fsdp_size; ++r)
+    if (c->cfg.actor_device[r] != ro.device) return LAM_EINVAL;
   Lock l(c->shm);
   lam_ctx::StreamPull& sp = c->streams[rid];
   if (sp.active) return LAM_EBUSY;
   bool any = false;
   for (int r = 0; r < c->cfg.fsdp_size; ++r) {
-    if (c->cfg.actor_device[r] != ro.device) continue;
     RankPub& rp = c->pubs[r];
     if (rp.sub_tensor_dst != tdst) {
       rp.sub_tensor_dst = tdst;
@@ -1337,7 +1390,8 @@ extern "C" lam_status lam_pull(lam_ctx* c, int32_t rid, const lam_tp_layout* L, 
     return LAM_EINVAL;
   }
   cudaEvent_t t0 = prof_begin(c, ro.device, (cudaStream_t)stream);
-  uint32_t* work = pull_counter(c, ro.device);
+  cudaEvent_t wev = nullptr;
+  uint32_t* work = pull_counter(c, ro.device, &wev);
   int rc = work ? launch_pull(pp->d_tiles, pp->n_tiles, rb->second, c->pull_ctas, stream, pp->kinds, work)
                 : (int)cudaErrorMemoryAllocation;
   if (rc) {
@@ -1345,6 +1399,8 @@ extern "C" lam_status lam_pull(lam_ctx* c, int32_t rid, const lam_tp_layout* L, 
     fprintf(stderr, "liblam: pull launch failed: %s\n", cudaGetErrorString((cudaError_t)rc));
     return LAM_ECUDA;
   }
+  CK(cudaEventRecord(wev, (cudaStream_t)stream));
+  CK(cudaEventRecord(pp->last_ev, (cudaStream_t)stream));
   prof_end(c, 2, ro.device, (cudaStream_t)stream, t0);
   cudaEvent_t ev = get_event(c, ro.device);
   CK(cudaEventRecord(ev, (cudaStream_t)stream));
@@ -1555,11 +1611,15 @@ extern "C" void lam_destroy(lam_ctx* c) {
     if (kv.second.side) cudaStreamDestroy(kv.second.side);
   }
   for (auto& kv : c->plans) {
+    cudaSetDevice(kv.second.device);
     cudaFree(kv.second.d_tiles);
+    if (kv.second.last_ev) cudaEventDestroy(kv.second.last_ev);
   }
   for (auto& kv : c->pull_work) {
     cudaSetDevice(kv.first);
     if (kv.second.d) cudaFree(kv.second.d);
+    for (cudaEvent_t e : kv.second.ev)
+      if (e) cudaEventDestroy(e);
   }
   for (auto& kv : c->d_rank_base) {
     cudaSetDevice(kv.first.second);

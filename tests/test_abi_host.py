@@ -148,7 +148,7 @@ def test_config_struct_size_matches_library():
 
 
 @pytest.mark.parametrize("config,tp", [("chain", 0), ("colocated", 0), ("colocated", 2), ("relay-tp", 2),
-                                       ("relay-tp", 1), ("host", 1), ("host", 2)])
+                                       ("relay-tp", 1), ("host", 1), ("host", 2), ("stress", 0)])
 @pytest.mark.parametrize("N", [1, 2, 4, 8])
 def test_bench_placements_are_valid(config, tp, N):
     """bench.py placements at every N the driver's scaling run uses: devices in range, every rollout
@@ -171,7 +171,9 @@ def test_bench_placements_are_valid(config, tp, N):
     ranks = sorted(r for _, _, _, r in T["rollouts"])
     tpr = T["rollouts"][0][2]
     assert ranks == sorted(list(range(tpr)) * (len(ranks) // tpr))
-    if config == "chain":
+    if config == "stress":
+        assert len(T["rollouts"]) == 6                       # BASELINE configs[4]: 6 rollouts
+    if config in ("chain", "stress"):
         P = sum(int(np.prod(s)) for _, s in otensors(OMODELS["7b"]))
         per_gpu = {d: 0 for d in range(N)}
         per_gpu[0] += 4 * P + 2 * 2 * P                      # fp32 masters + 2 master slots
