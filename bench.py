@@ -958,6 +958,11 @@ def main():
         for name, model, config, tp in HEADLINE:
             if config == "relay-tp" and N < 2 or config == "colocated" and N % tp:
                 continue
+            need = hbm_need(topology(config, N, tp), N, P_params(model))
+            if need > 175e9:
+                if rank == 0:
+                    headline[name] = dict(skipped=f"needs {need / 1e9:.0f} GB on one GPU at N={N}")
+                continue
             Q = Placement(args, D, model, config, tp, name)
             r = timed_steps(Q, args.extra_steps, 2, True)
             s = summarize(Q, r, args.extra_steps)
@@ -993,6 +998,21 @@ def main():
         print(json.dumps(out), flush=True)
     D.close()
     return 0
+
+
+def hbm_need(T, N, P):
+    """Largest per-GPU footprint of a placement: fp32 master shards + 2 ring slots of every part a GPU
+    stores + its rollouts' TP buffers (tests/test_abi_host.py checks the same count)."""
+    n = T["fsdp"]
+    per = {d: 0.0 for d in range(N)}
+    for d in T["actors"]:
+        per[d] += 4 * P / n + 2 * (2 * P / n)
+    for node in T["relays"]:
+        for d in node:
+            per[d] += 2 * (2 * P / n)
+    for _, dev, tpr, _ in T["rollouts"]:
+        per[dev] += 2 * P / tpr
+    return max(per.values())
 
 
 def P_params(model):
