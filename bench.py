@@ -68,6 +68,7 @@ def parse(argv=None):
     ap.add_argument("--no-stream-pull", action="store_true", help="same as --stream-pull off")
     ap.add_argument("--no-subscribe", action="store_true",
                     help="colocated rollouts pull after the pack instead of being written by it")
+    ap.add_argument("--slots", type=int, default=0, help="ring slots per node (0: 2, stress: 3)")
     ap.add_argument("--pack-ctas", type=int, default=0)
     ap.add_argument("--pull-ctas", type=int, default=0)
     ap.add_argument("--e2e-steps", type=int, default=2)
@@ -437,9 +438,10 @@ HEADLINE = [
 ]
 
 
-def nvlink_bound(T, N, P):
+def nvlink_bound(T, N, P, pull_in=None):
     """Publish->all lower bound: max over GPUs of the bf16 bytes that must enter (or
-    leave) that GPU over NVLink, / 900 GB/s (the stages pipeline).  Counted from the placement."""
+    leave) that GPU over NVLink, / 900 GB/s (the stages pipeline).  Counted from the placement: chain
+    hops between GPUs, plus `pull_in[d]` = bytes the rollouts on GPU d gather from other GPUs."""
     n = T["fsdp"]
     region = 2.0 * P / n                    # bf16 bytes of one actor rank's region
     ing = {d: 0.0 for d in range(N)}
@@ -451,6 +453,8 @@ def nvlink_bound(T, N, P):
                 ing[d] += region
                 egr[prev[r]] += region
         prev = {r: node[r] for r in range(n)}
+    for d, x in (pull_in or {}).items():
+        ing[d] += x
     return ing, egr
 
 
@@ -528,6 +532,7 @@ class Placement:
                          proc_rank=rank, n_procs=N, proc_of_device={d: d for d in range(N)},
                          shm_name=f"lam_bench_{port}_{os.getppid()}_{tag}", hop_ctas=args.hop_ctas,
                          pack_ctas=args.pack_ctas, pull_ctas=args.pull_ctas,
+                         slots=args.slots or (3 if config == "stress" and N > 1 else 2),
                          hop_mode=lam.LAM_HOP_COPY_ENGINE if args.hop_mode == "ce" else lam.LAM_HOP_KERNEL,
                          host_relays=T.get("host_relays", []))
         self.ctx = ctx = lam.Context(cfg)
@@ -871,7 +876,9 @@ def summarize(P: Placement, res, steps, rank0_extra=None):
                     algorithmic_bytes_per_launch=dom["bytes"], launch_ms=dom["ms"], peak_source=src)
         if dom["bound"] == "nvlink":
             roof["per_link_gbs"] = ach / 18.0       # 18 NVLink 5 links per GPU, 50 GB/s/dir each
-    ing, egr = nvlink_bound(P.T, N, P.info.params)
+    rem = 0.0 if P.config == "host" else float(sum(P.pull_bytes[rid][1] for rid in P.mine))
+    pull_in = {r: x for r, x in enumerate(D.gather(rem))}
+    ing, egr = nvlink_bound(P.T, N, P.info.params, pull_in)
     worst = max(max(ing.values()), max(egr.values()))
     bound_s = worst / (NVL_NOMINAL * 1e9)
     lat = sorted(res["lat"])
@@ -1198,9 +1205,9 @@ def run_e2e(args, P: Placement):
 def run_stress(args, D: Dist):
     """BASELINE configs[4]: the actor publishes every step while 6 rollouts pull staggered versions.
 
-    Actor loop (GPU 0), per step v: the optimizer waits for reads_done of the previous publish, then
-    writes the masters of version v (generator, harness) -> synthetic training step (bf16 GEMM loop of
-    ~stress_ms) -> lam_publish(v).  Every rank drives lam_relay_step; rollout k pulls (lam_pull of the
+    Actor loop (GPU 0), per step v: synthetic forward/backward (bf16 GEMM loop of ~stress_ms, which
+    overlaps the pack of v-1) -> the optimizer waits for reads_done of the previous publish, then writes
+    the masters of version v (generator, harness) -> lam_publish(v).  Every rank drives lam_relay_step; rollout k pulls (lam_pull of the
     newest complete version at its node) at exponential intervals of mean 2 x stress_ms (seed k).
     Reported: publish -> every-node-committed latency per version (the line's value, p50), actor stall
     per publish (host time in lam_publish + actor-stream wait on reads_done), pull latency p50/p99,
@@ -1253,8 +1260,14 @@ def run_stress(args, D: Dist):
             # write of the masters waits (on the stream) for the previous pack's reads_done
             actor_v += 1
             v = actor_v
-            if rd_prev is not None:
-                with torch.cuda.stream(P.actor_stream):
+            A, B, Cc, iters = gemm
+            with torch.cuda.stream(P.actor_stream):    # forward/backward of step v (overlaps pack v-1)
+                for _ in range(iters):
+                    torch.mm(A, B, out=Cc)
+                g_prev = torch.cuda.Event()
+                g_prev.record()
+            if rd_prev is not None:                    # the optimizer may overwrite the masters only
+                with torch.cuda.stream(P.actor_stream):    # once the previous pack has read them
                     w0, w1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                     w0.record()
                     P.actor_stream.wait_event(rd_prev)
@@ -1262,12 +1275,6 @@ def run_stress(args, D: Dist):
                     rd_wait.append((w0, w1))
             for sh in P.shards.values():              # optimizer: new master values (version v)
                 sh.fill(SEED, v, stream=P.actor_stream.cuda_stream)
-            A, B, Cc, iters = gemm
-            with torch.cuda.stream(P.actor_stream):
-                for _ in range(iters):
-                    torch.mm(A, B, out=Cc)
-                g_prev = torch.cuda.Event()
-                g_prev.record()
             rd = live_event(torch)
             t0 = time.perf_counter()
             for r, sh in P.shards.items():

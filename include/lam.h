@@ -358,6 +358,14 @@ void lam_ctl_unpin(lam_ctl*, int32_t node, int32_t slot);
 uint64_t lam_ctl_latest(lam_ctl*, int32_t node);
 int32_t lam_ctl_busy(lam_ctl*);
 lam_status lam_ctl_slot(lam_ctl*, int32_t node, int32_t slot, uint64_t* version, int32_t* state, int32_t* readers);
+/* Heartbeat: stamp process `proc` at now_ns (steady clock); declare dead every other process
+ * whose stamp is older than limit_s and fail (O(1) rebuild) every live relay node with a part in a dead
+ * process — node_procs[node] = bit mask of the processes holding a part of `node` (n_nodes entries).
+ * Returns the bit mask of the nodes failed by this call.  The runtime runs the same function inside every
+ * lam_relay_step (lam_config.heartbeat_timeout_s). */
+uint64_t lam_ctl_heartbeat(lam_ctl*, int32_t proc, int32_t n_procs, uint64_t now_ns, double limit_s,
+                           const uint64_t* node_procs);
+uint64_t lam_ctl_dead_procs(lam_ctl*);                                                  /* bit mask */
 
 /* Appendix D: chunk count k = clamp(round(sqrt((p-2) M T_byte / T_start)),
  * 1, k_cap); and T(p, k) = (p + k - 2)(M/k T_byte + T_start). */

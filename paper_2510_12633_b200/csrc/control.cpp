@@ -309,6 +309,25 @@ bool busy(Shm* sh, int S, int n_nodes) {
   return false;
 }
 
+uint64_t heartbeat(Shm* sh, int S, int proc, int n_procs, uint64_t now_ns, uint64_t limit_ns,
+                   const uint64_t* node_procs, int n_nodes) {
+  uint64_t failed = 0;
+  if (proc >= 0 && proc < LAM_MAX_DEVICES) sh->hb_ns[proc] = now_ns;
+  if (n_procs < 2 || limit_ns == 0) return 0;
+  for (int q = 0; q < n_procs && q < LAM_MAX_DEVICES; ++q) {
+    if (q == proc || (sh->dead_procs >> q & 1ull) || sh->hb_ns[q] == 0) continue;
+    // a stamp newer than now_ns (taken by another process after the caller read its clock) is alive
+    if (sh->hb_ns[q] >= now_ns || now_ns - sh->hb_ns[q] <= limit_ns) continue;
+    sh->dead_procs |= 1ull << q;
+    for (int node = 1; node < n_nodes; ++node)
+      if ((node_procs[node] >> q & 1ull) && !sh->node[node].dead && fail_node(sh, S, node, now_ns)) {
+        sh->stats.chain_rebuilds++;
+        failed |= 1ull << node;
+      }
+  }
+  return failed;
+}
+
 }  // namespace ctl
 }  // namespace lam
 
@@ -412,4 +431,15 @@ extern "C" lam_status lam_ctl_slot(lam_ctl* c, int32_t node, int32_t slot, uint6
   *state = s.state;
   *readers = s.readers;
   return LAM_OK;
+}
+
+extern "C" uint64_t lam_ctl_heartbeat(lam_ctl* c, int32_t proc, int32_t n_procs, uint64_t now_ns, double limit_s,
+                                      const uint64_t* node_procs) {
+  ShmLock l(c->sh);
+  return ctl::heartbeat(c->sh, c->S, proc, n_procs, now_ns, (uint64_t)(limit_s * 1e9), node_procs, c->n_nodes);
+}
+
+extern "C" uint64_t lam_ctl_dead_procs(lam_ctl* c) {
+  ShmLock l(c->sh);
+  return c->sh->dead_procs;
 }

@@ -97,6 +97,13 @@ void init(Shm* sh, int n_nodes);
 // abandoned and the successor starts over with the newest the new predecessor holds.
 // Returns false if the node is node 0 (the actor's slots: trainer failure, out of scope) or dead.
 bool fail_node(Shm* sh, int S, int node, uint64_t now_ns);
+// Heartbeats ("detects the failure via heartbeat monitoring"): stamp process `proc` at
+// now_ns; every other process whose last stamp is older than limit_ns is declared dead (once), and
+// every live relay node with a part in a dead process (bit q of node_procs[node] = process q holds a
+// part of it) fails through fail_node (O(1) rebuild each).  Processes that never stamped are not
+// judged.  Returns the bit mask of the nodes this call failed.
+uint64_t heartbeat(Shm* sh, int S, int proc, int n_procs, uint64_t now_ns, uint64_t limit_ns,
+                   const uint64_t* node_procs, int n_nodes);
 }  // namespace ctl
 
 }  // namespace lam

@@ -541,11 +541,18 @@ lam_status stream_wait_flag(lam_ctx* c, cudaStream_t st, const uint64_t* flag, u
   return LAM_OK;
 }
 
-// Enqueue the next chunks of the part's copy-engine hop, at most kCeWindow ahead of the copies
-// that completed: enqueueing hundreds of flag waits at once can block the host thread (full push
-// buffer) while it holds the cross-process lock — the predecessor's process could then never
-// launch the work those waits need.  lam_relay_step tops the window up.
+// Enqueue the next chunks of the part's copy-engine hop.  Gating, in order of preference:
+//  * host mirror (the producers mirror every chunk flag into the shared control block): a chunk is
+//    enqueued only once the predecessor verified it (or poisoned it: the copy is then made and
+//    k_verify fails it, which propagates the failure down the chain), so the copy stream holds
+//    nothing but copies — no wait kernel that a busy GPU (e.g. a streaming pull filling every SM)
+//    could delay, and the copy engines run back to back while the chain is flowing;
+//  * otherwise a device-side wait per chunk (stream memory op / one-thread polling kernel), at most
+//    kCeWindow chunks ahead of the copies that completed: enqueueing hundreds of flag waits at once
+//    can block the host thread (full push buffer) while it holds the cross-process lock.
+// lam_relay_step tops the queue up.
 constexpr uint32_t kCeWindow = 8;
+constexpr uint32_t kCeMirrorWindow = 24;   // copies in flight when gated by the mirror
 
 lam_status ce_topup(lam_ctx* c, Part& p) {
   if (!p.ce_version) return LAM_OK;
@@ -559,20 +566,28 @@ lam_status ce_topup(lam_ctx* c, Part& p) {
       p.ce_next = n;
       break;
     }
-    if (i >= kCeWindow) {
-      cudaError_t q = cudaEventQuery(p.chunk_ev[i - kCeWindow]);
+    const uint32_t g = p.my_chunks[i];
+    const uint64_t* mir = c->mirror_dev ? c->shm->chunk_done[p.node - 1][ps] : nullptr;
+    const uint32_t window = mir ? kCeMirrorWindow : kCeWindow;
+    if (i >= window) {
+      cudaError_t q = cudaEventQuery(p.chunk_ev[i - window]);
       if (q == cudaErrorNotReady) return LAM_OK;
       if (q != cudaSuccess) return LAM_ECUDA;
     }
-    const uint32_t g = p.my_chunks[i];
+    if (mir) {
+      const uint64_t f = __atomic_load_n(mir + g, __ATOMIC_ACQUIRE);
+      if (f != u && f != (u | kPoison)) return LAM_OK;   // not verified at the predecessor yet
+    }
     const int r = (int)c->plan.chunk_rank[g];
     const Part& q = c->parts[c->node_rank_part[p.node - 1][r]];
     ChunkMeta qm = meta_of(c, q, ps);
     const uint64_t off = (g - c->plan.chunk_base[r]) * c->plan.C, len = c->plan.chunk_len(g);
     const uint8_t* src = slot_data(q, ps) + q.rank_off[r] + off;
     uint8_t* dst = slot_data(p, s) + p.rank_off[r] + off;
-    lam_status st = stream_wait_flag(c, p.stream, qm.flags + g, u, m.abort_flag);
-    if (st != LAM_OK) return st;
+    if (!mir) {
+      lam_status st = stream_wait_flag(c, p.stream, qm.flags + g, u, m.abort_flag);
+      if (st != LAM_OK) return st;
+    }
     CK(cudaMemcpyAsync(dst, src, len, cudaMemcpyDefault, p.stream));
     CK(cudaEventRecord(p.chunk_ev[i], p.stream));
     CK(cudaStreamWaitEvent(p.vstream, p.chunk_ev[i], 0));
@@ -647,11 +662,9 @@ uint64_t steady_ns() {
   return (uint64_t)ts.tv_sec * 1000000000ull + (uint64_t)ts.tv_nsec;
 }
 
-// A node failed: rebuild the chain (control plane) and stop this process's kernels of the dead
-// node (a simulated failure keeps its memory alive; nothing reads it after the rebuild).
-lam_status fail_node_locked(lam_ctx* c, int node) {
-  if (!ctl::fail_node(c->shm, c->S, node, steady_ns())) return LAM_EINVAL;
-  c->shm->stats.chain_rebuilds++;
+// Stop this process's kernels of a failed node (a simulated failure keeps its memory alive; nothing
+// reads it after the rebuild).
+lam_status abort_node_locked(lam_ctx* c, int node) {
   for (Part& p : c->parts) {
     if (!p.local || p.node != node) continue;
     CK(cudaSetDevice(p.device));
@@ -665,26 +678,27 @@ lam_status fail_node_locked(lam_ctx* c, int node) {
   return LAM_OK;
 }
 
+// A node failed: rebuild the chain (control plane), then stop this process's kernels of that node.
+lam_status fail_node_locked(lam_ctx* c, int node) {
+  if (!ctl::fail_node(c->shm, c->S, node, steady_ns())) return LAM_EINVAL;
+  c->shm->stats.chain_rebuilds++;
+  return abort_node_locked(c, node);
+}
+
 // Heartbeats ("detects the failure via heartbeat monitoring"): every lam_relay_step
 // stamps this process; a process silent for longer than heartbeat_timeout_s is declared failed and
-// every relay node with a part on its GPUs is removed from the chain.
+// every relay node with a part on its GPUs is removed from the chain (ctl::heartbeat, O(1) each).
 lam_status heartbeat_locked(lam_ctx* c) {
-  Shm* sh = c->shm;
-  const uint64_t now = steady_ns();
-  sh->hb_ns[c->cfg.proc_rank] = now;
-  if (c->cfg.n_procs < 2 || c->cfg.heartbeat_timeout_s <= 0) return LAM_OK;
-  const uint64_t limit = (uint64_t)(c->cfg.heartbeat_timeout_s * 1e9);
-  for (int q = 0; q < c->cfg.n_procs; ++q) {
-    if (q == c->cfg.proc_rank || (sh->dead_procs >> q & 1ull) || sh->hb_ns[q] == 0) continue;
-    if (now - sh->hb_ns[q] <= limit) continue;
-    sh->dead_procs |= 1ull << q;
-    for (int node = 1; node < c->n_nodes; ++node)
-      for (int pi : c->node_parts[node])
-        if (c->cfg.proc_of_device[c->parts[pi].device] == q && !sh->node[node].dead) {
-          lam_status st = fail_node_locked(c, node);
-          if (st != LAM_OK) return st;
-        }
-  }
+  std::vector<uint64_t> node_procs(c->n_nodes, 0);
+  for (const Part& p : c->parts) node_procs[p.node] |= 1ull << c->cfg.proc_of_device[p.device];
+  const uint64_t limit = c->cfg.heartbeat_timeout_s > 0 ? (uint64_t)(c->cfg.heartbeat_timeout_s * 1e9) : 0;
+  const uint64_t failed = ctl::heartbeat(c->shm, c->S, c->cfg.proc_rank, c->cfg.n_procs, steady_ns(), limit,
+                                         node_procs.data(), c->n_nodes);
+  for (int node = 1; node < c->n_nodes; ++node)
+    if (failed >> node & 1ull) {
+      lam_status st = abort_node_locked(c, node);
+      if (st != LAM_OK) return st;
+    }
   return LAM_OK;
 }
 

@@ -463,7 +463,9 @@ class Ctl:
                               ("lam_ctl_pin", U64, [V, I32, P(I32)]), ("lam_ctl_unpin", None, [V, I32, I32]),
                               ("lam_ctl_latest", U64, [V, I32]), ("lam_ctl_busy", I32, [V]),
                               ("lam_ctl_fail", I32, [V, I32]), ("lam_ctl_pred", I32, [V, I32]),
-                              ("lam_ctl_slot", I32, [V, I32, I32, P(U64), P(I32), P(I32)])]:
+                              ("lam_ctl_slot", I32, [V, I32, I32, P(U64), P(I32), P(I32)]),
+                              ("lam_ctl_heartbeat", U64, [V, I32, I32, U64, C.c_double, P(U64)]),
+                              ("lam_ctl_dead_procs", U64, [V])]:
             f = getattr(L, fn)
             f.restype, f.argtypes = res, args
         self.h = L.lam_ctl_open(name.encode(), int(create), n_nodes, slots, fsdp)
@@ -510,6 +512,14 @@ class Ctl:
         v, st, rd = C.c_uint64(), C.c_int32(), C.c_int32()
         self.L.lam_ctl_slot(self.h, node, slot, C.byref(v), C.byref(st), C.byref(rd))
         return v.value, st.value, rd.value
+
+    def heartbeat(self, proc: int, n_procs: int, now_ns: int, limit_s: float, node_procs: list[int]) -> int:
+        """Stamp `proc`; fail relay nodes of processes silent > limit_s.  Returns the failed-node mask."""
+        arr = (C.c_uint64 * max(1, len(node_procs)))(*node_procs)
+        return self.L.lam_ctl_heartbeat(self.h, proc, n_procs, now_ns, limit_s, arr)
+
+    def dead_procs(self) -> int:
+        return self.L.lam_ctl_dead_procs(self.h)
 
     def close(self) -> None:
         if self.h:

@@ -236,3 +236,68 @@ def test_two_processes_share_the_version_table():
     assert errs == [], errs
     published = next(r[1] for r in results if r[0] == "published")
     assert published == list(range(1, versions + 1))
+
+
+# ------------------------------------------------------------------ NEXT-1: a relay process dies
+def _hb_worker(proc, n_procs, name, limit_s, node_procs, q, stop):
+    """One rank process: stamps its heartbeat every 5 ms through lam_ctl_heartbeat (what every
+    lam_relay_step does) and reports the nodes it saw failing and when (steady clock), until `stop`."""
+    import time as _t
+    c = lam.Ctl(name, False, len(node_procs), 2, 1)
+    seen = 0
+    c.heartbeat(proc, n_procs, _t.monotonic_ns(), limit_s, node_procs)
+    q.put((proc, "ready"))
+    while not stop.is_set():
+        failed = c.heartbeat(proc, n_procs, _t.monotonic_ns(), limit_s, node_procs)
+        if failed:
+            seen |= failed
+            q.put((proc, "failed", failed, _t.monotonic_ns(), [c.pred(n) for n in range(len(node_procs))]))
+        _t.sleep(0.005)
+    q.put((proc, "done", seen, c.dead_procs(), [c.pred(n) for n in range(len(node_procs))]))
+    c.close()
+
+
+def test_sigkill_of_a_relay_process_is_detected_by_heartbeat_and_the_chain_rebuilt():
+    """"the rollout manager detects the failure via heartbeat monitoring and immediately
+    reconstructs the broadcast chain ... a constant-time (O(1)) operation".  Four rank processes own
+    node k (node 0 = the actor's slots on process 0, relays 1..3 on processes 1..3); process 2 is
+    SIGKILLed.  The survivors' heartbeats must declare it dead within the limit (+ one period), fail
+    exactly node 2 once, and relink node 3 to node 1; detection well under the paper's one second."""
+    import signal
+    import time as _t
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    name = f"lam_hb_test_{os.getpid()}"
+    n = 4
+    node_procs = [1 << k for k in range(n)]            # node k lives on process k
+    owner = lam.Ctl(name, True, n, 2, 1)
+    limit = 0.5
+    stop = ctx.Event()
+    procs = [ctx.Process(target=_hb_worker, args=(k, n, name, limit, node_procs, q, stop)) for k in range(n)]
+    for pr in procs:
+        pr.start()
+    ready = [q.get(timeout=120) for _ in range(n)]     # every process stamped (spawn + import done)
+    assert sorted(m[0] for m in ready) == list(range(n)) and all(m[1] == "ready" for m in ready)
+    _t.sleep(0.5)
+    kill_ns = _t.monotonic_ns()
+    os.kill(procs[2].pid, signal.SIGKILL)
+    procs[2].join(timeout=10)
+    _t.sleep(1.5)                                      # 3 x the limit: detection must have happened
+    stop.set()
+    msgs = []
+    t0 = _t.time()
+    while sum(1 for m in msgs if m[1] == "done") < n - 1 and _t.time() - t0 < 60:
+        msgs.append(q.get(timeout=60))
+    for k in (0, 1, 3):
+        procs[k].join(timeout=30)
+    fails = [m for m in msgs if m[1] == "failed"]
+    assert len(fails) == 1, fails                      # node 2 failed once, by whichever survivor saw it first
+    proc, _, mask, t_ns, preds = fails[0]
+    assert proc != 2 and mask == 1 << 2
+    detect_s = (t_ns - kill_ns) / 1e9
+    assert limit - 0.05 <= detect_s < 1.0, detect_s    # "less than one second" (PAPER L697)
+    assert preds[3] == 1 and preds[2] == -1 and preds[1] == 0
+    done = [m for m in msgs if m[1] == "done"]
+    assert all(m[3] == 1 << 2 for m in done)           # every survivor sees process 2 (only) as dead
+    assert owner.pred(3) == 1
+    owner.close()

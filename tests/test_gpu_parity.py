@@ -330,9 +330,31 @@ def test_corrupt_chunk_is_never_committed(hop_mode):
 
 
 # ------------------------------------------------------------------------- 7B (bench config)
-def test_7b_single_gpu_sampled():
-    """The bench workload at full size on one GPU: sampled chunks vs the oracle, all chunk
-    checksums self-consistent, sampled TP=1 elements of every destination vs the oracle."""
+_HDR = None
+
+
+def _oracle_header(g):
+    from oracle.checksum import chunk_checksum
+    plan, v = _HDR
+    want = publish_chunk(plan, g, SEED, v)
+    return chunk_checksum(want), want.size
+
+
+def oracle_headers(plan, v):
+    """(S1, S2) and byte length of every chunk of IMG(v), computed by the oracle on a fork pool
+    (publish_chunk + chunk_checksum per chunk, all host cores)."""
+    import multiprocessing as mp
+    import os
+    global _HDR
+    _HDR = (plan, v)
+    with mp.get_context("fork").Pool(os.cpu_count() or 1) as pool:
+        return pool.map(_oracle_header, range(plan.total_chunks), chunksize=1)
+
+
+def test_7b_single_gpu_all_headers_sampled_elements():
+    """The bench workload at full size on one GPU: EVERY chunk header (all 227 of the 64 MiB chunks:
+    version, index, length, S1, S2) == the oracle's, the bytes of 3 whole chunks == the oracle's, and
+    sampled TP=1 elements of every destination == the oracle's (element by element)."""
     od = OMODELS["7b"]
     ctx = make_ctx("7b", 1, [0], [], [(0, 0)], C=64 << 20)
     info = ctx.plan_info()
@@ -341,15 +363,16 @@ def test_7b_single_gpu_sampled():
     publish_all(ctx, [shard], 3, False)
     until_idle(ctx)
     plan = image_plan([s for _, s in otensors(od)], 1, C)
-    assert plan.total_chunks == info.total_chunks
+    assert plan.total_chunks == info.total_chunks == 227
     hdr = ctx.read_headers(0, 3)
+    want_hdr = oracle_headers(plan, 3)
+    for g, ((s12, n), h) in enumerate(zip(want_hdr, hdr)):
+        assert (h["s1"], h["s2"]) == s12 and h["bytes"] == n, g
+        assert h["version"] == 3 and h["idx"] == g and h["n"] == plan.total_chunks, (g, h)
     for g in sorted({0, plan.total_chunks // 2, plan.total_chunks - 1}):
         want = publish_chunk(plan, g, SEED, 3)
         got = ctx.read_image(0, 3, g * C, want.size)
         assert np.array_equal(got, want), g
-        from oracle.checksum import chunk_checksum
-        assert (hdr[g]["s1"], hdr[g]["s2"]) == chunk_checksum(want)
-        assert hdr[g]["bytes"] == want.size and hdr[g]["version"] == 3
     del shard
     torch.cuda.empty_cache()
     rb = RolloutBuffers(MODELS["7b"], 1, 0, 0)
