@@ -70,6 +70,7 @@ def parse(argv=None):
                     help="colocated rollouts pull after the pack instead of being written by it")
     ap.add_argument("--slots", type=int, default=0, help="ring slots per node (0: 2, stress: 3)")
     ap.add_argument("--pack-ctas", type=int, default=0)
+    ap.add_argument("--pack-sms", type=int, default=0, help="confine the pack to this many SMs (0 = all)")
     ap.add_argument("--pull-ctas", type=int, default=0)
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
@@ -531,7 +532,7 @@ class Placement:
                          rollouts=[(n, d) for n, d, _, _ in self.rollouts], chunk_bytes=args.chunk_mb << 20,
                          proc_rank=rank, n_procs=N, proc_of_device={d: d for d in range(N)},
                          shm_name=f"lam_bench_{port}_{os.getppid()}_{tag}", hop_ctas=args.hop_ctas,
-                         pack_ctas=args.pack_ctas, pull_ctas=args.pull_ctas,
+                         pack_ctas=args.pack_ctas, pull_ctas=args.pull_ctas, pack_sms=args.pack_sms,
                          slots=args.slots or (3 if config == "stress" and N > 1 else 2),
                          hop_mode=lam.LAM_HOP_COPY_ENGINE if args.hop_mode == "ce" else lam.LAM_HOP_KERNEL,
                          host_relays=T.get("host_relays", []))
@@ -554,6 +555,7 @@ class Placement:
                      for rid in self.mine}
         self.pull_bytes = {rid: ctx.pull_bytes(rid, self.bufs[rid].tp) for rid in self.mine}
         self.stream = torch.cuda.Stream()
+        self.rstream = {rid: torch.cuda.Stream() for rid in self.mine}   # one engine stream per rollout
         self.actor_stream = torch.cuda.Stream()
         torch.cuda.synchronize()
         self.v = 0
@@ -843,8 +845,8 @@ def summarize(P: Placement, res, steps, rank0_extra=None):
     D = P.D
     N = P.N
     ms_max = D.max(res["ms"])
-    launches = sum(n for _, n in res["kt"].values())
-    launches_all = int(D.sum(launches))
+    # every kernel liblam launched in the timed region (the stats block is shared by all ranks)
+    launches_all = int(res["st1"]["kernel_launches"] - res["st0"]["kernel_launches"])
     avg, cand = roofline_of(P, res["kt"], steps)
     mine_info = dict(rank=P.rank, ms=round(res["ms"], 3), **{k: (round(v, 3) if v else None) for k, v in avg.items()},
                      cand=cand)
@@ -950,9 +952,15 @@ def main():
         stall = actor_stall(P)
     pub_timed = sorted(P.pub_host[:args.steps]) if P.pub_host else []
     if stall is not None or pub_timed:
+        s0, s1 = res["st0"], res["st1"]
+        npub = max(1, s1["publishes"] - s0["publishes"])
         stall = dict(stall or {}, publish_host_us=dict(
             p50=round(pub_timed[len(pub_timed) // 2] * 1e6, 1) if pub_timed else None,
-            max=round(pub_timed[-1] * 1e6, 1) if pub_timed else None, n=len(pub_timed)))
+            max=round(pub_timed[-1] * 1e6, 1) if pub_timed else None, n=len(pub_timed),
+            what="Python caller: ctypes marshalling + lam_publish"),
+            publish_lib_us=dict(mean=round((s1["publish_ns_total"] - s0["publish_ns_total"]) / npub / 1e3, 1),
+                                max_since_start=round(s1["publish_ns_max"] / 1e3, 1),
+                                what="inside lam_publish (steady clock, library stats)"))
     cpu = None
     if rank == 0 and N == 1 and not args.quick and not args.no_cpu_baseline:
         cpu = cpu_baseline(args, P)
@@ -1066,7 +1074,7 @@ def cpu_baseline(args, P: Placement):
     return res
 
 
-def actor_stall(P: Placement, reps=5, target_ms=25.0):
+def actor_stall(P: Placement, reps=5, target_ms=25.0, sms_list=(0, 24, 40, 56, 74)):
     """Actor stall per publish, the trainer's view of step 5 ("pushes the new
     actor weights to the master relay and immediately resumes its next training iteration"):
       reads_done_wait_ms  actor-stream wait on reads_done before the next optimizer step, when that step
@@ -1074,7 +1082,9 @@ def actor_stall(P: Placement, reps=5, target_ms=25.0):
       inflation_ms        that training step's slowdown from the concurrent pack (SM / HBM contention,
                           PAPER L401-402): synthetic step = a bf16 GEMM loop of ~target_ms on the actor
                           stream (torch/cuBLAS: it stands in for the trainer, it is not the path).
-    Pack-only publishes (no subscriber), each committed before the next; medians over `reps`."""
+    Pack-only publishes (no subscriber), each committed before the next; medians over `reps`.
+    pack_sms_sweep: the same with the pack confined to k SMs (lam_set_pack_sms), trading pack time for
+    trainer SMs; the line's own numbers use --pack-sms."""
     torch, ctx, lam = P.torch, P.ctx, P.lam
     actor_stream = P.actor_stream
     n = 8192
@@ -1098,7 +1108,7 @@ def actor_stall(P: Placement, reps=5, target_ms=25.0):
             for _ in range(iters):
                 torch.mm(a, b, out=c)
 
-    alone, total, wait, busy = [], [], [], []
+    alone = []
     for _ in range(reps):
         with torch.cuda.stream(actor_stream):
             s0, s1 = ev(), ev()
@@ -1108,6 +1118,29 @@ def actor_stall(P: Placement, reps=5, target_ms=25.0):
             s1.record()
         s1.synchronize()
         alone.append(s0.elapsed_time(s1))
+    med = lambda x: sorted(x)[len(x) // 2]
+    sweep = []
+    for sms in sms_list:                               # pack confined to `sms` SMs (0 = all)
+        ctx.set_pack_sms(sms)
+        r = _stall_reps(P, reps, train_step, ev)
+        sweep.append(dict(pack_sms=sms, inflation_ms=round(r[0] - med(alone), 3), masters_busy_ms=round(r[2], 3),
+                          reads_done_wait_ms=round(r[1], 4)))
+    ctx.set_pack_sms(P.args.pack_sms)
+    tot, wt, bz = _stall_reps(P, reps, train_step, ev)
+    del a, b, c
+    return dict(step_ms_alone=round(med(alone), 3), step_ms_with_publish=round(tot, 3),
+                inflation_ms=round(tot - med(alone), 3),
+                inflation_frac=round(tot / med(alone) - 1, 4),
+                reads_done_wait_ms=round(wt, 4), masters_busy_ms=round(bz, 3), pack_sms=P.args.pack_sms,
+                pack_sms_sweep=sweep,
+                actor_step=f"bf16 GEMM {n}^3 x {iters} on the actor stream (~{target_ms:.0f} ms)", reps=reps)
+
+
+def _stall_reps(P, reps, train_step, ev):
+    """Medians over `reps` of (step time with a concurrent publish, reads_done wait, pack duration)."""
+    torch, ctx, lam = P.torch, P.ctx, P.lam
+    actor_stream = P.actor_stream
+    total, wait, busy = [], [], []
     for _ in range(reps):
         P.v += 1
         v = P.v
@@ -1131,12 +1164,7 @@ def actor_stall(P: Placement, reps=5, target_ms=25.0):
         wait.append(t_mid.elapsed_time(t1))
         busy.append(max(t0.elapsed_time(e) for e in rd.values()))
     med = lambda x: sorted(x)[len(x) // 2]
-    del a, b, c
-    return dict(step_ms_alone=round(med(alone), 3), step_ms_with_publish=round(med(total), 3),
-                inflation_ms=round(med(total) - med(alone), 3),
-                inflation_frac=round(med(total) / med(alone) - 1, 4),
-                reads_done_wait_ms=round(med(wait), 4), masters_busy_ms=round(med(busy), 3),
-                actor_step=f"bf16 GEMM {n}^3 x {iters} on the actor stream (~{target_ms:.0f} ms)", reps=reps)
+    return med(total), med(wait), med(busy)
 
 
 def measure_pcie(torch):
@@ -1310,10 +1338,10 @@ def run_stress(args, D: Dist):
             elif time.time() >= next_pull[rid]:
                 lat0 = ctx.latest(node)
                 tc = time.time()
-                v = ctx.pull(rid, P.bufs[rid].tp, P.stream.cuda_stream)
+                v = ctx.pull(rid, P.bufs[rid].tp, P.rstream[rid].cuda_stream)
                 if v:
                     ev = torch.cuda.Event()
-                    ev.record(P.stream)
+                    ev.record(P.rstream[rid])
                     inflight[rid] = (v, ev, tc, lat0)
                 next_pull[rid] = time.time() + rng[rid].exponential(mean_s)
         if (actor_v >= steps or not P.my_ranks) and not inflight and ctx.latest(0) >= steps and \

@@ -132,6 +132,9 @@ typedef struct {
   int32_t hop_mode;                        /* LAM_HOP_KERNEL (default) | LAM_HOP_COPY_ENGINE */
   double heartbeat_timeout_s;              /* n_procs > 1: a process silent this long is declared
                                               failed and its relay nodes leave the chain (0 = off) */
+  int32_t pack_sms;                        /* > 0: the pack runs on SMs 0..pack_sms-1 only (every SM
+                                              fully occupied), leaving the others to the trainer's
+                                              kernels (actor stall); 0 = all SMs */
 } lam_config;
 
 /* How a relay moves a chunk from its predecessor (both receiver-driven, chunk-pipelined, verified):
@@ -194,6 +197,10 @@ typedef struct {
   uint64_t chain_rebuilds;   /* relay failures handled (lam_fail_node or heartbeat timeout) */
   uint64_t chain_resumes;    /* hops restarted from a new predecessor, from the lowest missing chunk */
   uint64_t last_repair_ns;   /* failure declared -> successor's resumed hop launched (steady clock) */
+  uint64_t kernel_launches;  /* every kernel this library launched (pack, hop, verify, flag wait, pull) */
+  uint64_t publish_ns_total, publish_ns_max;  /* host time inside lam_publish (entry -> return, steady
+                                                 clock), summed / largest over successful calls: the
+                                                 actor's own stall per publish */
 } lam_stats;
 
 /* ---- lifecycle ------------------------------------------------------------------------- */
@@ -291,6 +298,8 @@ lam_status lam_read_headers(lam_ctx*, int32_t node, uint64_t version, lam_chunk_
  * kind (0 = pack, 1 = hop, 2 = pull), the summed device milliseconds and launch count of launches
  * that completed since the last call, and resets them. */
 lam_status lam_set_profiling(lam_ctx*, int32_t on);
+/* Change lam_config.pack_sms for later publishes (0 = all SMs). */
+lam_status lam_set_pack_sms(lam_ctx*, int32_t sms);
 lam_status lam_kernel_times(lam_ctx*, double ms_out[3], uint64_t count_out[3]);
 
 /* Bytes a pull of `layout` at rollout `rollout_id` reads from the rollout's own GPU's HBM (local) and

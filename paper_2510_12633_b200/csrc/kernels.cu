@@ -151,9 +151,22 @@ __global__ void __launch_bounds__(kPackThreads) k_pack(const PackUnit* __restric
                                                        uint64_t version, uint64_t n_total,
                                                        const uint64_t* __restrict__ chunk_len,
                                                        uint8_t* const* __restrict__ sub_dst,
-                                                       uint32_t* __restrict__ work) {
+                                                       uint32_t* __restrict__ work, uint32_t sms) {
   __shared__ uint64_t red[2][kPackThreads / 32];
   __shared__ uint32_t s_next;
+  // SM confinement (lam_config.pack_sms): the grid is one full wave over every SM; CTAs that landed on
+  // an SM outside [0, sms) leave at once, so the pack holds only `sms` SMs (fully occupied) and the
+  // trainer's kernels keep the rest.  Every unit then comes from the work counter.
+  uint32_t first = blockIdx.x;
+  if (sms) {
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    if (smid >= sms) return;
+    if (threadIdx.x == 0) s_next = atomicAdd(work, 1u);
+    __syncthreads();
+    first = s_next;
+    __syncthreads();
+  }
   // Dynamic unit distribution: a CTA's first unit is blockIdx.x, every further one comes from a work
   // counter (zeroed before the launch), fetched at the start of the current unit so its latency is
   // hidden.  The static round-robin left ncu's per-SM active cycles at min 14.4 M / avg 17.9 M / max
@@ -164,8 +177,9 @@ __global__ void __launch_bounds__(kPackThreads) k_pack(const PackUnit* __restric
   // on a handful of hot header addresses serialised in L2.
   uint32_t cur = 0xFFFFFFFFu, acc_n = 0;
   uint64_t acc1 = 0, acc2 = 0;
-  for (uint32_t ui = blockIdx.x; ui < n_units;) {
-    if (threadIdx.x == 0) s_next = gridDim.x + atomicAdd(work, 1u);   // read after the barriers below
+  const uint32_t base = sms ? 0u : gridDim.x;   // unconfined: units [0, grid) are the CTAs' first ones
+  for (uint32_t ui = first; ui < n_units;) {
+    if (threadIdx.x == 0) s_next = base + atomicAdd(work, 1u);   // read after the barriers below
     const PackUnit u = units[ui];
     if (u.chunk != cur) {                                   // uniform: every thread read the same unit
       if (cur != 0xFFFFFFFFu) {
@@ -252,18 +266,23 @@ __global__ void __launch_bounds__(kPackThreads) k_pack(const PackUnit* __restric
 
 int launch_pack(const PackUnit* units, uint32_t n_units, const float* const* shard_ptrs, uint8_t* dst,
                 ChunkMeta meta, const uint32_t* units_per_chunk, uint64_t version, uint64_t n_total,
-                const uint64_t* chunk_len, int ctas, void* stream, uint8_t* const* sub_dst, uint32_t* work) {
+                const uint64_t* chunk_len, int ctas, void* stream, uint8_t* const* sub_dst, uint32_t* work,
+                int sms) {
   if (n_units == 0) return 0;
   cudaError_t e = cudaMemsetAsync(work, 0, sizeof(uint32_t), (cudaStream_t)stream);
   if (e != cudaSuccess) return (int)e;
-  if (ctas <= 0) ctas = sub_dst ? resident_ctas(k_pack<true>, kPackThreads) : resident_ctas(k_pack<false>, kPackThreads);
-  unsigned grid = (unsigned)(n_units < (uint32_t)ctas ? n_units : (uint32_t)ctas);
+  if (ctas <= 0 || sms > 0)
+    ctas = sub_dst ? resident_ctas(k_pack<true>, kPackThreads) : resident_ctas(k_pack<false>, kPackThreads);
+  // confined: the full wave must land everywhere (the CTAs on SMs >= sms leave), not n_units of it
+  unsigned grid = (unsigned)(sms > 0 || n_units >= (uint32_t)ctas ? (uint32_t)ctas : n_units);
   if (sub_dst)
     k_pack<true><<<grid, kPackThreads, 0, (cudaStream_t)stream>>>(units, n_units, shard_ptrs, dst, meta,
-                                                                  units_per_chunk, version, n_total, chunk_len, sub_dst, work);
+                                                                  units_per_chunk, version, n_total, chunk_len, sub_dst, work,
+                                                                  (uint32_t)(sms > 0 ? sms : 0));
   else
     k_pack<false><<<grid, kPackThreads, 0, (cudaStream_t)stream>>>(units, n_units, shard_ptrs, dst, meta,
-                                                                   units_per_chunk, version, n_total, chunk_len, nullptr, work);
+                                                                   units_per_chunk, version, n_total, chunk_len, nullptr, work,
+                                                                   (uint32_t)(sms > 0 ? sms : 0));
   return (int)cudaGetLastError();
 }
 

@@ -133,7 +133,8 @@ constexpr uint32_t kMirrorChunks = 2048;  // chunks per slot mirrored to the hos
 
 int launch_pack(const PackUnit* units, uint32_t n_units, const float* const* shard_ptrs, uint8_t* dst,
                 ChunkMeta meta, const uint32_t* units_per_chunk, uint64_t version, uint64_t n_total,
-                const uint64_t* chunk_len, int ctas, void* stream, uint8_t* const* sub_dst, uint32_t* work);
+                const uint64_t* chunk_len, int ctas, void* stream, uint8_t* const* sub_dst, uint32_t* work,
+                int sms = 0);   // sms > 0: only CTAs on SMs [0, sms) work (the rest exit at once)
 int launch_hop(const HopTile* tiles, uint32_t n_tiles, const RankLink* links, ChunkMeta meta,
                const uint32_t* tiles_per_chunk, uint64_t version, uint32_t* err_word,
                uint64_t timeout_ns, int ctas, void* stream);

@@ -158,7 +158,7 @@ struct lam_ctx {
   bool connected = false;
   lam_status pending_error = LAM_OK;
   uint64_t timeout_ns = 60ull * 1000000000ull;
-  int pack_ctas = 0, hop_ctas = 0, pull_ctas = 0;
+  int pack_ctas = 0, hop_ctas = 0, pull_ctas = 0, pack_sms = 0;
   uint64_t* mirror_dev = nullptr;     // device view of shm->chunk_done (null: no streaming pulls)
   bool shm_registered = false;
   struct StreamPull {                 // lam_pull_stream in progress (per rollout)
@@ -538,6 +538,7 @@ lam_status stream_wait_flag(lam_ctx* c, cudaStream_t st, const uint64_t* flag, u
   if (fn && fn((void*)st, (unsigned long long)(uintptr_t)flag, v, 0x0 /*CU_STREAM_WAIT_VALUE_GEQ*/) == 0)
     return LAM_OK;
   if (launch_wait_flag(flag, v, c->timeout_ns, abort_flag, st)) return LAM_ECUDA;
+  c->shm->stats.kernel_launches++;
   return LAM_OK;
 }
 
@@ -593,6 +594,7 @@ lam_status ce_topup(lam_ctx* c, Part& p) {
     CK(cudaStreamWaitEvent(p.vstream, p.chunk_ev[i], 0));
     if (launch_verify(dst, g, len, qm.flags, qm.hdr, m, u, p.err_dev + s, p.d_my_chunks, i, n, 32, p.vstream))
       return LAM_ECUDA;
+    c->shm->stats.kernel_launches++;
   }
   // all chunks enqueued: join the verify stream, close the timing bracket, arm completion polling
   CK(cudaEventRecord(p.chunk_ev.back(), p.vstream));
@@ -782,6 +784,7 @@ lam_status launch_hop_part(lam_ctx* c, Part& p, int s, bool* launched) {
       fprintf(stderr, "liblam: hop launch failed: %s\n", cudaGetErrorString((cudaError_t)rc));
       return LAM_ECUDA;
     }
+    if (n_tiles) c->shm->stats.kernel_launches++;
   }
   prof_end(c, 1, p.device, p.stream, t0);
   CK(cudaEventRecord(p.done_ev[s], p.stream));
@@ -826,6 +829,7 @@ lam_status stream_progress(lam_ctx* c, int rid, int* transitions) {
       if (!work) return LAM_ENOMEM;
       if (launch_pull(sp.plan->d_tiles + b, e - b, rb->second, c->pull_ctas, sp.stream, sp.plan->kinds, work))
         return LAM_ECUDA;
+      c->shm->stats.kernel_launches += __builtin_popcount(sp.plan->kinds);
       CK(cudaEventRecord(wev, sp.stream));
       CK(cudaEventRecord(sp.plan->last_ev, sp.stream));
       prof_end(c, 2, sp.device, sp.stream, t0);
@@ -1087,6 +1091,7 @@ extern "C" lam_status lam_init(const lam_config* cfg, lam_ctx** out) {
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   c->pack_ctas = cfg->pack_ctas > 0 ? cfg->pack_ctas : 0;  // 0: one resident wave (occupancy API)
+  c->pack_sms = cfg->pack_sms > 0 && cfg->pack_sms < sms ? cfg->pack_sms : 0;
   c->hop_ctas = cfg->hop_ctas > 0 ? cfg->hop_ctas : 32;  // TMA hop: ~785 GB/s at 32 CTAs
   c->pull_ctas = cfg->pull_ctas > 0 ? cfg->pull_ctas : 0;
   if (cfg->spin_timeout_s > 0) c->timeout_ns = (uint64_t)(cfg->spin_timeout_s * 1e9);
@@ -1207,8 +1212,24 @@ extern "C" lam_status lam_connect(lam_ctx* c) {
   return connect_links(c);
 }
 
+static lam_status publish_impl(lam_ctx* c, uint64_t v, int32_t rank, const lam_shard* shards, int32_t n,
+                               void* actor_stream, void* reads_done);
+
 extern "C" lam_status lam_publish(lam_ctx* c, uint64_t v, int32_t rank, const lam_shard* shards, int32_t n,
                                   void* actor_stream, void* reads_done) {
+  const uint64_t t0 = steady_ns();
+  const lam_status st = publish_impl(c, v, rank, shards, n, actor_stream, reads_done);
+  if (st == LAM_OK) {
+    const uint64_t dt = steady_ns() - t0;
+    Lock l(c->shm);
+    c->shm->stats.publish_ns_total += dt;
+    if (dt > c->shm->stats.publish_ns_max) c->shm->stats.publish_ns_max = dt;
+  }
+  return st;
+}
+
+static lam_status publish_impl(lam_ctx* c, uint64_t v, int32_t rank, const lam_shard* shards, int32_t n,
+                               void* actor_stream, void* reads_done) {
   if (!c || !c->connected || rank < 0 || rank >= c->cfg.fsdp_size || n < 0 || (n && !shards) || v == 0)
     return LAM_EINVAL;
   if (!owns(c, c->cfg.actor_device[rank])) return LAM_EINVAL;
@@ -1295,11 +1316,12 @@ extern "C" lam_status lam_publish(lam_ctx* c, uint64_t v, int32_t rank, const la
   }
   int rc = launch_pack(rp.d_units, rp.n_units, rp.d_ptrs, slot_data(p, s), m, rp.d_units_per_chunk, v,
                        c->plan.total_chunks, c->dev[dev].d_chunk_len, c->pack_ctas, side, sub,
-                       c->dev[dev].d_pack_work);
+                       c->dev[dev].d_pack_work, c->pack_sms);
   if (rc) {
     fprintf(stderr, "liblam: pack launch failed: %s\n", cudaGetErrorString((cudaError_t)rc));
     return LAM_ECUDA;
   }
+  if (rp.n_units) c->shm->stats.kernel_launches++;
   prof_end(c, 0, dev, side, t0);
   if (reads_done) CK(cudaEventRecord((cudaEvent_t)reads_done, side));
   CK(cudaEventRecord(rp.ev[s], side));
@@ -1415,6 +1437,7 @@ extern "C" lam_status lam_pull(lam_ctx* c, int32_t rid, const lam_tp_layout* L, 
   }
   CK(cudaEventRecord(wev, (cudaStream_t)stream));
   CK(cudaEventRecord(pp->last_ev, (cudaStream_t)stream));
+  if (pp->n_tiles) c->shm->stats.kernel_launches += __builtin_popcount(pp->kinds);
   prof_end(c, 2, ro.device, (cudaStream_t)stream, t0);
   cudaEvent_t ev = get_event(c, ro.device);
   CK(cudaEventRecord(ev, (cudaStream_t)stream));
@@ -1568,6 +1591,13 @@ extern "C" lam_status lam_pull_bytes(lam_ctx* c, int32_t rid, const lam_tp_layou
   if (st != LAM_OK) return st;
   *local = pp->local_bytes;
   *remote = pp->remote_bytes;
+  return LAM_OK;
+}
+
+extern "C" lam_status lam_set_pack_sms(lam_ctx* c, int32_t sms) {
+  if (!c || sms < 0) return LAM_EINVAL;
+  Lock l(c->shm);
+  c->pack_sms = sms;
   return LAM_OK;
 }
 

@@ -47,7 +47,7 @@ class lam_config(C.Structure):
                 ("n_procs", C.c_int32), ("proc_of_device", C.c_int32 * LAM_MAX_DEVICES),
                 ("shm_name", C.c_char * 64), ("pack_ctas", C.c_int32), ("hop_ctas", C.c_int32),
                 ("pull_ctas", C.c_int32), ("spin_timeout_s", C.c_double), ("hop_mode", C.c_int32),
-                ("heartbeat_timeout_s", C.c_double)]
+                ("heartbeat_timeout_s", C.c_double), ("pack_sms", C.c_int32)]
 
 
 class lam_shard(C.Structure):
@@ -93,7 +93,8 @@ class lam_stats(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in ("publishes", "publish_busy", "hops_launched", "versions_skipped",
                                           "pulls", "checksum_errors", "timeouts", "plan_cache_hits",
                                           "plan_cache_misses", "chain_rebuilds", "chain_resumes",
-                                          "last_repair_ns")]
+                                          "last_repair_ns", "kernel_launches", "publish_ns_total",
+                                          "publish_ns_max")]
 
 
 _LIB = None
@@ -247,6 +248,7 @@ class Config:
     spin_timeout_s: float = 0.0
     hop_mode: int = LAM_HOP_KERNEL
     heartbeat_timeout_s: float = 0.0
+    pack_sms: int = 0                                            # > 0: pack confined to SMs 0..pack_sms-1
     host_relays: list[int] = field(default_factory=list)     # relay nodes (1-based) kept in host memory
 
     def to_c(self) -> lam_config:
@@ -278,6 +280,7 @@ class Config:
                                                                   self.spin_timeout_s)
         c.hop_mode = self.hop_mode
         c.heartbeat_timeout_s = self.heartbeat_timeout_s
+        c.pack_sms = self.pack_sms
         return c
 
 
@@ -397,6 +400,9 @@ class Context:
 
     def set_profiling(self, on: bool) -> None:
         _check(self.L.lam_set_profiling(self.h, int(on)), "lam_set_profiling")
+
+    def set_pack_sms(self, sms: int) -> None:
+        _check(self.L.lam_set_pack_sms(self.h, int(sms)), "lam_set_pack_sms")
 
     def kernel_times(self) -> dict:
         """{'pack'|'hop'|'pull': (total_ms, launches)} of completed launches since the last call."""

@@ -115,6 +115,25 @@ def test_tiny_publish_pull_single_gpu(layout, N, C, tp):
     ctx.close()
 
 
+@pytest.mark.parametrize("sms", [1, 16, 74])
+def test_tiny_pack_confined_to_k_sms(sms):
+    """lam_config.pack_sms (actor-stall control): the pack's CTAs outside SMs [0, k) leave at once and
+    every unit comes from the work counter — the image, headers and a pull stay bit-exact (specials,
+    ragged chunks, FSDP-4)."""
+    od = OMODELS["tiny"]
+    N, C = 4, 3 * 4096
+    ctx = make_ctx("tiny", N, [0] * N, [], [(0, 0)], C=C, pack_sms=sms)
+    shards = [ActorShard(MODELS["tiny"], N, r, 0) for r in range(N)]
+    for v in (1, 2):
+        publish_all(ctx, shards, v, True)
+        until_idle(ctx)
+        plan = image_plan([s for _, s in otensors(od)], N, C)
+        oimg, ohdr = publish(plan, SEED, v, specials=True)
+        check_image(ctx, 0, v, oimg, ohdr, C)
+    check_pull(ctx, 0, 2, 1, 0, 2, True, od)
+    ctx.close()
+
+
 @pytest.mark.parametrize("model,layout,N,C,tps", [
     ("odd", lam.LAM_FSDP2_DIM0, 1, 4096, (1, 2, 4, 8)),      # KV-head replication, vocab padding
     ("odd", lam.LAM_FSDP1_FLAT, 3, 4096, (2, 8)),            # ... with mid-row FSDP1 cuts

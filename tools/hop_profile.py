@@ -21,28 +21,32 @@ from synth import SEED  # noqa: E402
 
 
 def main():
-    model = sys.argv[1] if len(sys.argv) > 1 else "7b"
+    args = [a for a in sys.argv[1:] if not a.startswith("--")]
+    model = args[0] if args else "7b"
     mode = lam.LAM_HOP_COPY_ENGINE if "--ce" in sys.argv else lam.LAM_HOP_KERNEL
-    ctx = lam.Context(lam.Config(model=MODELS[model], relays=[[1]], rollouts=[], chunk_bytes=128 << 20,
-                                 hop_mode=mode))
+    nrel = int(args[1]) if len(args) > 1 else 1
+    ctx = lam.Context(lam.Config(model=MODELS[model], relays=[[d] for d in range(1, nrel + 1)], rollouts=[],
+                                 chunk_bytes=128 << 20, hop_mode=mode))
     sh = ActorShard(MODELS[model], 1, 0, 0)
     sh.fill(SEED, 1)
     torch.cuda.synchronize()
     ctx.set_profiling(True)
-    for v in (1, 2):
+    for v in (1, 2, 3):
         assert ctx.publish(v, 0, sh.shards(), 0) == lam.LAM_OK
         while ctx.latest(0) < v:            # the pack completes before the hop is launched
             ctx.relay_step()
         t0 = time.time()
-        while ctx.latest(1) < v:
+        while ctx.latest(nrel) < v:
             ctx.relay_step()
             if time.time() - t0 > 120:
                 raise TimeoutError
+        t1 = time.time()
         torch.cuda.synchronize()
         kt = ctx.kernel_times()
         ms, n = kt["hop"]
         M = ctx.plan_info().snapshot_bytes
-        print(f"v{v}: hop {ms / max(n, 1):.3f} ms = {M / (ms / max(n, 1) / 1e3) / 1e9:.1f} GB/s "
+        print(f"v{v}: {nrel} relay(s), {'ce' if mode else 'kernel'}: hop avg {ms / max(n, 1):.3f} ms = "
+              f"{M / (ms / max(n, 1) / 1e3) / 1e9:.1f} GB/s; master complete -> last relay {1e3 * (t1 - t0):.2f} ms "
               f"(pack {kt['pack'][0]:.3f} ms)", flush=True)
     ctx.close()
 
