@@ -59,8 +59,9 @@ def parse(argv=None):
     ap.add_argument("--tp", type=int, default=0, help="rollout TP size (colocated / relay-tp)")
     ap.add_argument("--chunk-mb", type=int, default=0, help="chunk size; 0 = Appendix D k*")
     ap.add_argument("--hop-ctas", type=int, default=0)
-    ap.add_argument("--hop-mode", default="kernel", choices=["kernel", "ce"],
-                    help="relay hop: TMA kernel or copy engines + k_verify")
+    ap.add_argument("--hop-mode", default="kernel", choices=["kernel", "ce", "mc"],
+                    help="relay hop: TMA kernel, copy engines + k_verify, or NVSwitch multicast (NEXT-2: the "
+                         "pack stores once through a multicast object, every relay verifies its replica)")
     ap.add_argument("--stream-pull", default="auto", choices=["auto", "on", "off"],
                     help="on: rollouts reshard chunk by chunk while their relay receives (lam_pull_stream); "
                          "off: pull once the relay committed (lam_pull); auto: on for chain / relay-tp, off for "
@@ -439,20 +440,26 @@ HEADLINE = [
 ]
 
 
-def nvlink_bound(T, N, P, pull_in=None):
+def nvlink_bound(T, N, P, pull_in=None, multicast=False):
     """Publish->all lower bound: max over GPUs of the bf16 bytes that must enter (or
     leave) that GPU over NVLink, / 900 GB/s (the stages pipeline).  Counted from the placement: chain
-    hops between GPUs, plus `pull_in[d]` = bytes the rollouts on GPU d gather from other GPUs."""
+    hops between GPUs, plus `pull_in[d]` = bytes the rollouts on GPU d gather from other GPUs.
+    multicast (NEXT-2): every relay receives from node 0 and the switch replicates, so the source's
+    egress is each region once, whatever the number of relays."""
     n = T["fsdp"]
     region = 2.0 * P / n                    # bf16 bytes of one actor rank's region
     ing = {d: 0.0 for d in range(N)}
     egr = {d: 0.0 for d in range(N)}
     prev = {r: T["actors"][r] for r in range(n)}
+    sent = set()
     for node in T["relays"]:                # chain hops: each relay part receives its rank's region
         for r, d in enumerate(node):
-            if d != prev[r]:
+            src = T["actors"][r] if multicast else prev[r]
+            if d != src:
                 ing[d] += region
-                egr[prev[r]] += region
+                if not multicast or r not in sent:
+                    egr[src] += region
+                    sent.add(r)
         prev = {r: node[r] for r in range(n)}
     for d, x in (pull_in or {}).items():
         ing[d] += x
@@ -534,7 +541,8 @@ class Placement:
                          shm_name=f"lam_bench_{port}_{os.getppid()}_{tag}", hop_ctas=args.hop_ctas,
                          pack_ctas=args.pack_ctas, pull_ctas=args.pull_ctas, pack_sms=args.pack_sms,
                          slots=args.slots or (3 if config == "stress" and N > 1 else 2),
-                         hop_mode=lam.LAM_HOP_COPY_ENGINE if args.hop_mode == "ce" else lam.LAM_HOP_KERNEL,
+                         hop_mode={"ce": lam.LAM_HOP_COPY_ENGINE, "mc": lam.LAM_HOP_MULTICAST}.get(args.hop_mode,
+                                                                                               lam.LAM_HOP_KERNEL),
                          host_relays=T.get("host_relays", []))
         self.ctx = ctx = lam.Context(cfg)
         if N > 1:
@@ -682,10 +690,20 @@ def roofline_of(P: Placement, kt, steps):
     if kt["pull"][1] and n_pulled:      # a streamed pull = many launches: per pull = sum / (steps x rollouts)
         avg["pull"] = kt["pull"][0] / (steps * n_pulled)
     cand = []
-    if avg["pack"]:
+    mc = P.args.hop_mode == "mc" and P.N > 1
+    if avg["pack"] and mc:
+        # NEXT-2: the pack's stores go through the NVSwitch multicast object — NVLink egress of the image
+        # once (each relay GPU receives M), 4 B/param of HBM reads on the side
+        cand.append(dict(kernel="k_pack(multicast)", ms=avg["pack"], bound="nvlink",
+                         bytes=2.0 * sum(sh.numel for sh in P.shards.values())))
+    elif avg["pack"]:
         b = (8.0 if P.subs else 6.0) * sum(sh.numel for sh in P.shards.values())
         cand.append(dict(kernel="k_pack" + ("+subscriber" if P.subs else ""), ms=avg["pack"], bound="hbm", bytes=b))
-    if avg["hop"]:
+    if avg["hop"] and mc:   # verify + commit from the local replica: HBM read + write
+        # it runs as long as the multicast pack feeds it (it waits on the chunk flags): reported, never
+        # the dominant kernel
+        cand.append(dict(kernel="k_hop(replica)", ms=avg["hop"], bound="hbm", bytes=2.0 * M, follows=True))
+    elif avg["hop"]:
         part_bytes = M if P.config in ("chain", "host", "stress") else M / max(1, P.T["fsdp"])
         cand.append(dict(kernel="k_hop", ms=avg["hop"], bound="pcie" if P.config == "host" else "nvlink",
                          bytes=float(part_bytes)))
@@ -859,7 +877,7 @@ def summarize(P: Placement, res, steps, rank0_extra=None):
     except Exception:
         pass
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
-    allc = [c for pr in per_rank for c in pr["cand"]]
+    allc = [c for pr in per_rank for c in pr["cand"] if not c.get("follows")]
     dom = max(allc, key=lambda c: c["ms"]) if allc else None
     roof = None
     if dom:
@@ -878,9 +896,12 @@ def summarize(P: Placement, res, steps, rank0_extra=None):
                     algorithmic_bytes_per_launch=dom["bytes"], launch_ms=dom["ms"], peak_source=src)
         if dom["bound"] == "nvlink":
             roof["per_link_gbs"] = ach / 18.0       # 18 NVLink 5 links per GPU, 50 GB/s/dir each
+            nvl = traffic_of("nvlink:" + dom["kernel"], P.model_name, N, P.config)
+            if nvl:   # ncu nvlrx/nvltx of the same kernel (raw link bytes incl. packet headers / read requests)
+                roof["nvlink_traffic"] = dict(nvl, source="ncu nvlrx__bytes.sum / nvltx__bytes.sum per launch")
     rem = 0.0 if P.config == "host" else float(sum(P.pull_bytes[rid][1] for rid in P.mine))
     pull_in = {r: x for r, x in enumerate(D.gather(rem))}
-    ing, egr = nvlink_bound(P.T, N, P.info.params, pull_in)
+    ing, egr = nvlink_bound(P.T, N, P.info.params, pull_in, multicast=P.args.hop_mode == "mc")
     worst = max(max(ing.values()), max(egr.values()))
     bound_s = worst / (NVL_NOMINAL * 1e9)
     lat = sorted(res["lat"])

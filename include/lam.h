@@ -137,12 +137,21 @@ typedef struct {
                                               kernels (actor stall); 0 = all SMs */
 } lam_config;
 
-/* How a relay moves a chunk from its predecessor (both receiver-driven, chunk-pipelined, verified):
+/* How a relay moves a chunk from its predecessor (all chunk-pipelined and verified):
  *  LAM_HOP_KERNEL       k_hop: TMA bulk copies through shared memory by ~32 SMs, checksum on the fly
  *  LAM_HOP_COPY_ENGINE  copy engines (zero SMs for the transfer): per chunk the relay's stream waits
  *                       for the predecessor's flag (stream memory op), cudaMemcpyAsync pulls the chunk
- *                       over NVLink, then k_verify checksums it in local HBM and releases the flag. */
-enum { LAM_HOP_KERNEL = 0, LAM_HOP_COPY_ENGINE = 1 };
+ *                       over NVLink, then k_verify checksums it in local HBM and releases the flag.
+ *  LAM_HOP_MULTICAST    NVSwitch multicast broadcast (the bandwidth
+ *                       term M·T_byte is the floor): no chain — every relay's predecessor is node 0.  The
+ *                       pack stores the bf16 image once through a multicast object (multimem.st) bound
+ *                       to node 0's slots on the actor GPU and to a replica of them on every relay GPU,
+ *                       followed by each chunk's flag; each relay's k_hop then verifies and commits the
+ *                       chunk from its local replica (HBM -> HBM).  The source GPU sends M once, relays
+ *                       forward nothing.  Requires every actor rank on one GPU, HBM relay nodes, node-0
+ *                       rollouts on that GPU, and multicast-capable devices (NVSwitch); costs each relay
+ *                       GPU S extra image-sized replicas.  LAM_EINVAL otherwise. */
+enum { LAM_HOP_KERNEL = 0, LAM_HOP_COPY_ENGINE = 1, LAM_HOP_MULTICAST = 2 };
 
 /* One fp32 master shard piece owned by the caller: elements [elem_offset, elem_offset+elem_count)
  * of the flattened tensor `tensor_id`, at `ptr` (device memory of the actor rank's GPU). */

@@ -47,7 +47,7 @@ def build(verbose: bool = False, force: bool = False) -> list[str]:
     nvcc = _nvcc()
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
     headers.append(os.path.join(ROOT, "include", "lam.h"))
-    srcs = ["kernels.cu", "plan.cpp", "model.cpp", "control.cpp", "runtime.cpp"]
+    srcs = ["kernels.cu", "plan.cpp", "model.cpp", "control.cpp", "mcast.cpp", "runtime.cpp"]
     objs, jobs = [], []
     for s in srcs:
         src = os.path.join(CSRC, s)

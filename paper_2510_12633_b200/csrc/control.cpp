@@ -141,11 +141,11 @@ static void open_slot(ShmSlot& sl, uint64_t v, int src_slot) {
   sl.epoch++;
 }
 
-void init(Shm* sh, int n_nodes) {
+void init(Shm* sh, int n_nodes, bool star) {
   sh->n_nodes = n_nodes;
   for (int i = 0; i <= LAM_MAX_NODES; ++i) {
     sh->node[i].dead = 0;
-    sh->node[i].pred = i - 1;
+    sh->node[i].pred = star && i > 0 ? 0 : i - 1;
   }
 }
 

@@ -88,8 +88,9 @@ uint64_t pin_latest(Shm* sh, int S, int node, int* slot);
 void unpin(Shm* sh, int node, int slot);
 // Anything FILLING, or a node behind its predecessor?
 bool busy(Shm* sh, int S, int n_nodes);
-// Chain of n_nodes (called once by the creator): every node alive, pred = node - 1.
-void init(Shm* sh, int n_nodes);
+// Chain of n_nodes (called once by the creator): every node alive, pred = node - 1; star (the
+// LAM_HOP_MULTICAST broadcast, NEXT-2): every relay's predecessor is node 0.
+void init(Shm* sh, int n_nodes, bool star = false);
 // Relay failure: mark `node` dead and rebuild the chain in O(1): its successor is
 // linked to its (live) predecessor.  A successor that was filling from it re-pins the same version
 // at the new predecessor and restarts (slot epoch++, launch mask cleared: the runtime resumes from

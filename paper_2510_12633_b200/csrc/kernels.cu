@@ -52,9 +52,25 @@ __device__ __forceinline__ uint64_t globaltimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+// NVSwitch multicast stores (LAM_HOP_MULTICAST, mcast.cpp): one store through the multicast VA lands
+// at the same offset in every team GPU's member (the switch replicates it).
+__device__ __forceinline__ void mc_st_v4(void* p, uint4 v) {
+  asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ void mc_st_b32(void* p, uint32_t v) {
+  asm volatile("multimem.st.relaxed.sys.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void mc_st_release_u64(uint64_t* p, uint64_t v) {
+  asm volatile("multimem.st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 // Release a chunk flag (device memory, read by the next relay over NVLink) and mirror it to host
-// shared memory, where lam_relay_step of any process sees it and drives streaming pulls.
+// shared memory, where lam_relay_step of any process sees it and drives streaming pulls.  Multicast
+// mode: the flag also goes through the switch to every relay GPU's member (after the chunk's data,
+// which took the same path), where that relay polls it in local HBM.
 __device__ __forceinline__ void publish_flag(const ChunkMeta& meta, uint32_t chunk, uint64_t value) {
+  if (meta.mc_flags) mc_st_release_u64(meta.mc_flags + chunk, value);
   st_release_sys(meta.flags + chunk, value);
   if (meta.mirror) st_release_sys(meta.mirror + chunk, value);
 }
@@ -142,8 +158,10 @@ __device__ void pack_flush(ChunkMeta meta, const uint32_t* units_per_chunk, cons
 }
 
 // SUB: compiled with the colocated-subscriber stores (separate instantiation: the plain pack keeps
-// its register budget and occupancy)
-template <bool SUB>
+// its register budget and occupancy).  MC: `dst` is the multicast VA of node 0's slot (NEXT-2): every
+// 16-B store is a multimem.st, so the bf16 image lands in the actor GPU's slot and in every relay
+// GPU's replica in the same pass.
+template <bool SUB, bool MC>
 __global__ void __launch_bounds__(kPackThreads) k_pack(const PackUnit* __restrict__ units, uint32_t n_units,
                                                        const float* const* __restrict__ shard_ptrs,
                                                        uint8_t* __restrict__ dst, ChunkMeta meta,
@@ -212,7 +230,7 @@ __global__ void __launch_bounds__(kPackThreads) k_pack(const PackUnit* __restric
           const uint32_t vk = v + k * kPackThreads;
           const uint4 w = make_uint4(pack2(a[k].x, a[k].y), pack2(a[k].z, a[k].w), pack2(b[k].x, b[k].y),
                                      pack2(b[k].z, b[k].w));
-          st_v4(out + 16 * (size_t)vk, w);
+          if (MC) mc_st_v4(out + 16 * (size_t)vk, w); else st_v4(out + 16 * (size_t)vk, w);
           if (out2) st_v4_any(out2 + 16 * (size_t)vk, w);
           cks4((uint64_t)u.word0 + 4ull * vk, w, s1, s2);
         }
@@ -220,7 +238,7 @@ __global__ void __launch_bounds__(kPackThreads) k_pack(const PackUnit* __restric
       for (; v < nvec; v += kPackThreads) {
         const uint4 a = ld_stream_v4(src + 8 * (size_t)v), b = ld_stream_v4(src + 8 * (size_t)v + 4);
         const uint4 w = make_uint4(pack2(a.x, a.y), pack2(a.z, a.w), pack2(b.x, b.y), pack2(b.z, b.w));
-        st_v4(out + 16 * (size_t)v, w);
+        if (MC) mc_st_v4(out + 16 * (size_t)v, w); else st_v4(out + 16 * (size_t)v, w);
         if (out2) st_v4_any(out2 + 16 * (size_t)v, w);
         cks4((uint64_t)u.word0 + 4ull * v, w, s1, s2);
       }
@@ -229,7 +247,7 @@ __global__ void __launch_bounds__(kPackThreads) k_pack(const PackUnit* __restric
       for (uint32_t v = threadIdx.x; v < nvec; v += kPackThreads) {
         const uint32_t* q = s32 + 8 * (size_t)v;
         const uint4 w = make_uint4(pack2(q[0], q[1]), pack2(q[2], q[3]), pack2(q[4], q[5]), pack2(q[6], q[7]));
-        st_v4(out + 16 * (size_t)v, w);
+        if (MC) mc_st_v4(out + 16 * (size_t)v, w); else st_v4(out + 16 * (size_t)v, w);
         if (out2) st_v4_any(out2 + 16 * (size_t)v, w);
         cks4((uint64_t)u.word0 + 4ull * v, w, s1, s2);
       }
@@ -241,8 +259,12 @@ __global__ void __launch_bounds__(kPackThreads) k_pack(const PackUnit* __restric
       for (uint32_t e = nvec * 8 + 2 * threadIdx.x; e < u.n; e += 2 * kPackThreads) {
         const uint32_t lo = rne_bf16(s32[e]);
         const uint32_t hi = (e + 1 < u.n) ? rne_bf16(s32[e + 1]) : 0u;
-        o16[e] = (uint16_t)lo;
-        if (e + 1 < u.n) o16[e + 1] = (uint16_t)hi;
+        if (MC) {   // one word (e even, out 16-B aligned); the half past the segment is zero pad anyway
+          mc_st_b32(o16 + e, lo | (hi << 16));
+        } else {
+          o16[e] = (uint16_t)lo;
+          if (e + 1 < u.n) o16[e + 1] = (uint16_t)hi;
+        }
         if (out2) {
           reinterpret_cast<uint16_t*>(out2)[e] = (uint16_t)lo;
           if (e + 1 < u.n) reinterpret_cast<uint16_t*>(out2)[e + 1] = (uint16_t)hi;
@@ -271,18 +293,13 @@ int launch_pack(const PackUnit* units, uint32_t n_units, const float* const* sha
   if (n_units == 0) return 0;
   cudaError_t e = cudaMemsetAsync(work, 0, sizeof(uint32_t), (cudaStream_t)stream);
   if (e != cudaSuccess) return (int)e;
-  if (ctas <= 0 || sms > 0)
-    ctas = sub_dst ? resident_ctas(k_pack<true>, kPackThreads) : resident_ctas(k_pack<false>, kPackThreads);
+  const bool mc = meta.mc_flags != nullptr;
+  auto kern = sub_dst ? (mc ? k_pack<true, true> : k_pack<true, false>) : (mc ? k_pack<false, true> : k_pack<false, false>);
+  if (ctas <= 0 || sms > 0) ctas = resident_ctas(kern, kPackThreads);
   // confined: the full wave must land everywhere (the CTAs on SMs >= sms leave), not n_units of it
   unsigned grid = (unsigned)(sms > 0 || n_units >= (uint32_t)ctas ? (uint32_t)ctas : n_units);
-  if (sub_dst)
-    k_pack<true><<<grid, kPackThreads, 0, (cudaStream_t)stream>>>(units, n_units, shard_ptrs, dst, meta,
-                                                                  units_per_chunk, version, n_total, chunk_len, sub_dst, work,
-                                                                  (uint32_t)(sms > 0 ? sms : 0));
-  else
-    k_pack<false><<<grid, kPackThreads, 0, (cudaStream_t)stream>>>(units, n_units, shard_ptrs, dst, meta,
-                                                                   units_per_chunk, version, n_total, chunk_len, nullptr, work,
-                                                                   (uint32_t)(sms > 0 ? sms : 0));
+  kern<<<grid, kPackThreads, 0, (cudaStream_t)stream>>>(units, n_units, shard_ptrs, dst, meta, units_per_chunk, version,
+                                                        n_total, chunk_len, sub_dst, work, (uint32_t)(sms > 0 ? sms : 0));
   return (int)cudaGetLastError();
 }
 

@@ -128,6 +128,7 @@ struct ChunkMeta {          // device view of one slot's metadata in a node part
   uint32_t* cnt;            // [total_chunks]
   int32_t* abort_flag;      // [1]
   uint64_t* mirror;         // [total_chunks] host-visible copy of flags (shared memory) or null
+  uint64_t* mc_flags;       // LAM_HOP_MULTICAST pack: multicast VA of the slot's flag array, else null
 };
 constexpr uint32_t kMirrorChunks = 2048;  // chunks per slot mirrored to the host (streaming pulls)
 

@@ -31,6 +31,7 @@
 
 #include "control.h"
 #include "lam_internal.h"
+#include "mcast.h"
 
 namespace lam {
 
@@ -57,6 +58,9 @@ struct Part {
   int host_fd = -1;                  // memfd (owner) or /proc/<pid>/fd reopen (other processes)
   size_t host_bytes = 0;
   bool host_registered = false;
+  // LAM_HOP_MULTICAST: node 0's slot data is the actor GPU's member of the multicast team (mcast.h);
+  // the metadata block is a separate allocation (exported by IPC like a host part's)
+  bool mc = false;
   // local-only
   cudaStream_t stream = nullptr;
   cudaEvent_t done_ev[LAM_MAX_SLOTS] = {};
@@ -69,6 +73,8 @@ struct Part {
   RankLink* d_links = nullptr;       // [S][S][N] (my slot, pred slot, rank)
   // copy-engine hop mode
   cudaStream_t vstream = nullptr;    // verify stream
+  cudaStream_t cstream2 = nullptr;   // second copy stream: odd chunks (two copies in flight hide the
+                                     // copy engines' per-copy start-up, ~16 us per 128 MiB copy)
   std::vector<uint32_t> my_chunks;   // this part's chunks in processing order
   uint32_t* d_my_chunks = nullptr;
   std::vector<cudaEvent_t> chunk_ev; // [n_my + 1]: per-chunk copy done, last = verify stream done
@@ -146,6 +152,8 @@ struct lam_ctx {
   std::vector<Part> parts;
   std::vector<RankPub> pubs;                  // [N]; local ranks only used
   std::map<int, DevLocal> dev;                // devices owned by this process
+  bool star = false;                          // LAM_HOP_MULTICAST: every relay is fed by node 0
+  McTeam mc;                                  // LAM_HOP_MULTICAST team (NEXT-2)
   std::map<std::string, PullPlan> plans;
   uint64_t plan_clock = 0;
   struct PullRing { uint32_t* d = nullptr; uint32_t next = 0; std::vector<cudaEvent_t> ev; };
@@ -192,6 +200,9 @@ bool owns(const lam_ctx* c, int device) {
 int node_part_device(const lam_ctx* c, int node, int rank) {
   return node == 0 ? c->cfg.actor_device[rank] : c->cfg.relay[node - 1].part_device[rank];
 }
+
+// The predecessor a relay node has while nobody failed: node - 1 (chain), or node 0 (multicast star).
+int base_pred(const lam_ctx* c, int node) { return c->star ? 0 : node - 1; }
 
 #define CK(x)                                             \
   do {                                                    \
@@ -241,6 +252,7 @@ ChunkMeta meta_of(const lam_ctx* c, const Part& p, int slot) {
   cm.cnt = reinterpret_cast<uint32_t*>(m + c->sm.cnt);
   cm.abort_flag = reinterpret_cast<int32_t*>(m + c->sm.abort);
   cm.mirror = c->mirror_dev ? c->mirror_dev + ((uint64_t)p.node * LAM_MAX_SLOTS + slot) * kShmMirrorChunks : nullptr;
+  cm.mc_flags = nullptr;
   return cm;
 }
 
@@ -314,7 +326,18 @@ lam_status validate(const lam_config& c, std::string* why) {
     if (c.rollout[i].node < 0 || c.rollout[i].node > c.n_relays || !dev_ok(c.rollout[i].device))
       return bad("rollout " + std::to_string(i));
   if (c.n_procs > 1 && c.shm_name[0] == 0) return bad("shm_name required with n_procs > 1");
-  if (c.hop_mode != LAM_HOP_KERNEL && c.hop_mode != LAM_HOP_COPY_ENGINE) return bad("hop_mode");
+  if (c.hop_mode != LAM_HOP_KERNEL && c.hop_mode != LAM_HOP_COPY_ENGINE && c.hop_mode != LAM_HOP_MULTICAST)
+    return bad("hop_mode");
+  if (c.hop_mode == LAM_HOP_MULTICAST) {
+    // one source GPU (the multicast writer), HBM relays, node-0 readers on the source GPU
+    for (int r = 1; r < c.fsdp_size; ++r)
+      if (c.actor_device[r] != c.actor_device[0]) return bad("multicast hops need every actor rank on one GPU");
+    for (int i = 0; i < c.n_relays; ++i)
+      if (c.relay[i].host_memory) return bad("multicast hops need HBM relay nodes");
+    for (int i = 0; i < c.n_rollouts; ++i)
+      if (c.rollout[i].node == 0 && c.rollout[i].device != c.actor_device[0])
+        return bad("multicast hops: a rollout of node 0 must be on the actor GPU");
+  }
   return LAM_OK;
 }
 
@@ -370,9 +393,31 @@ lam_status alloc_parts(lam_ctx* c) {
     p.meta_base = p.slot_stride * S;
     p.meta_stride = c->sm.bytes;
     p.alloc_bytes = p.meta_base + p.meta_stride * S;
+  }
+  if (c->star) {
+    // multicast team members (NEXT-2): node 0's S slots followed by S flag arrays, on the actor GPU
+    // and every relay GPU this process owns
+    const Part& p0 = c->parts[c->node_parts[0][0]];
+    c->mc.flag_stride = align_up(8 * std::max<uint64_t>(total, 1), 4096);
+    c->mc.flags_off = p0.slot_stride * S;
+    std::vector<int> local;
+    for (int d : c->mc.devices)
+      if (owns(c, d)) local.push_back(d);
+    if (!local.empty()) {
+      lam_status ms = mc_alloc_members(c->mc, local, c->mc.flags_off + c->mc.flag_stride * S);
+      if (ms != LAM_OK) return ms;
+    }
+  }
+  for (Part& p : c->parts) {
     if (!p.local) continue;
     CK(cudaSetDevice(p.device));
-    if (p.host) {
+    if (p.node == 0 && c->star) {
+      // slot data = the actor GPU's member of the multicast team (zero-filled); metadata separate
+      p.mc = true;
+      p.data = c->mc.va.at(p.device);
+      if (cudaMalloc(&p.meta, (size_t)p.meta_stride * S) != cudaSuccess) return LAM_ENOMEM;
+      CK(cudaMemset(p.meta, 0, (size_t)p.meta_stride * S));
+    } else if (p.host) {
       // slot data in pinned host memory (zero-filled by the kernel), metadata in HBM
       const size_t hb = (size_t)p.slot_stride * S;
       int fd = (int)memfd_create("lam_host_relay", 0);
@@ -438,12 +483,29 @@ lam_status alloc_parts(lam_ctx* c) {
         CK(cudaMemcpy(p.d_my_chunks, p.my_chunks.data(), 4 * p.my_chunks.size(), cudaMemcpyHostToDevice));
       if (c->cfg.hop_mode == LAM_HOP_COPY_ENGINE) {
         CK(cudaStreamCreateWithPriority(&p.vstream, cudaStreamNonBlocking, lo));
+        CK(cudaStreamCreateWithPriority(&p.cstream2, cudaStreamNonBlocking, lo));
         p.chunk_ev.resize(p.my_chunks.size() + 1);
         for (auto& e : p.chunk_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
       }
     }
   }
   return LAM_OK;
+}
+
+// LAM_HOP_MULTICAST: create/import the multicast object, add and bind this process's team devices.
+// Called outside the control-block lock (cuMulticastBindMem blocks until every process added its GPU).
+lam_status mc_connect(lam_ctx* c) {
+  if (!c->star || c->mc.mc) return LAM_OK;
+  std::vector<int> local;
+  std::set<int> procs;
+  for (int d : c->mc.devices) {
+    if (owns(c, d)) local.push_back(d);
+    procs.insert(c->cfg.proc_of_device[d]);
+  }
+  if (local.empty()) return LAM_OK;
+  const bool owner = owns(c, c->mc.owner_dev);
+  const std::string sock = std::string("lam-mc-") + c->cfg.shm_name;
+  return mc_setup(c->mc, local, owner, owner ? (int)procs.size() - 1 : 0, sock.c_str());
 }
 
 lam_status connect_links(lam_ctx* c) {
@@ -466,7 +528,7 @@ lam_status connect_links(lam_ctx* c) {
       }
   }
   for (auto& p : c->parts)
-    if (!p.data || !p.meta) {
+    if ((!p.data && !p.mc) || !p.meta) {
       fprintf(stderr, "liblam: part of node %d on device %d not mapped (missing lam_import_ipc?)\n", p.node, p.device);
       return LAM_EIPC;
     }
@@ -477,12 +539,19 @@ lam_status connect_links(lam_ctx* c) {
     for (int s = 0; s < S; ++s)
       for (int ps = 0; ps < S; ++ps)
         for (int r : p.ranks) {
-          const Part& q = c->parts[c->node_rank_part[p.node - 1][r]];
+          const Part& q = c->parts[c->node_rank_part[base_pred(c, p.node)][r]];
           ChunkMeta qm = meta_of(c, q, ps);
           RankLink& L = links[((size_t)s * S + ps) * N + r];
           L.src = slot_data(q, ps) + q.rank_off[r];
           L.src_flags = qm.flags;
           L.src_hdr = qm.hdr;
+          if (c->star) {
+            // the relay's replica of node 0's slot in its own GPU's team member, and the chunk flags
+            // the pack multicast next to it: data and flags are read from local HBM
+            uint8_t* mine = c->mc.va.at(p.device);
+            L.src = mine + (uint64_t)ps * q.slot_stride + q.rank_off[r];
+            L.src_flags = reinterpret_cast<const uint64_t*>(mine + c->mc.flags_off + (uint64_t)ps * c->mc.flag_stride);
+          }
           L.dst = slot_data(p, s) + p.rank_off[r];
         }
     CK(cudaSetDevice(p.device));
@@ -585,12 +654,14 @@ lam_status ce_topup(lam_ctx* c, Part& p) {
     const uint64_t off = (g - c->plan.chunk_base[r]) * c->plan.C, len = c->plan.chunk_len(g);
     const uint8_t* src = slot_data(q, ps) + q.rank_off[r] + off;
     uint8_t* dst = slot_data(p, s) + p.rank_off[r] + off;
+    // alternate chunks between two copy streams (the verify stream orders the commits)
+    cudaStream_t cs = (i & 1u) && p.cstream2 ? p.cstream2 : p.stream;
     if (!mir) {
-      lam_status st = stream_wait_flag(c, p.stream, qm.flags + g, u, m.abort_flag);
+      lam_status st = stream_wait_flag(c, cs, qm.flags + g, u, m.abort_flag);
       if (st != LAM_OK) return st;
     }
-    CK(cudaMemcpyAsync(dst, src, len, cudaMemcpyDefault, p.stream));
-    CK(cudaEventRecord(p.chunk_ev[i], p.stream));
+    CK(cudaMemcpyAsync(dst, src, len, cudaMemcpyDefault, cs));
+    CK(cudaEventRecord(p.chunk_ev[i], cs));
     CK(cudaStreamWaitEvent(p.vstream, p.chunk_ev[i], 0));
     if (launch_verify(dst, g, len, qm.flags, qm.hdr, m, u, p.err_dev + s, p.d_my_chunks, i, n, 32, p.vstream))
       return LAM_ECUDA;
@@ -765,13 +836,17 @@ lam_status launch_hop_part(lam_ctx* c, Part& p, int s, bool* launched) {
     p.ce_next = 0;
     p.ce_version = u;
     p.ce_t0 = t0;
+    if (p.cstream2) {   // the second copy stream starts after this hop's set-up (and same-GPU waits)
+      CK(cudaEventRecord(p.chunk_ev.back(), p.stream));
+      CK(cudaStreamWaitEvent(p.cstream2, p.chunk_ev.back(), 0));
+    }
     sl.launched_mask |= 1ull << p.pos;
     c->shm->stats.hops_launched++;
     *launched = true;
     return ce_topup(c, p);
   } else {
     const RankLink* links = p.d_links + (size_t)(s * c->S + ps) * c->cfg.fsdp_size;
-    if (pred != p.node - 1) {  // rebuilt chain: links to the new predecessor
+    if (pred != base_pred(c, p.node)) {  // rebuilt chain: links to the new predecessor
       lam_status st = build_links(c, p, s, pred, ps);
       if (st != LAM_OK) return st;
       links = p.d_links_dyn;
@@ -1096,9 +1171,22 @@ extern "C" lam_status lam_init(const lam_config* cfg, lam_ctx** out) {
   c->pull_ctas = cfg->pull_ctas > 0 ? cfg->pull_ctas : 0;
   if (cfg->spin_timeout_s > 0) c->timeout_ns = (uint64_t)(cfg->spin_timeout_s * 1e9);
   c->pubs.resize(cfg->fsdp_size);
+  if (cfg->hop_mode == LAM_HOP_MULTICAST) {
+    c->star = true;
+    std::set<int> team{cfg->actor_device[0]};
+    for (int i = 0; i < cfg->n_relays; ++i)
+      for (int r = 0; r < cfg->fsdp_size; ++r) team.insert(cfg->relay[i].part_device[r]);
+    c->mc.devices.assign(team.begin(), team.end());
+    c->mc.owner_dev = cfg->actor_device[0];
+    for (int d : c->mc.devices)
+      if (owns(c.get(), d) && !mc_supported(d, &why)) {
+        fprintf(stderr, "liblam: LAM_HOP_MULTICAST: %s\n", why.c_str());
+        return LAM_EINVAL;
+      }
+  }
   st = setup_shm(c.get());
   if (st != LAM_OK) return st;
-  if (cfg->n_procs == 1 || cfg->proc_rank == 0) ctl::init(c->shm, c->n_nodes);
+  if (cfg->n_procs == 1 || cfg->proc_rank == 0) ctl::init(c->shm, c->n_nodes, c->star);
   c->streams.resize(cfg->n_rollouts);
   // map the control block for the producer kernels' chunk-flag mirror (streaming pulls)
   for (int d = 0; d < LAM_MAX_DEVICES; ++d)
@@ -1125,7 +1213,8 @@ extern "C" lam_status lam_init(const lam_config* cfg, lam_ctx** out) {
     for (int s = 0; s < c->S; ++s) cudaEventCreateWithFlags(&c->pubs[r].ev[s], cudaEventDisableTiming);
   }
   if (cfg->n_procs == 1) {
-    st = connect_links(c.get());
+    st = mc_connect(c.get());
+    if (st == LAM_OK) st = connect_links(c.get());
     if (st != LAM_OK) {
       lam_destroy(c.release());
       return st;
@@ -1138,7 +1227,8 @@ extern "C" lam_status lam_init(const lam_config* cfg, lam_ctx** out) {
 struct IpcEntry {
   int32_t part, device;
   cudaIpcMemHandle_t h;          // HBM part: the whole allocation; host part: the metadata block
-  int32_t host, pid, fd, _pad;   // host part: memfd of the slot data, reopened via /proc/<pid>/fd/<fd>
+  int32_t host, pid, fd, mc;     // host part: memfd of the slot data, reopened via /proc/<pid>/fd/<fd>;
+                                 // mc: node 0 of LAM_HOP_MULTICAST (metadata block only, data = own member)
   uint64_t host_bytes;
 };
 
@@ -1147,9 +1237,9 @@ extern "C" lam_status lam_export_ipc(lam_ctx* c, void* buf, size_t cap, size_t* 
   std::vector<IpcEntry> v;
   for (Part& p : c->parts)
     if (p.local) {
-      IpcEntry e{p.index, p.device, {}, p.host ? 1 : 0, (int32_t)getpid(), p.host_fd, 0, p.host_bytes};
+      IpcEntry e{p.index, p.device, {}, p.host ? 1 : 0, (int32_t)getpid(), p.host_fd, p.mc ? 1 : 0, p.host_bytes};
       cudaSetDevice(p.device);
-      CK(cudaIpcGetMemHandle(&e.h, p.host ? p.meta : p.base));
+      CK(cudaIpcGetMemHandle(&e.h, (p.host || p.mc) ? p.meta : p.base));
       v.push_back(e);
     }
   size_t need = sizeof(int32_t) + v.size() * sizeof(IpcEntry);
@@ -1185,7 +1275,12 @@ extern "C" lam_status lam_import_ipc(lam_ctx* c, int32_t proc, const void* buf, 
       return LAM_EIPC;
     }
     p.ipc_opened = true;
-    if (e.host) {
+    if (e.mc) {
+      p.mc = true;
+      p.meta = (uint8_t*)ptr;
+      auto it = c->mc.va.find(my_dev);   // this process reads node 0's slots from its own replica
+      p.data = it != c->mc.va.end() ? it->second : nullptr;
+    } else if (e.host) {
       p.meta = (uint8_t*)ptr;
       char path[64];
       snprintf(path, sizeof path, "/proc/%d/fd/%d", e.pid, e.fd);
@@ -1208,6 +1303,8 @@ extern "C" lam_status lam_import_ipc(lam_ctx* c, int32_t proc, const void* buf, 
 extern "C" lam_status lam_connect(lam_ctx* c) {
   if (!c) return LAM_EINVAL;
   if (c->connected) return LAM_OK;
+  lam_status st = mc_connect(c);   // before the lock: binding waits for the other processes
+  if (st != LAM_OK) return st;
   Lock l(c->shm);
   return connect_links(c);
 }
@@ -1314,7 +1411,13 @@ static lam_status publish_impl(lam_ctx* c, uint64_t v, int32_t rank, const lam_s
     }
     sub = rp.d_sub;
   }
-  int rc = launch_pack(rp.d_units, rp.n_units, rp.d_ptrs, slot_data(p, s), m, rp.d_units_per_chunk, v,
+  uint8_t* dst = slot_data(p, s);
+  if (p.mc) {   // NEXT-2: store through the multicast VA (the switch replicates into every relay GPU)
+    if (!c->mc.mc_va) return LAM_ECUDA;
+    dst = c->mc.mc_va + (uint64_t)s * p.slot_stride;
+    m.mc_flags = reinterpret_cast<uint64_t*>(c->mc.mc_va + c->mc.flags_off + (uint64_t)s * c->mc.flag_stride);
+  }
+  int rc = launch_pack(rp.d_units, rp.n_units, rp.d_ptrs, dst, m, rp.d_units_per_chunk, v,
                        c->plan.total_chunks, c->dev[dev].d_chunk_len, c->pack_ctas, side, sub,
                        c->dev[dev].d_pack_work, c->pack_sms);
   if (rc) {
@@ -1556,6 +1659,8 @@ extern "C" lam_status lam_read_image(lam_ctx* c, int32_t node, uint64_t v, uint6
     uint64_t n = std::min(end, rend) - off;
     const Part& p = c->parts[c->node_rank_part[node][r]];
     const uint8_t* src = slot_data(p, s) + p.rank_off[r] + (off - c->plan.chunk_base[r] * C);
+    // own parts: copy from their device (a multicast member is mapped for its own GPU only)
+    if (p.local) CK(cudaSetDevice(p.device));
     CK(cudaMemcpy(h, src, n, cudaMemcpyDefault));
     h += n;
     off += n;
@@ -1685,6 +1790,9 @@ extern "C" void lam_destroy(lam_ctx* c) {
       if (p.ipc_opened) cudaIpcCloseMemHandle(p.meta);
       else if (p.local && p.meta) { cudaSetDevice(p.device); cudaFree(p.meta); }
       p.base = nullptr;
+    } else if (p.mc) {
+      if (p.ipc_opened) cudaIpcCloseMemHandle(p.meta);
+      else if (p.local && p.meta) { cudaSetDevice(p.device); cudaFree(p.meta); }
     } else if (p.ipc_opened && p.base) {
       cudaIpcCloseMemHandle(p.base);
     }
@@ -1696,6 +1804,7 @@ extern "C" void lam_destroy(lam_ctx* c) {
     if (p.d_my_chunks) cudaFree(p.d_my_chunks);
     for (cudaEvent_t e : p.chunk_ev) cudaEventDestroy(e);
     if (p.vstream) cudaStreamDestroy(p.vstream);
+    if (p.cstream2) cudaStreamDestroy(p.cstream2);
     if (p.base) cudaFree(p.base);
     if (p.err_host) cudaFreeHost(p.err_host);
     for (int s = 0; s < LAM_MAX_SLOTS; ++s)
@@ -1708,6 +1817,7 @@ extern "C" void lam_destroy(lam_ctx* c) {
   for (auto& kv : c->tev_pool)
     for (cudaEvent_t e : kv.second) cudaEventDestroy(e);
   for (auto& t : c->timed) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }
+  mc_release(c->mc);
   if (c->shm_registered) cudaHostUnregister(c->shm);
   shm_release(c->shm, c->cfg.shm_name, c->shm_mapped, c->shm_owner);
   delete c;

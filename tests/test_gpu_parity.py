@@ -319,6 +319,71 @@ def test_version_rules_and_busy():
     ctx.close()
 
 
+def test_tiny_multicast_broadcast():
+    """NEXT-2: LAM_HOP_MULTICAST — the pack stores the image once through an NVSwitch
+    multicast object; every relay (one per other GPU; all on GPU 0 with one GPU) verifies and commits it
+    from its local replica.  Three versions with specials, full image/header compare at every node and
+    TP=1 / TP=2 pulls at every relay against the oracle."""
+    n = ngpu()
+    od = OMODELS["tiny"]
+    C = 8 * 4096
+    relays = [[d] for d in range(1, n)] if n >= 2 else [[0], [0]]
+    rollouts = [(i + 1, relays[i][0]) for i in range(len(relays))]
+    try:
+        ctx = make_ctx("tiny", 1, [0], relays, rollouts, C=C, hop_mode=lam.LAM_HOP_MULTICAST)
+    except lam.LamError as e:
+        if e.status == lam.LAM_EINVAL:
+            pytest.skip("multicast objects not supported on this box (no NVSwitch / fabric manager)")
+        raise
+    shard = ActorShard(MODELS["tiny"], 1, 0, 0)
+    plan = image_plan([s for _, s in otensors(od)], 1, C)
+    for v in (1, 2, 3):
+        publish_all(ctx, [shard], v, True)
+        until_idle(ctx)
+        oimg, ohdr = publish(plan, SEED, v, specials=True)
+        for node in range(len(relays) + 1):
+            assert ctx.latest(node) == v
+            check_image(ctx, node, v, oimg, ohdr, C)
+        for rid, (_, dev) in enumerate(rollouts):
+            check_pull(ctx, rid, 1, 0, dev, v, True, od)
+            check_pull(ctx, rid, 2, v % 2, dev, v, True, od)
+    st = ctx.stats()
+    assert st["publishes"] == 3 and st["hops_launched"] == 3 * len(relays) and st["checksum_errors"] == 0
+    ctx.close()
+
+
+def test_multicast_corrupt_replica_is_never_committed():
+    """A byte flipped in node 0's slot after the multicast pack: the replicas got the bytes the pack
+    checksummed, so only a relay on the actor GPU (whose replica IS node 0's slot) sees the flipped
+    byte — its k_hop rejects the version and it keeps serving v1."""
+    C = 16 * 4096
+    try:
+        ctx = make_ctx("tiny", 1, [0], [[0]], [(1, 0)], C=C, hop_mode=lam.LAM_HOP_MULTICAST)
+    except lam.LamError as e:
+        if e.status == lam.LAM_EINVAL:
+            pytest.skip("multicast objects not supported on this box")
+        raise
+    shard = ActorShard(MODELS["tiny"], 1, 0, 0)
+    publish_all(ctx, [shard], 1, False)
+    until_idle(ctx)
+    assert ctx.latest(1) == 1
+    publish_all(ctx, [shard], 2, False)
+    torch.cuda.synchronize()                                # pack done, relay hop not launched yet
+    ptr = ctx.debug_region(0, 2, 0) + 5 * C + 1000
+    byte = torch.empty(1, dtype=torch.uint8, device="cuda:0")
+    _memcpy(byte.data_ptr(), ptr, 1)
+    byte ^= 0xFF
+    _memcpy(ptr, byte.data_ptr(), 1)
+    torch.cuda.synchronize()
+    with pytest.raises(lam.LamError) as e:
+        until_idle(ctx)
+    assert e.value.status == lam.LAM_ECHECKSUM
+    until_idle(ctx)
+    assert ctx.latest(0) == 2 and ctx.latest(1) == 1
+    check_pull(ctx, 0, 1, 0, 0, 1, False, OMODELS["tiny"])
+    ctx.close()
+
+
 @pytest.mark.parametrize("hop_mode", HOP_MODES)
 def test_corrupt_chunk_is_never_committed(hop_mode):
     """A byte flipped in the master's slot after packing: the relay's checksum rejects the version,
