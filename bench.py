@@ -283,6 +283,17 @@ def _oracle_pull_tensor(t):
     return 0
 
 
+def line_config(args, N):
+    """The `config` object of the JSON line — identical for the lam arm and the reference arm (the
+    driver compares the two arms only on the same config)."""
+    T = topology(args.config if args.config != "stress" else "chain", N, args.tp)
+    return dict(workload=f"{args.model} [{args.config}]: " + T["desc"],
+                model=f"Qwen2.5-{args.model.upper()}-shaped", params=int(P_params(args.model)),
+                snapshot_bytes=int(2 * P_params(args.model)), global_batch=None, seq_len=None,
+                parallelism=f"{args.config} N={N}" + ("" if args.hop_mode == "kernel" else f" hop={args.hop_mode}"),
+                l2="inputs (fp32 masters, slots) >> 126 MB L2")
+
+
 def run_reference(args):
     """The reference arm of this tier: the CPU oracle, as it stands, timed on the host cores on the lam
     arm's workload — every timed step a FULL publish -> relay -> TP=1 pull of the snapshot on a process
@@ -312,9 +323,8 @@ def run_reference(args):
     out = dict(metric=METRIC, value=value, unit=UNIT, impl="reference", n_gpus=N, steps=args.steps,
                warmup=args.warmup, ms_per_step=value * 1e3, higher_is_better=False, scaling="weak",
                vs_baseline=None, dtype="bf16", data="synthetic",
-               config=dict(workload=f"{args.model} [{args.config}]: " + desc,
-                           model=f"Qwen2.5-{args.model.upper()}-shaped",
-                           reference="CPU oracle publish -> relay -> TP=1 pull, full snapshot per step"),
+               config=line_config(args, N),
+               reference="CPU oracle publish -> relay -> TP=1 pull, full snapshot per step",
                cpu_baseline=dict(kind="oracle", cores=o.workers, value=value, unit=UNIT, sample=sample,
                                  measured="full step", host=hi, wall_s=round(wall, 2),
                                  setup_s=round(time.perf_counter() - t_setup - wall, 2),
@@ -1019,10 +1029,7 @@ def main():
             metric=METRIC, value=M["sec"], unit=UNIT, n_gpus=N, steps=args.steps, warmup=args.warmup,
             ms_per_step=M["ms_per_step"], higher_is_better=False, scaling="weak", vs_baseline=None, dtype="bf16",
             data="synthetic",
-            config=dict(workload=f"{args.model} [{args.config}]: " + T["desc"],
-                        model=f"Qwen2.5-{args.model.upper()}-shaped", params=None, snapshot_bytes=None,
-                        global_batch=None, seq_len=None, parallelism=f"{args.config} N={N}",
-                        l2="inputs (fp32 masters, slots) >> 126 MB L2"),
+            config=line_config(args, N),
             roofline=M["roofline"], nvlink_bound=M["nvlink_bound"], kernels_ms=M["kernels_ms"],
             per_rank=M["per_rank"], host_latency_ms=M["host_latency_ms"], pull_latency=plat,
             paper_context="actor stall 0.64 s (32B) / 1.40 s (72B); 72B to 127 relays < 1.6 s on 128x8 H800 + RDMA",
@@ -1298,7 +1305,7 @@ def run_stress(args, D: Dist):
     mean_s = 2 * args.stress_ms / 1e3
     next_pull = {rid: t_start + rng[rid].exponential(mean_s) for rid in P.mine}
     records, lat, samples, stale = [], [], [], []
-    pub_host, rd_wait, pub_t, commit_t = [], [], {}, {}
+    pub_host, rd_wait, pub_t, commit_t, pub_busy = [], [], {}, {}, []
     seen = [0] * n_nodes
     rd_prev = g_prev = None
     inflight = {}                # rid -> (version, event, t_call, latest_at_call)
@@ -1326,10 +1333,13 @@ def run_stress(args, D: Dist):
                 sh.fill(SEED, v, stream=P.actor_stream.cuda_stream)
             rd = live_event(torch)
             t0 = time.perf_counter()
+            busy = 0
             for r, sh in P.shards.items():
                 while ctx.publish(v, r, sh.shards(), P.actor_stream.cuda_stream, rd.cuda_event) == lam.LAM_EBUSY:
+                    busy += 1
                     ctx.relay_step()
             pub_host.append(time.perf_counter() - t0)
+            pub_busy.append(busy)
             pub_t[v] = time.time()
             rd_prev = rd
         ctx.relay_step()
@@ -1380,7 +1390,7 @@ def run_stress(args, D: Dist):
     stats = ctx.stats()
     mine = dict(lat=lat, stale=stale, n=len(records), torn=sum(not r.content_ok for r in records), viol=viol[:8],
                 nviol=len(viol), pub_host=pub_host, rd_wait=[w0.elapsed_time(w1) for w0, w1 in rd_wait],
-                pub_t=pub_t)
+                pub_t=pub_t, pub_busy=pub_busy)
     allr = D.gather(mine)
     out = None
     if rank == 0:
@@ -1392,7 +1402,9 @@ def run_stress(args, D: Dist):
         ph = [x * 1e3 for a in allr for x in a["pub_host"]]
         rw = [x for a in allr for x in a["rd_wait"]]
         stall = sorted(h + w for h, w in zip(ph[1:], rw))
-        phs, rws = sorted(ph), sorted(rw)
+        # the first publish of a shard list builds the pack plan (one-time set-up, reported apart)
+        phs, rws = sorted(ph[1:]), sorted(rw)
+        busy = [b for a in allr for b in a["pub_busy"][1:]]
         out = dict(metric=METRIC, value=(pct(commit, 0.5) / 1e3 if commit else None), unit=UNIT, n_gpus=N,
                    steps=steps, warmup=0, ms_per_step=pct(commit, 0.5), higher_is_better=False, scaling="weak",
                    vs_baseline=None, dtype="bf16", data="synthetic",
@@ -1406,7 +1418,12 @@ def run_stress(args, D: Dist):
                        actor_stall_ms=dict(p50=pct(stall, 0.5), p99=pct(stall, 0.99), max=stall[-1] if stall else None,
                                            what="host time in lam_publish + actor-stream wait on reads_done "
                                                 "before the next optimizer write"),
-                       publish_host_ms=dict(p50=pct(phs, 0.5), p99=pct(phs, 0.99)),
+                       publish_host_ms=dict(p50=pct(phs, 0.5), p99=pct(phs, 0.99), first=round(ph[0], 3) if ph else None,
+                                            what="host time in lam_publish (+ LAM_EBUSY retries) after the first "
+                                                 "publish; first = one-time pack-plan build"),
+                       publish_busy=dict(publishes_that_waited=sum(1 for b in busy if b), of=len(busy),
+                                         what="LAM_EBUSY: every node-0 slot was packing, latest, or being read "
+                                              "by relay 1 — the publish waited for one (back-pressure)"),
                        reads_done_wait_ms=dict(p50=pct(rws, 0.5), p99=pct(rws, 0.99)),
                        pull_latency_ms=dict(p50=pct(lat_all, 0.5), p99=pct(lat_all, 0.99), n=len(lat_all)),
                        staleness_versions=dict(p50=pct(st_all, 0.5), p99=pct(st_all, 0.99),

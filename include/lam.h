@@ -320,6 +320,10 @@ lam_status lam_pull_bytes(lam_ctx*, int32_t rollout_id, const lam_tp_layout* lay
 /* Test hook: device pointer (valid in this process) of actor rank `rank`'s region of the slot
  * holding `version` (FILLING or COMPLETE) at `node`.  Used by fault-injection tests only. */
 lam_status lam_debug_region(lam_ctx*, int32_t node, uint64_t version, int32_t rank, void** dev_ptr);
+/* Test hook (LAM_HOP_MULTICAST): device pointer of actor rank `rank`'s region in device `device`'s
+ * multicast replica of node 0's slot holding `version` (the device must be a team GPU of this
+ * process).  LAM_EINVAL in the other hop modes.  Used by fault-injection tests only. */
+lam_status lam_debug_replica(lam_ctx*, int32_t device, uint64_t version, int32_t rank, void** dev_ptr);
 
 /* Model table of the library (independent of any caller-side copy). */
 int32_t lam_model_n_tensors(const lam_model_dims*);

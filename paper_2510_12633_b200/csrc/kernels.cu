@@ -95,7 +95,16 @@ __device__ __forceinline__ uint32_t rne_bf16(uint32_t u) {
   uint32_t r = (u + 0x7FFFu + ((u >> 16) & 1u)) >> 16;
   return ((u & 0x7FFFFFFFu) > 0x7F800000u) ? 0x7FC0u : r;
 }
-__device__ __forceinline__ uint32_t pack2(uint32_t lo, uint32_t hi) { return rne_bf16(lo) | (rne_bf16(hi) << 16); }
+// Two elements at once on the conversion unit: cvt.rn.bf16x2.f32 (F2FP) rounds to nearest even, keeps
+// subnormals and overflows to inf exactly like rne_bf16 (tools/cvt_probe.cu on the box: 0 mismatches over
+// all 2^32 non-NaN patterns); its NaN result (0x7FFF) is replaced by 0x7FC0 (HSET2 NaN mask + LOP3).
+// 3 instructions per 2 elements instead of ~16.
+__device__ __forceinline__ uint32_t pack2(uint32_t lo, uint32_t hi) {
+  uint32_t d, m;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(__uint_as_float(hi)), "f"(__uint_as_float(lo)));
+  asm("set.nan.u32.bf16x2 %0, %1, %1;" : "=r"(m) : "r"(d));
+  return (d & ~m) | (0x7FC07FC0u & m);
+}
 
 // checksum contribution of 4 consecutive words starting at word index i0:
 //   S1 += sum w, S2 += sum (i+1) w = (i0+1)*sum + w1 + 2 w2 + 3 w3      (mod 2^64)

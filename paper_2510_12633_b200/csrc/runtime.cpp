@@ -73,8 +73,6 @@ struct Part {
   RankLink* d_links = nullptr;       // [S][S][N] (my slot, pred slot, rank)
   // copy-engine hop mode
   cudaStream_t vstream = nullptr;    // verify stream
-  cudaStream_t cstream2 = nullptr;   // second copy stream: odd chunks (two copies in flight hide the
-                                     // copy engines' per-copy start-up, ~16 us per 128 MiB copy)
   std::vector<uint32_t> my_chunks;   // this part's chunks in processing order
   uint32_t* d_my_chunks = nullptr;
   std::vector<cudaEvent_t> chunk_ev; // [n_my + 1]: per-chunk copy done, last = verify stream done
@@ -483,7 +481,6 @@ lam_status alloc_parts(lam_ctx* c) {
         CK(cudaMemcpy(p.d_my_chunks, p.my_chunks.data(), 4 * p.my_chunks.size(), cudaMemcpyHostToDevice));
       if (c->cfg.hop_mode == LAM_HOP_COPY_ENGINE) {
         CK(cudaStreamCreateWithPriority(&p.vstream, cudaStreamNonBlocking, lo));
-        CK(cudaStreamCreateWithPriority(&p.cstream2, cudaStreamNonBlocking, lo));
         p.chunk_ev.resize(p.my_chunks.size() + 1);
         for (auto& e : p.chunk_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
       }
@@ -654,8 +651,7 @@ lam_status ce_topup(lam_ctx* c, Part& p) {
     const uint64_t off = (g - c->plan.chunk_base[r]) * c->plan.C, len = c->plan.chunk_len(g);
     const uint8_t* src = slot_data(q, ps) + q.rank_off[r] + off;
     uint8_t* dst = slot_data(p, s) + p.rank_off[r] + off;
-    // alternate chunks between two copy streams (the verify stream orders the commits)
-    cudaStream_t cs = (i & 1u) && p.cstream2 ? p.cstream2 : p.stream;
+    cudaStream_t cs = p.stream;
     if (!mir) {
       lam_status st = stream_wait_flag(c, cs, qm.flags + g, u, m.abort_flag);
       if (st != LAM_OK) return st;
@@ -836,10 +832,6 @@ lam_status launch_hop_part(lam_ctx* c, Part& p, int s, bool* launched) {
     p.ce_next = 0;
     p.ce_version = u;
     p.ce_t0 = t0;
-    if (p.cstream2) {   // the second copy stream starts after this hop's set-up (and same-GPU waits)
-      CK(cudaEventRecord(p.chunk_ev.back(), p.stream));
-      CK(cudaStreamWaitEvent(p.cstream2, p.chunk_ev.back(), 0));
-    }
     sl.launched_mask |= 1ull << p.pos;
     c->shm->stats.hops_launched++;
     *launched = true;
@@ -967,6 +959,17 @@ lam_status step_locked(lam_ctx* c, int* transitions, bool* busy) {
         memset(p.prof_host, 0, 64);
       }
       const lam_status e = p.err_host[s] ? -(lam_status)p.err_host[s] : LAM_OK;
+      if (e != LAM_OK && getenv("LAM_DEBUG_FAIL")) {   // diagnostics: which chunk failed first
+        std::vector<uint64_t> f(c->plan.total_chunks);
+        ChunkMeta fm = meta_of(c, p, s);
+        if (cudaMemcpy(f.data(), fm.flags, 8 * f.size(), cudaMemcpyDeviceToHost) == cudaSuccess)
+          for (size_t g = 0; g < f.size(); ++g)
+            if (f[g] & kPoison) {
+              fprintf(stderr, "liblam: node %d dev %d slot %d v%llu: chunk %zu of %zu failed (%s)\n", p.node, p.device,
+                      s, (unsigned long long)p.inflight_version[s], g, f.size(), lam_strerror(e));
+              break;
+            }
+      }
       if (ctl::part_done(sh, p.node, s, p.inflight_version[s], (int)c->node_parts[p.node].size(), e,
                          p.launched_epoch[s])) {
         (*transitions)++;
@@ -1744,6 +1747,20 @@ extern "C" lam_status lam_debug_region(lam_ctx* c, int32_t node, uint64_t v, int
   return LAM_OK;
 }
 
+extern "C" lam_status lam_debug_replica(lam_ctx* c, int32_t device, uint64_t v, int32_t rank, void** ptr) {
+  if (!c || !ptr || rank < 0 || rank >= c->cfg.fsdp_size || !c->star) return LAM_EINVAL;
+  Lock l(c->shm);
+  auto it = c->mc.va.find(device);
+  if (it == c->mc.va.end()) return LAM_EINVAL;
+  const ShmNode& n = c->shm->node[0];
+  int s = find_slot(n, c->S, v, S_COMPLETE);
+  if (s < 0) s = find_slot(n, c->S, v, S_FILLING);
+  if (s < 0) return LAM_ENOVERSION;
+  const Part& p0 = c->parts[c->node_rank_part[0][rank]];
+  *ptr = it->second + (uint64_t)s * p0.slot_stride + p0.rank_off[rank];
+  return LAM_OK;
+}
+
 extern "C" void lam_destroy(lam_ctx* c) {
   if (!c) return;
   for (Part& p : c->parts) {
@@ -1804,7 +1821,6 @@ extern "C" void lam_destroy(lam_ctx* c) {
     if (p.d_my_chunks) cudaFree(p.d_my_chunks);
     for (cudaEvent_t e : p.chunk_ev) cudaEventDestroy(e);
     if (p.vstream) cudaStreamDestroy(p.vstream);
-    if (p.cstream2) cudaStreamDestroy(p.cstream2);
     if (p.base) cudaFree(p.base);
     if (p.err_host) cudaFreeHost(p.err_host);
     for (int s = 0; s < LAM_MAX_SLOTS; ++s)

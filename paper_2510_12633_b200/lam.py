@@ -128,6 +128,7 @@ def load() -> C.CDLL:
         "lam_set_profiling": (C.c_int32, [V, C.c_int32]),
         "lam_kernel_times": (C.c_int32, [V, P(C.c_double), P(C.c_uint64)]),
         "lam_debug_region": (C.c_int32, [V, C.c_int32, C.c_uint64, C.c_int32, P(V)]),
+        "lam_debug_replica": (C.c_int32, [V, C.c_int32, C.c_uint64, C.c_int32, P(V)]),
         "lam_model_n_tensors": (C.c_int32, [P(lam_model_dims)]),
         "lam_model_tensor": (C.c_int32, [P(lam_model_dims), C.c_int32, C.c_char_p, C.c_int32,
                                          P(C.c_int64), P(C.c_int32)]),
@@ -153,7 +154,7 @@ def load() -> C.CDLL:
 
 EXPORTED = ["lam_config_size", "lam_init", "lam_export_ipc", "lam_import_ipc", "lam_connect", "lam_destroy", "lam_strerror",
             "lam_publish", "lam_relay_step", "lam_pull", "lam_latest", "lam_get_plan_info", "lam_get_stats",
-            "lam_read_image", "lam_read_headers", "lam_debug_region", "lam_set_profiling", "lam_kernel_times", "lam_pull_bytes", "lam_model_n_tensors", "lam_model_tensor", "lam_vllm_layout",
+            "lam_read_image", "lam_read_headers", "lam_debug_region", "lam_debug_replica", "lam_set_profiling", "lam_kernel_times", "lam_pull_bytes", "lam_model_n_tensors", "lam_model_tensor", "lam_vllm_layout",
             "lam_plan_segments", "lam_plan_copy_tiles", "lam_optimal_chunks", "lam_chain_latency"]
 
 
@@ -413,6 +414,11 @@ class Context:
     def debug_region(self, node: int, version: int, rank: int) -> int:
         p = C.c_void_p()
         _check(self.L.lam_debug_region(self.h, node, version, rank, C.byref(p)), "lam_debug_region")
+        return p.value
+
+    def debug_replica(self, device: int, version: int, rank: int) -> int:
+        p = C.c_void_p()
+        _check(self.L.lam_debug_replica(self.h, device, version, rank, C.byref(p)), "lam_debug_replica")
         return p.value
 
     def close(self) -> None:

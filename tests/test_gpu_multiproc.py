@@ -42,6 +42,7 @@ CASES = [  # (min GPUs, args)
     (2, ["--config", "host", "--model", "tiny", "--versions", "3"]),                 # NEXT-3 host tier
     (4, ["--config", "host", "--model", "tiny", "--tp", "2", "--stream"]),
     (4, ["--config", "host", "--model", "tiny", "--versions", "2", "--hop-mode", "1"]),
+    (2, ["--config", "chain", "--model", "7b", "--chunk-kb", str(128 << 10), "--hop-mode", "1"]),   # CE, 7B
     # NEXT-2 multicast broadcast: the multicast object crosses processes (SCM_RIGHTS), every relay
     # verifies its replica
     (2, ["--config", "chain", "--model", "tiny", "--versions", "3", "--hop-mode", "2"]),

@@ -321,13 +321,15 @@ def test_version_rules_and_busy():
 
 def test_tiny_multicast_broadcast():
     """NEXT-2: LAM_HOP_MULTICAST — the pack stores the image once through an NVSwitch
-    multicast object; every relay (one per other GPU; all on GPU 0 with one GPU) verifies and commits it
+    multicast object; every relay (one per other GPU) verifies and commits it
     from its local replica.  Three versions with specials, full image/header compare at every node and
     TP=1 / TP=2 pulls at every relay against the oracle."""
     n = ngpu()
+    if n < 2:
+        pytest.skip("multicast needs >= 2 GPUs (a one-device multicast team is invalid)")
     od = OMODELS["tiny"]
     C = 8 * 4096
-    relays = [[d] for d in range(1, n)] if n >= 2 else [[0], [0]]
+    relays = [[d] for d in range(1, n)]
     rollouts = [(i + 1, relays[i][0]) for i in range(len(relays))]
     try:
         ctx = make_ctx("tiny", 1, [0], relays, rollouts, C=C, hop_mode=lam.LAM_HOP_MULTICAST)
@@ -353,12 +355,14 @@ def test_tiny_multicast_broadcast():
 
 
 def test_multicast_corrupt_replica_is_never_committed():
-    """A byte flipped in node 0's slot after the multicast pack: the replicas got the bytes the pack
-    checksummed, so only a relay on the actor GPU (whose replica IS node 0's slot) sees the flipped
-    byte — its k_hop rejects the version and it keeps serving v1."""
+    """A byte flipped in GPU 1's multicast replica of node 0's slot after the pack: relay 1's k_hop
+    recomputes the checksum from that replica, rejects the version, and keeps serving v1 (SPEC L643);
+    node 0 itself is intact."""
+    if ngpu() < 2:
+        pytest.skip("multicast needs >= 2 GPUs (a one-device multicast team is invalid)")
     C = 16 * 4096
     try:
-        ctx = make_ctx("tiny", 1, [0], [[0]], [(1, 0)], C=C, hop_mode=lam.LAM_HOP_MULTICAST)
+        ctx = make_ctx("tiny", 1, [0], [[1]], [(1, 1)], C=C, hop_mode=lam.LAM_HOP_MULTICAST)
     except lam.LamError as e:
         if e.status == lam.LAM_EINVAL:
             pytest.skip("multicast objects not supported on this box")
@@ -369,18 +373,19 @@ def test_multicast_corrupt_replica_is_never_committed():
     assert ctx.latest(1) == 1
     publish_all(ctx, [shard], 2, False)
     torch.cuda.synchronize()                                # pack done, relay hop not launched yet
-    ptr = ctx.debug_region(0, 2, 0) + 5 * C + 1000
-    byte = torch.empty(1, dtype=torch.uint8, device="cuda:0")
-    _memcpy(byte.data_ptr(), ptr, 1)
-    byte ^= 0xFF
-    _memcpy(ptr, byte.data_ptr(), 1)
-    torch.cuda.synchronize()
+    ptr = ctx.debug_replica(1, 2, 0) + 5 * C + 1000
+    with torch.cuda.device(1):
+        byte = torch.empty(1, dtype=torch.uint8, device="cuda:1")
+        _memcpy(byte.data_ptr(), ptr, 1)
+        byte ^= 0xFF
+        _memcpy(ptr, byte.data_ptr(), 1)
+        torch.cuda.synchronize()
     with pytest.raises(lam.LamError) as e:
         until_idle(ctx)
     assert e.value.status == lam.LAM_ECHECKSUM
     until_idle(ctx)
     assert ctx.latest(0) == 2 and ctx.latest(1) == 1
-    check_pull(ctx, 0, 1, 0, 0, 1, False, OMODELS["tiny"])
+    check_pull(ctx, 0, 1, 0, 1, 1, False, OMODELS["tiny"])
     ctx.close()
 
 
