@@ -135,6 +135,8 @@ typedef struct {
   int32_t pack_sms;                        /* > 0: the pack runs on SMs 0..pack_sms-1 only (every SM
                                               fully occupied), leaving the others to the trainer's
                                               kernels (actor stall); 0 = all SMs */
+  int32_t hybrid_mc_pct;                   /* LAM_HOP_HYBRID: share of the chunks (percent, spread evenly)
+                                              that go by multicast; 0 => 60 */
 } lam_config;
 
 /* How a relay moves a chunk from its predecessor (all chunk-pipelined and verified):
@@ -151,7 +153,16 @@ typedef struct {
  *                       forward nothing.  Requires every actor rank on one GPU, HBM relay nodes, node-0
  *                       rollouts on that GPU, and multicast-capable devices (NVSwitch); costs each relay
  *                       GPU S extra image-sized replicas.  LAM_EINVAL otherwise. */
-enum { LAM_HOP_KERNEL = 0, LAM_HOP_COPY_ENGINE = 1, LAM_HOP_MULTICAST = 2 };
+/*  LAM_HOP_HYBRID       both at once (B200-native; NEXT-2 and the chain of P:L661-665 share the links):
+ *                       the pack multicasts a share of the chunks (hybrid_mc_pct) into every relay GPU's
+ *                       replica and stores the others locally; each relay's k_hop takes the multicast
+ *                       chunks from its replica (local HBM) and pulls the rest from its chain
+ *                       predecessor, verifying all of them.  A relay GPU's ingress is still M, but the
+ *                       multicast share costs no relay egress and no read requests, so the middle of the
+ *                       chain no longer both serves and receives the whole image.  Same requirements as
+ *                       LAM_HOP_MULTICAST, plus no relay part on the actor GPU.  A relay that starts a
+ *                       version node 0 no longer holds pulls every chunk from its predecessor. */
+enum { LAM_HOP_KERNEL = 0, LAM_HOP_COPY_ENGINE = 1, LAM_HOP_MULTICAST = 2, LAM_HOP_HYBRID = 3 };
 
 /* One fp32 master shard piece owned by the caller: elements [elem_offset, elem_offset+elem_count)
  * of the flattened tensor `tensor_id`, at `ptr` (device memory of the actor rank's GPU). */

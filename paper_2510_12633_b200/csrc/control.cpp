@@ -137,16 +137,24 @@ static void open_slot(ShmSlot& sl, uint64_t v, int src_slot) {
   sl.parts_done = sl.parts_finished = 0;
   sl.err = 0;
   sl.src_slot = src_slot;
+  sl.src0_slot = -1;
   sl.launched_mask = 0;
   sl.epoch++;
 }
 
-void init(Shm* sh, int n_nodes, bool star) {
+void init(Shm* sh, int n_nodes, bool star, bool hybrid) {
   sh->n_nodes = n_nodes;
+  sh->hybrid = hybrid ? 1 : 0;
   for (int i = 0; i <= LAM_MAX_NODES; ++i) {
     sh->node[i].dead = 0;
     sh->node[i].pred = star && i > 0 ? 0 : i - 1;
   }
+}
+
+// A hybrid fill's pin of node 0's slot (the multicast source) ends with the fill.
+static void unpin_src0(Shm* sh, ShmSlot& sl) {
+  if (sl.src0_slot >= 0 && sh->node[0].slot[sl.src0_slot].readers > 0) sh->node[0].slot[sl.src0_slot].readers--;
+  sl.src0_slot = -1;
 }
 
 bool fail_node(Shm* sh, int S, int node, uint64_t now_ns) {
@@ -161,6 +169,7 @@ bool fail_node(Shm* sh, int S, int node, uint64_t now_ns) {
     ShmSlot& sl = d.slot[s];
     if (sl.state == S_FILLING) {
       if (sl.src_slot >= 0 && sh->node[d.pred].slot[sl.src_slot].readers > 0) sh->node[d.pred].slot[sl.src_slot].readers--;
+      unpin_src0(sh, sl);
       sl.state = S_FREE;
       sl.version = 0;
       sl.src_slot = -1;
@@ -184,6 +193,7 @@ bool fail_node(Shm* sh, int S, int node, uint64_t now_ns) {
         sl.parts_done = sl.parts_finished = 0;
         sl.epoch++;
       } else {                             // abandon: start over with what the new predecessor has
+        unpin_src0(sh, sl);
         sl.state = S_FREE;
         sl.version = 0;
         sl.src_slot = -1;
@@ -248,6 +258,15 @@ int start(Shm* sh, int S, int node, bool* started) {
   }
   open_slot(n.slot[s], u, ps);
   pred.slot[ps].readers++;
+  if (sh->hybrid && node > 0) {              // multicast share of v: node 0's slot, if it still holds v
+    ShmNode& n0 = sh->node[0];
+    int s0 = find_slot(n0, S, u, S_COMPLETE);
+    if (s0 < 0) s0 = find_slot(n0, S, u, S_FILLING);
+    if (s0 >= 0) {
+      n0.slot[s0].readers++;
+      n.slot[s].src0_slot = s0;
+    }
+  }
   n.started = u;
   *started = true;
   return s;
@@ -269,6 +288,7 @@ bool part_done(Shm* sh, int node, int slot, uint64_t v, int n_parts, lam_status 
       ShmSlot& src = sh->node[n.pred].slot[sl.src_slot];
       if (src.readers > 0) src.readers--;
     }
+    unpin_src0(sh, sl);
     if (sl.err == 0) {
       sl.state = S_COMPLETE;
       if (v > n.latest) n.latest = v;

@@ -28,7 +28,8 @@ struct ShmSlot {
   int32_t parts_done, parts_finished;  // node 0: ranks packed; relays: parts completed ok / at all
   int32_t err, src_slot;               // first error; predecessor slot pinned while FILLING
   uint64_t launched_mask;              // node 0: ranks published; relays: parts launched
-  uint32_t epoch, _pad;                // bumped when the fill restarts from a new predecessor
+  uint32_t epoch;                      // bumped when the fill restarts from a new predecessor
+  int32_t src0_slot;                   // hybrid broadcast: node 0's slot pinned as the multicast source
 };
 struct ShmNode {
   ShmSlot slot[LAM_MAX_SLOTS];
@@ -46,6 +47,7 @@ struct Shm {
   uint64_t fail_ns[LAM_MAX_NODES + 1]; // steady-clock time each node was declared failed
   uint64_t hb_ns[LAM_MAX_DEVICES];     // per process heartbeat (steady clock, ns)
   uint64_t dead_procs;                 // bit mask
+  int32_t hybrid, _pad2;               // LAM_HOP_HYBRID: relays also read node 0's multicast replica
   uint64_t last_fail_ns;               // most recent failure (repair-time accounting)
   ShmNode node[LAM_MAX_NODES + 1];
   // Host-visible mirror of every slot's chunk flags, written by the producer kernels through a
@@ -54,7 +56,7 @@ struct Shm {
   uint64_t chunk_done[LAM_MAX_NODES + 1][LAM_MAX_SLOTS][2048];
 };
 constexpr uint32_t kShmMirrorChunks = 2048;
-constexpr uint64_t kMagic = 0x4c414d5f53484d33ull;  // "LAM_SHM3"
+constexpr uint64_t kMagic = 0x4c414d5f53484d34ull;  // "LAM_SHM4"
 
 struct ShmLock {
   pthread_mutex_t* m;
@@ -89,8 +91,10 @@ void unpin(Shm* sh, int node, int slot);
 // Anything FILLING, or a node behind its predecessor?
 bool busy(Shm* sh, int S, int n_nodes);
 // Chain of n_nodes (called once by the creator): every node alive, pred = node - 1; star (the
-// LAM_HOP_MULTICAST broadcast, NEXT-2): every relay's predecessor is node 0.
-void init(Shm* sh, int n_nodes, bool star = false);
+// LAM_HOP_MULTICAST broadcast, NEXT-2): every relay's predecessor is node 0.  hybrid (LAM_HOP_HYBRID):
+// a chain whose relays also read part of every version from node 0's multicast replica, so a relay
+// that starts v also pins node 0's slot of v (while node 0 still holds it) until its fill ends.
+void init(Shm* sh, int n_nodes, bool star = false, bool hybrid = false);
 // Relay failure: mark `node` dead and rebuild the chain in O(1): its successor is
 // linked to its (live) predecessor.  A successor that was filling from it re-pins the same version
 // at the new predecessor and restarts (slot epoch++, launch mask cleared: the runtime resumes from

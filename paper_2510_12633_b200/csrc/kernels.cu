@@ -70,7 +70,7 @@ __device__ __forceinline__ void mc_st_release_u64(uint64_t* p, uint64_t v) {
 // mode: the flag also goes through the switch to every relay GPU's member (after the chunk's data,
 // which took the same path), where that relay polls it in local HBM.
 __device__ __forceinline__ void publish_flag(const ChunkMeta& meta, uint32_t chunk, uint64_t value) {
-  if (meta.mc_flags) mc_st_release_u64(meta.mc_flags + chunk, value);
+  if (meta.mc_flags && (!meta.mc_class || meta.mc_class[chunk])) mc_st_release_u64(meta.mc_flags + chunk, value);
   st_release_sys(meta.flags + chunk, value);
   if (meta.mirror) st_release_sys(meta.mirror + chunk, value);
 }
@@ -167,13 +167,14 @@ __device__ void pack_flush(ChunkMeta meta, const uint32_t* units_per_chunk, cons
 }
 
 // SUB: compiled with the colocated-subscriber stores (separate instantiation: the plain pack keeps
-// its register budget and occupancy).  MC: `dst` is the multicast VA of node 0's slot (NEXT-2): every
-// 16-B store is a multimem.st, so the bf16 image lands in the actor GPU's slot and in every relay
-// GPU's replica in the same pass.
+// its register budget and occupancy).  MC: `mc_dst` is the multicast VA of node 0's slot (NEXT-2): the
+// 16-B stores of a multicast chunk (every chunk, or those meta.mc_class marks — LAM_HOP_HYBRID) are
+// multimem.st, so its bf16 bytes land in the actor GPU's slot and in every relay GPU's replica in the
+// same pass; other chunks go to `dst` (the actor GPU's slot) only.
 template <bool SUB, bool MC>
 __global__ void __launch_bounds__(kPackThreads) k_pack(const PackUnit* __restrict__ units, uint32_t n_units,
                                                        const float* const* __restrict__ shard_ptrs,
-                                                       uint8_t* __restrict__ dst, ChunkMeta meta,
+                                                       uint8_t* __restrict__ dst, uint8_t* mc_dst, ChunkMeta meta,
                                                        const uint32_t* __restrict__ units_per_chunk,
                                                        uint64_t version, uint64_t n_total,
                                                        const uint64_t* __restrict__ chunk_len,
@@ -219,7 +220,8 @@ __global__ void __launch_bounds__(kPackThreads) k_pack(const PackUnit* __restric
       acc_n = 0;
     }
     const float* src = shard_ptrs[u.shard] + u.src_elem;
-    uint8_t* out = dst + u.dst_off;
+    const bool mcs = MC && (!meta.mc_class || meta.mc_class[u.chunk]);   // uniform per unit
+    uint8_t* out = (mcs ? mc_dst : dst) + u.dst_off;
     // colocated subscriber (lam_subscribe): the same bf16 bytes also go to its TP=1 buffer
     uint8_t* out2 = SUB ? sub_dst[ui] : nullptr;
     uint64_t s1 = 0, s2 = 0;
@@ -239,7 +241,7 @@ __global__ void __launch_bounds__(kPackThreads) k_pack(const PackUnit* __restric
           const uint32_t vk = v + k * kPackThreads;
           const uint4 w = make_uint4(pack2(a[k].x, a[k].y), pack2(a[k].z, a[k].w), pack2(b[k].x, b[k].y),
                                      pack2(b[k].z, b[k].w));
-          if (MC) mc_st_v4(out + 16 * (size_t)vk, w); else st_v4(out + 16 * (size_t)vk, w);
+          if (mcs) mc_st_v4(out + 16 * (size_t)vk, w); else st_v4(out + 16 * (size_t)vk, w);
           if (out2) st_v4_any(out2 + 16 * (size_t)vk, w);
           cks4((uint64_t)u.word0 + 4ull * vk, w, s1, s2);
         }
@@ -247,7 +249,7 @@ __global__ void __launch_bounds__(kPackThreads) k_pack(const PackUnit* __restric
       for (; v < nvec; v += kPackThreads) {
         const uint4 a = ld_stream_v4(src + 8 * (size_t)v), b = ld_stream_v4(src + 8 * (size_t)v + 4);
         const uint4 w = make_uint4(pack2(a.x, a.y), pack2(a.z, a.w), pack2(b.x, b.y), pack2(b.z, b.w));
-        if (MC) mc_st_v4(out + 16 * (size_t)v, w); else st_v4(out + 16 * (size_t)v, w);
+        if (mcs) mc_st_v4(out + 16 * (size_t)v, w); else st_v4(out + 16 * (size_t)v, w);
         if (out2) st_v4_any(out2 + 16 * (size_t)v, w);
         cks4((uint64_t)u.word0 + 4ull * v, w, s1, s2);
       }
@@ -256,7 +258,7 @@ __global__ void __launch_bounds__(kPackThreads) k_pack(const PackUnit* __restric
       for (uint32_t v = threadIdx.x; v < nvec; v += kPackThreads) {
         const uint32_t* q = s32 + 8 * (size_t)v;
         const uint4 w = make_uint4(pack2(q[0], q[1]), pack2(q[2], q[3]), pack2(q[4], q[5]), pack2(q[6], q[7]));
-        if (MC) mc_st_v4(out + 16 * (size_t)v, w); else st_v4(out + 16 * (size_t)v, w);
+        if (mcs) mc_st_v4(out + 16 * (size_t)v, w); else st_v4(out + 16 * (size_t)v, w);
         if (out2) st_v4_any(out2 + 16 * (size_t)v, w);
         cks4((uint64_t)u.word0 + 4ull * v, w, s1, s2);
       }
@@ -268,7 +270,7 @@ __global__ void __launch_bounds__(kPackThreads) k_pack(const PackUnit* __restric
       for (uint32_t e = nvec * 8 + 2 * threadIdx.x; e < u.n; e += 2 * kPackThreads) {
         const uint32_t lo = rne_bf16(s32[e]);
         const uint32_t hi = (e + 1 < u.n) ? rne_bf16(s32[e + 1]) : 0u;
-        if (MC) {   // one word (e even, out 16-B aligned); the half past the segment is zero pad anyway
+        if (mcs) {  // one word (e even, out 16-B aligned); the half past the segment is zero pad anyway
           mc_st_b32(o16 + e, lo | (hi << 16));
         } else {
           o16[e] = (uint16_t)lo;
@@ -295,7 +297,7 @@ __global__ void __launch_bounds__(kPackThreads) k_pack(const PackUnit* __restric
   }
 }
 
-int launch_pack(const PackUnit* units, uint32_t n_units, const float* const* shard_ptrs, uint8_t* dst,
+int launch_pack(const PackUnit* units, uint32_t n_units, const float* const* shard_ptrs, uint8_t* dst, uint8_t* mc_dst,
                 ChunkMeta meta, const uint32_t* units_per_chunk, uint64_t version, uint64_t n_total,
                 const uint64_t* chunk_len, int ctas, void* stream, uint8_t* const* sub_dst, uint32_t* work,
                 int sms) {
@@ -307,7 +309,7 @@ int launch_pack(const PackUnit* units, uint32_t n_units, const float* const* sha
   if (ctas <= 0 || sms > 0) ctas = resident_ctas(kern, kPackThreads);
   // confined: the full wave must land everywhere (the CTAs on SMs >= sms leave), not n_units of it
   unsigned grid = (unsigned)(sms > 0 || n_units >= (uint32_t)ctas ? (uint32_t)ctas : n_units);
-  kern<<<grid, kPackThreads, 0, (cudaStream_t)stream>>>(units, n_units, shard_ptrs, dst, meta, units_per_chunk, version,
+  kern<<<grid, kPackThreads, 0, (cudaStream_t)stream>>>(units, n_units, shard_ptrs, dst, mc_dst, meta, units_per_chunk, version,
                                                         n_total, chunk_len, sub_dst, work, (uint32_t)(sms > 0 ? sms : 0));
   return (int)cudaGetLastError();
 }

@@ -7,7 +7,9 @@
 // part) followed by S chunk-flag arrays.  On the actor GPU the member IS node 0's slot data; on a
 // relay GPU it is the local replica ("mirror") of node 0's slots that the relay's verify-and-commit
 // hop reads from local HBM.  The pack stores through the multicast VA (multimem.st), which exists
-// only in the process of the actor GPU.
+// only in the process of the actor GPU.  The actor GPU's member is also handed to the other processes
+// (mapped there, read over NVLink): LAM_HOP_HYBRID relays pull the chunks that do not go by multicast
+// from it.
 //
 // Driver API through cudaGetDriverEntryPoint (the library does not link libcuda).  With one process
 // per GPU the multicast handle (a POSIX file descriptor) travels from the actor's process to the
@@ -122,8 +124,9 @@ socklen_t sock_addr(const char* name, sockaddr_un* a) {
   return (socklen_t)(offsetof(sockaddr_un, sun_path) + 1 + n);
 }
 
-// Owner: hand `fd` to `n_peers` connecting processes (SCM_RIGHTS), waiting at most timeout_ms.
-bool serve_fd(const char* name, int fd, int n_peers, uint64_t timeout_ms) {
+// Owner: hand `fds` (the multicast object, the owner's member) to `n_peers` connecting processes
+// (SCM_RIGHTS), waiting at most timeout_ms.
+bool serve_fd(const char* name, const int fds[2], int n_peers, uint64_t timeout_ms) {
   int ls = socket(AF_UNIX, SOCK_STREAM | SOCK_CLOEXEC, 0);
   if (ls < 0) return false;
   sockaddr_un a;
@@ -147,7 +150,7 @@ bool serve_fd(const char* name, int fd, int n_peers, uint64_t timeout_ms) {
     if (cs < 0) { ok = false; break; }
     char byte = 'm';
     iovec io{&byte, 1};
-    char ctrl[CMSG_SPACE(sizeof(int))] = {};
+    char ctrl[CMSG_SPACE(2 * sizeof(int))] = {};
     msghdr m = {};
     m.msg_iov = &io;
     m.msg_iovlen = 1;
@@ -156,8 +159,8 @@ bool serve_fd(const char* name, int fd, int n_peers, uint64_t timeout_ms) {
     cmsghdr* cm = CMSG_FIRSTHDR(&m);
     cm->cmsg_level = SOL_SOCKET;
     cm->cmsg_type = SCM_RIGHTS;
-    cm->cmsg_len = CMSG_LEN(sizeof(int));
-    memcpy(CMSG_DATA(cm), &fd, sizeof(int));
+    cm->cmsg_len = CMSG_LEN(2 * sizeof(int));
+    memcpy(CMSG_DATA(cm), fds, 2 * sizeof(int));
     ok = sendmsg(cs, &m, 0) == 1;
     close(cs);
   }
@@ -165,14 +168,14 @@ bool serve_fd(const char* name, int fd, int n_peers, uint64_t timeout_ms) {
   return ok;
 }
 
-// Peer: receive the owner's descriptor (retrying until the owner listens).
-int fetch_fd(const char* name, uint64_t timeout_ms) {
+// Peer: receive the owner's two descriptors (retrying until the owner listens).
+bool fetch_fd(const char* name, uint64_t timeout_ms, int fds[2]) {
   const uint64_t t_end = now_ms() + timeout_ms;
   sockaddr_un a;
   const socklen_t al = sock_addr(name, &a);
   while (now_ms() < t_end) {
     int s = socket(AF_UNIX, SOCK_STREAM | SOCK_CLOEXEC, 0);
-    if (s < 0) return -1;
+    if (s < 0) return false;
     if (connect(s, (sockaddr*)&a, al) != 0) {
       close(s);
       usleep(2000);
@@ -180,7 +183,7 @@ int fetch_fd(const char* name, uint64_t timeout_ms) {
     }
     char byte = 0;
     iovec io{&byte, 1};
-    char ctrl[CMSG_SPACE(sizeof(int))] = {};
+    char ctrl[CMSG_SPACE(2 * sizeof(int))] = {};
     msghdr m = {};
     m.msg_iov = &io;
     m.msg_iovlen = 1;
@@ -189,13 +192,12 @@ int fetch_fd(const char* name, uint64_t timeout_ms) {
     const ssize_t r = recvmsg(s, &m, 0);
     close(s);
     cmsghdr* cm = CMSG_FIRSTHDR(&m);
-    if (r != 1 || !cm || cm->cmsg_type != SCM_RIGHTS) return -1;
-    int fd = -1;
-    memcpy(&fd, CMSG_DATA(cm), sizeof(int));
-    return fd;
+    if (r != 1 || !cm || cm->cmsg_type != SCM_RIGHTS || cm->cmsg_len != CMSG_LEN(2 * sizeof(int))) return false;
+    memcpy(fds, CMSG_DATA(cm), 2 * sizeof(int));
+    return true;
   }
   fprintf(stderr, "liblam: multicast: no owner on socket %s\n", name);
-  return -1;
+  return false;
 }
 
 }  // namespace
@@ -237,11 +239,18 @@ lam_status mc_alloc_members(McTeam& t, const std::vector<int>& local_devs, uint6
       return LAM_ECUDA;
     }
     t.va[dev] = (uint8_t*)(uintptr_t)va;
-    CUmemAccessDesc acc = {};
-    acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
-    acc.location.id = dev;
-    acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
-    if (!cu_ok(d.access(va, t.size, &acc, 1), "cuMemSetAccess(member)")) return LAM_ECUDA;
+    // the owner's member (node 0's slots) is also read by this process's other team GPUs (single-process
+    // hybrid relays pull non-multicast chunks from it over NVLink); every other member only locally
+    std::vector<CUmemAccessDesc> acc;
+    for (int other : local_devs)
+      if (other == dev || dev == t.owner_dev) {
+        CUmemAccessDesc a = {};
+        a.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+        a.location.id = other;
+        a.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+        acc.push_back(a);
+      }
+    if (!cu_ok(d.access(va, t.size, acc.data(), acc.size()), "cuMemSetAccess(member)")) return LAM_ECUDA;
     if (cudaMemset((void*)va, 0, t.size) != cudaSuccess) return LAM_ECUDA;   // pad bytes / flags zero
   }
   return LAM_OK;
@@ -255,20 +264,48 @@ lam_status mc_setup(McTeam& t, const std::vector<int>& local_devs, bool owner, i
     CUmulticastObjectProp mp = mc_prop((int)t.devices.size(), t.size);
     if (!cu_ok(d.create(&t.mc, &mp), "cuMulticastCreate")) return LAM_ECUDA;
     if (n_peer_procs > 0) {
-      int fd = -1;
-      if (!cu_ok(d.exp(&fd, t.mc, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0), "cuMemExportToShareableHandle"))
+      // the multicast object, and the owner's member (node 0's slot data: relays of the hybrid mode
+      // pull the chunks that do not go by multicast from it)
+      int fds[2] = {-1, -1};
+      if (!cu_ok(d.exp(&fds[0], t.mc, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0), "cuMemExportToShareableHandle") ||
+          !cu_ok(d.exp(&fds[1], t.mem.at(t.owner_dev), CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0),
+                 "cuMemExportToShareableHandle(member)")) {
+        for (int f : fds)
+          if (f >= 0) close(f);
         return LAM_EIPC;
-      const bool ok = serve_fd(sock, fd, n_peer_procs, timeout_ms);
-      close(fd);
+      }
+      const bool ok = serve_fd(sock, fds, n_peer_procs, timeout_ms);
+      close(fds[0]);
+      close(fds[1]);
       if (!ok) return LAM_EIPC;
     }
   } else {
-    int fd = fetch_fd(sock, timeout_ms);
-    if (fd < 0) return LAM_EIPC;
-    const bool ok = cu_ok(d.imp(&t.mc, (void*)(uintptr_t)fd, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR),
-                          "cuMemImportFromShareableHandle");
-    close(fd);
+    int fds[2] = {-1, -1};
+    if (!fetch_fd(sock, timeout_ms, fds)) return LAM_EIPC;
+    bool ok = cu_ok(d.imp(&t.mc, (void*)(uintptr_t)fds[0], CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR),
+                    "cuMemImportFromShareableHandle");
+    CUmemGenericAllocationHandle om = 0;
+    ok = ok && cu_ok(d.imp(&om, (void*)(uintptr_t)fds[1], CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR),
+                     "cuMemImportFromShareableHandle(member)");
+    close(fds[0]);
+    close(fds[1]);
     if (!ok) return LAM_EIPC;
+    t.owner_imported = om;
+    // map the owner's member here, readable by this process's GPUs (over NVLink)
+    CUdeviceptr va = 0;
+    if (!cu_ok(d.reserve(&va, t.size, 0, 0, 0), "cuMemAddressReserve(owner member)")) return LAM_ECUDA;
+    if (!cu_ok(d.map(va, t.size, 0, om, 0), "cuMemMap(owner member)")) {
+      d.addr_free(va, t.size);
+      return LAM_ECUDA;
+    }
+    t.owner_va = (uint8_t*)(uintptr_t)va;
+    std::vector<CUmemAccessDesc> acc(local_devs.size());
+    for (size_t i = 0; i < local_devs.size(); ++i) {
+      acc[i].location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+      acc[i].location.id = local_devs[i];
+      acc[i].flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    }
+    if (!cu_ok(d.access(va, t.size, acc.data(), acc.size()), "cuMemSetAccess(owner member)")) return LAM_ECUDA;
   }
   for (int dev : local_devs) {
     CUdevice cd;
@@ -300,6 +337,13 @@ lam_status mc_setup(McTeam& t, const std::vector<int>& local_devs, bool owner, i
 void mc_release(McTeam& t) {
   const Drv& d = drv();
   if (!d.ok) return;
+  if (t.owner_va) {
+    d.unmap((CUdeviceptr)(uintptr_t)t.owner_va, t.size);
+    d.addr_free((CUdeviceptr)(uintptr_t)t.owner_va, t.size);
+    t.owner_va = nullptr;
+  }
+  if (t.owner_imported) d.mem_release(t.owner_imported);
+  t.owner_imported = 0;
   if (t.mc_va) {
     d.unmap((CUdeviceptr)(uintptr_t)t.mc_va, t.size);
     d.addr_free((CUdeviceptr)(uintptr_t)t.mc_va, t.size);

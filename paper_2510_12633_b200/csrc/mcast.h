@@ -22,6 +22,8 @@ struct McTeam {
   std::map<int, unsigned long long> mem; // local team devices: member allocation
   std::map<int, uint8_t*> va;            // local team devices: member VA
   std::vector<int> bound;                // local devices bound to the object
+  uint8_t* owner_va = nullptr;           // peer processes: the owner's member (node 0's slots) mapped here
+  unsigned long long owner_imported = 0; // ... and its imported handle
 };
 
 // Is the device able to join a multicast team (NVSwitch + fabric manager)?

@@ -86,6 +86,10 @@ struct Part {
   std::vector<HopTile> h_tiles;      // host copy of the full tile list
   HopTile* d_resume = nullptr;       // tiles of the chunks still missing after a rebuild
   RankLink* d_links_dyn = nullptr;   // links to a predecessor other than node - 1
+  // hybrid: tiles of multicast chunks index links[N + rank] (the replica), the others links[rank]
+  HopTile* d_tiles_hyb = nullptr;
+  RankLink* d_links_hyb = nullptr;   // [S][2N] (my slot): filled per launch from h_links_hyb
+  RankLink* h_links_hyb = nullptr;   // pinned staging
   unsigned long long* prof_host = nullptr;  // LAM_HOP_PROF counters (host-mapped)
 };
 
@@ -130,6 +134,7 @@ struct PendingPull {
 
 struct DevLocal {
   uint64_t* d_chunk_len = nullptr;   // per device: [total_chunks]
+  uint8_t* d_chunk_mc = nullptr;     // hybrid: [total_chunks] multicast class (actor GPU)
   uint32_t* d_pack_work = nullptr;   // k_pack's dynamic unit counter (packs are serialised on `side`)
   cudaStream_t side = nullptr;
 };
@@ -151,7 +156,10 @@ struct lam_ctx {
   std::vector<RankPub> pubs;                  // [N]; local ranks only used
   std::map<int, DevLocal> dev;                // devices owned by this process
   bool star = false;                          // LAM_HOP_MULTICAST: every relay is fed by node 0
-  McTeam mc;                                  // LAM_HOP_MULTICAST team (NEXT-2)
+  bool hyb = false;                           // LAM_HOP_HYBRID: chain + multicast share
+  bool mcast = false;                         // a multicast team exists (star or hybrid)
+  McTeam mc;                                  // the multicast team (NEXT-2)
+  std::vector<uint8_t> chunk_mc;              // hybrid: 1 = chunk goes by multicast
   std::map<std::string, PullPlan> plans;
   uint64_t plan_clock = 0;
   struct PullRing { uint32_t* d = nullptr; uint32_t next = 0; std::vector<cudaEvent_t> ev; };
@@ -251,6 +259,7 @@ ChunkMeta meta_of(const lam_ctx* c, const Part& p, int slot) {
   cm.abort_flag = reinterpret_cast<int32_t*>(m + c->sm.abort);
   cm.mirror = c->mirror_dev ? c->mirror_dev + ((uint64_t)p.node * LAM_MAX_SLOTS + slot) * kShmMirrorChunks : nullptr;
   cm.mc_flags = nullptr;
+  cm.mc_class = nullptr;
   return cm;
 }
 
@@ -324,9 +333,16 @@ lam_status validate(const lam_config& c, std::string* why) {
     if (c.rollout[i].node < 0 || c.rollout[i].node > c.n_relays || !dev_ok(c.rollout[i].device))
       return bad("rollout " + std::to_string(i));
   if (c.n_procs > 1 && c.shm_name[0] == 0) return bad("shm_name required with n_procs > 1");
-  if (c.hop_mode != LAM_HOP_KERNEL && c.hop_mode != LAM_HOP_COPY_ENGINE && c.hop_mode != LAM_HOP_MULTICAST)
+  if (c.hop_mode != LAM_HOP_KERNEL && c.hop_mode != LAM_HOP_COPY_ENGINE && c.hop_mode != LAM_HOP_MULTICAST &&
+      c.hop_mode != LAM_HOP_HYBRID)
     return bad("hop_mode");
-  if (c.hop_mode == LAM_HOP_MULTICAST) {
+  if (c.hop_mode == LAM_HOP_HYBRID) {   // a relay waiting on its replica must not share the pack's GPU
+    for (int i = 0; i < c.n_relays; ++i)
+      for (int r = 0; r < c.fsdp_size; ++r)
+        if (c.relay[i].part_device[r] == c.actor_device[0]) return bad("hybrid hops: a relay part on the actor GPU");
+    if (c.hybrid_mc_pct < 0 || c.hybrid_mc_pct > 100) return bad("hybrid_mc_pct");
+  }
+  if (c.hop_mode == LAM_HOP_MULTICAST || c.hop_mode == LAM_HOP_HYBRID) {
     // one source GPU (the multicast writer), HBM relays, node-0 readers on the source GPU
     for (int r = 1; r < c.fsdp_size; ++r)
       if (c.actor_device[r] != c.actor_device[0]) return bad("multicast hops need every actor rank on one GPU");
@@ -392,7 +408,14 @@ lam_status alloc_parts(lam_ctx* c) {
     p.meta_stride = c->sm.bytes;
     p.alloc_bytes = p.meta_base + p.meta_stride * S;
   }
-  if (c->star) {
+  if (c->hyb) {
+    // hybrid: spread the multicast share evenly over the chunks (chunk g goes by multicast iff
+    // floor((g+1) pct / 100) > floor(g pct / 100))
+    const uint64_t pct = c->cfg.hybrid_mc_pct > 0 ? (uint64_t)c->cfg.hybrid_mc_pct : 60;
+    c->chunk_mc.assign(total, 0);
+    for (uint64_t g = 0; g < total; ++g) c->chunk_mc[g] = (g + 1) * pct / 100 > g * pct / 100;
+  }
+  if (c->mcast) {
     // multicast team members (NEXT-2): node 0's S slots followed by S flag arrays, on the actor GPU
     // and every relay GPU this process owns
     const Part& p0 = c->parts[c->node_parts[0][0]];
@@ -409,7 +432,7 @@ lam_status alloc_parts(lam_ctx* c) {
   for (Part& p : c->parts) {
     if (!p.local) continue;
     CK(cudaSetDevice(p.device));
-    if (p.node == 0 && c->star) {
+    if (p.node == 0 && c->mcast) {
       // slot data = the actor GPU's member of the multicast team (zero-filled); metadata separate
       p.mc = true;
       p.data = c->mc.va.at(p.device);
@@ -439,7 +462,9 @@ lam_status alloc_parts(lam_ctx* c) {
     }
     int lo = 0, hi = 0;
     CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-    CK(cudaStreamCreateWithPriority(&p.stream, cudaStreamNonBlocking, lo));  // lowest priority: SM-light
+    // relay hops at the greatest priority: a hop (32 SM-light CTAs) launched while a rollout's reshard
+    // fills the GPU gets the first SMs that free up instead of queueing behind the rest of the pull
+    CK(cudaStreamCreateWithPriority(&p.stream, cudaStreamNonBlocking, p.node > 0 ? hi : lo));
     for (int s = 0; s < S; ++s) CK(cudaEventCreateWithFlags(&p.done_ev[s], cudaEventDisableTiming));
     CK(cudaHostAlloc(&p.err_host, sizeof(uint32_t) * LAM_MAX_SLOTS, cudaHostAllocMapped | cudaHostAllocPortable));
     memset(p.err_host, 0, sizeof(uint32_t) * LAM_MAX_SLOTS);
@@ -452,6 +477,10 @@ lam_status alloc_parts(lam_ctx* c) {
       if (total) CK(cudaMemcpy(dl.d_chunk_len, len.data(), 8 * total, cudaMemcpyHostToDevice));
       CK(cudaStreamCreateWithPriority(&dl.side, cudaStreamNonBlocking, lo));
       CK(cudaMalloc(&dl.d_pack_work, sizeof(uint32_t)));
+      if (c->hyb && total) {
+        CK(cudaMalloc(&dl.d_chunk_mc, total));
+        CK(cudaMemcpy(dl.d_chunk_mc, c->chunk_mc.data(), total, cudaMemcpyHostToDevice));
+      }
       c->dev[p.device] = dl;
     }
     if (p.node > 0) {
@@ -470,6 +499,15 @@ lam_status alloc_parts(lam_ctx* c) {
       }
       CK(cudaMalloc(&p.d_resume, sizeof(HopTile) * std::max<size_t>(tiles.size(), 1)));
       CK(cudaMalloc(&p.d_links_dyn, sizeof(RankLink) * N));
+      if (c->hyb) {
+        std::vector<HopTile> th = tiles;
+        for (HopTile& t : th)
+          if (c->chunk_mc[t.chunk]) t.rank += (uint32_t)N;
+        CK(cudaMalloc(&p.d_tiles_hyb, sizeof(HopTile) * std::max<size_t>(th.size(), 1)));
+        if (!th.empty()) CK(cudaMemcpy(p.d_tiles_hyb, th.data(), sizeof(HopTile) * th.size(), cudaMemcpyHostToDevice));
+        CK(cudaMalloc(&p.d_links_hyb, sizeof(RankLink) * 2 * N * S));
+        CK(cudaHostAlloc(&p.h_links_hyb, sizeof(RankLink) * 2 * N * S, cudaHostAllocPortable));
+      }
       p.h_tiles = tiles;
       CK(cudaMalloc(&p.d_tiles_per_chunk, 4 * std::max<uint64_t>(total, 1)));
       if (total) CK(cudaMemcpy(p.d_tiles_per_chunk, tpc.data(), 4 * total, cudaMemcpyHostToDevice));
@@ -492,7 +530,7 @@ lam_status alloc_parts(lam_ctx* c) {
 // LAM_HOP_MULTICAST: create/import the multicast object, add and bind this process's team devices.
 // Called outside the control-block lock (cuMulticastBindMem blocks until every process added its GPU).
 lam_status mc_connect(lam_ctx* c) {
-  if (!c->star || c->mc.mc) return LAM_OK;
+  if (!c->mcast || c->mc.mc) return LAM_OK;
   std::vector<int> local;
   std::set<int> procs;
   for (int d : c->mc.devices) {
@@ -502,7 +540,12 @@ lam_status mc_connect(lam_ctx* c) {
   if (local.empty()) return LAM_OK;
   const bool owner = owns(c, c->mc.owner_dev);
   const std::string sock = std::string("lam-mc-") + c->cfg.shm_name;
-  return mc_setup(c->mc, local, owner, owner ? (int)procs.size() - 1 : 0, sock.c_str());
+  lam_status st = mc_setup(c->mc, local, owner, owner ? (int)procs.size() - 1 : 0, sock.c_str());
+  if (st != LAM_OK) return st;
+  if (!owner)   // node 0's slot data as seen from this process: the owner's member, mapped over NVLink
+    for (Part& p : c->parts)
+      if (p.node == 0 && p.mc && !p.local) p.data = c->mc.owner_va;
+  return LAM_OK;
 }
 
 lam_status connect_links(lam_ctx* c) {
@@ -837,11 +880,33 @@ lam_status launch_hop_part(lam_ctx* c, Part& p, int s, bool* launched) {
     *launched = true;
     return ce_topup(c, p);
   } else {
-    const RankLink* links = p.d_links + (size_t)(s * c->S + ps) * c->cfg.fsdp_size;
+    const int N = c->cfg.fsdp_size;
+    const RankLink* links = p.d_links + (size_t)(s * c->S + ps) * N;
     if (pred != base_pred(c, p.node)) {  // rebuilt chain: links to the new predecessor
       lam_status st = build_links(c, p, s, pred, ps);
       if (st != LAM_OK) return st;
       links = p.d_links_dyn;
+    } else if (c->hyb && !resume && sl.src0_slot >= 0) {
+      // hybrid: links [0, N) = the chain predecessor's slot, [N, 2N) = this GPU's replica of node 0's
+      // slot holding u (pinned by this fill); the multicast chunks' tiles point at the latter
+      const int s0 = sl.src0_slot;
+      const Part& p0 = c->parts[c->node_parts[0][0]];
+      ChunkMeta m0 = meta_of(c, p0, s0);
+      RankLink* h = p.h_links_hyb + (size_t)s * 2 * N;
+      CK(cudaStreamSynchronize(p.stream));   // the staging row of slot s is reused: its last copy is done
+      CK(cudaMemcpy(h, links, sizeof(RankLink) * N, cudaMemcpyDeviceToHost));
+      uint8_t* mine = c->mc.va.at(p.device);
+      for (int r : p.ranks) {
+        RankLink& L = h[N + r];
+        L.src = mine + (uint64_t)s0 * p0.slot_stride + p0.rank_off[r];
+        L.src_flags = reinterpret_cast<const uint64_t*>(mine + c->mc.flags_off + (uint64_t)s0 * c->mc.flag_stride);
+        L.src_hdr = m0.hdr;
+        L.dst = slot_data(p, s) + p.rank_off[r];
+      }
+      CK(cudaMemcpyAsync(p.d_links_hyb + (size_t)s * 2 * N, h, sizeof(RankLink) * 2 * N, cudaMemcpyHostToDevice,
+                         p.stream));
+      links = p.d_links_hyb + (size_t)s * 2 * N;
+      tiles = p.d_tiles_hyb;
     }
     int rc = launch_hop(tiles, n_tiles, links, m, p.d_tiles_per_chunk, u, p.err_dev + s, c->timeout_ns,
                         // host-tier destination: PCIe stores need more CTAs in flight (v6 box run:
@@ -1174,8 +1239,10 @@ extern "C" lam_status lam_init(const lam_config* cfg, lam_ctx** out) {
   c->pull_ctas = cfg->pull_ctas > 0 ? cfg->pull_ctas : 0;
   if (cfg->spin_timeout_s > 0) c->timeout_ns = (uint64_t)(cfg->spin_timeout_s * 1e9);
   c->pubs.resize(cfg->fsdp_size);
-  if (cfg->hop_mode == LAM_HOP_MULTICAST) {
-    c->star = true;
+  if (cfg->hop_mode == LAM_HOP_MULTICAST || cfg->hop_mode == LAM_HOP_HYBRID) {
+    c->star = cfg->hop_mode == LAM_HOP_MULTICAST;
+    c->hyb = cfg->hop_mode == LAM_HOP_HYBRID;
+    c->mcast = true;
     std::set<int> team{cfg->actor_device[0]};
     for (int i = 0; i < cfg->n_relays; ++i)
       for (int r = 0; r < cfg->fsdp_size; ++r) team.insert(cfg->relay[i].part_device[r]);
@@ -1189,7 +1256,7 @@ extern "C" lam_status lam_init(const lam_config* cfg, lam_ctx** out) {
   }
   st = setup_shm(c.get());
   if (st != LAM_OK) return st;
-  if (cfg->n_procs == 1 || cfg->proc_rank == 0) ctl::init(c->shm, c->n_nodes, c->star);
+  if (cfg->n_procs == 1 || cfg->proc_rank == 0) ctl::init(c->shm, c->n_nodes, c->star, c->hyb);
   c->streams.resize(cfg->n_rollouts);
   // map the control block for the producer kernels' chunk-flag mirror (streaming pulls)
   for (int d = 0; d < LAM_MAX_DEVICES; ++d)
@@ -1281,8 +1348,7 @@ extern "C" lam_status lam_import_ipc(lam_ctx* c, int32_t proc, const void* buf, 
     if (e.mc) {
       p.mc = true;
       p.meta = (uint8_t*)ptr;
-      auto it = c->mc.va.find(my_dev);   // this process reads node 0's slots from its own replica
-      p.data = it != c->mc.va.end() ? it->second : nullptr;
+      p.data = nullptr;   // set by lam_connect: the actor GPU's member, imported with the multicast object
     } else if (e.host) {
       p.meta = (uint8_t*)ptr;
       char path[64];
@@ -1415,12 +1481,14 @@ static lam_status publish_impl(lam_ctx* c, uint64_t v, int32_t rank, const lam_s
     sub = rp.d_sub;
   }
   uint8_t* dst = slot_data(p, s);
+  uint8_t* mc_dst = nullptr;
   if (p.mc) {   // NEXT-2: store through the multicast VA (the switch replicates into every relay GPU)
     if (!c->mc.mc_va) return LAM_ECUDA;
-    dst = c->mc.mc_va + (uint64_t)s * p.slot_stride;
+    mc_dst = c->mc.mc_va + (uint64_t)s * p.slot_stride;
     m.mc_flags = reinterpret_cast<uint64_t*>(c->mc.mc_va + c->mc.flags_off + (uint64_t)s * c->mc.flag_stride);
+    m.mc_class = c->hyb ? c->dev[dev].d_chunk_mc : nullptr;   // hybrid: only the multicast share
   }
-  int rc = launch_pack(rp.d_units, rp.n_units, rp.d_ptrs, dst, m, rp.d_units_per_chunk, v,
+  int rc = launch_pack(rp.d_units, rp.n_units, rp.d_ptrs, dst, mc_dst, m, rp.d_units_per_chunk, v,
                        c->plan.total_chunks, c->dev[dev].d_chunk_len, c->pack_ctas, side, sub,
                        c->dev[dev].d_pack_work, c->pack_sms);
   if (rc) {
@@ -1748,7 +1816,7 @@ extern "C" lam_status lam_debug_region(lam_ctx* c, int32_t node, uint64_t v, int
 }
 
 extern "C" lam_status lam_debug_replica(lam_ctx* c, int32_t device, uint64_t v, int32_t rank, void** ptr) {
-  if (!c || !ptr || rank < 0 || rank >= c->cfg.fsdp_size || !c->star) return LAM_EINVAL;
+  if (!c || !ptr || rank < 0 || rank >= c->cfg.fsdp_size || !c->mcast) return LAM_EINVAL;
   Lock l(c->shm);
   auto it = c->mc.va.find(device);
   if (it == c->mc.va.end()) return LAM_EINVAL;
@@ -1774,6 +1842,7 @@ extern "C" void lam_destroy(lam_ctx* c) {
     cudaDeviceSynchronize();
     if (kv.second.d_chunk_len) cudaFree(kv.second.d_chunk_len);
     if (kv.second.d_pack_work) cudaFree(kv.second.d_pack_work);
+    if (kv.second.d_chunk_mc) cudaFree(kv.second.d_chunk_mc);
     if (kv.second.side) cudaStreamDestroy(kv.second.side);
   }
   for (auto& kv : c->plans) {
@@ -1818,6 +1887,9 @@ extern "C" void lam_destroy(lam_ctx* c) {
     if (p.d_tiles) cudaFree(p.d_tiles);
     if (p.d_tiles_per_chunk) cudaFree(p.d_tiles_per_chunk);
     if (p.d_links) cudaFree(p.d_links);
+    if (p.d_tiles_hyb) cudaFree(p.d_tiles_hyb);
+    if (p.d_links_hyb) cudaFree(p.d_links_hyb);
+    if (p.h_links_hyb) cudaFreeHost(p.h_links_hyb);
     if (p.d_my_chunks) cudaFree(p.d_my_chunks);
     for (cudaEvent_t e : p.chunk_ev) cudaEventDestroy(e);
     if (p.vstream) cudaStreamDestroy(p.vstream);
