@@ -378,6 +378,11 @@ int64_t lam_plan_copy_tiles(const lam_model_dims*, int32_t actor_layout, int32_t
  * Semantics: PAPER L548-550, L652-670; SPEC L546-547, L633, L638, L643, L661 (see control.h). */
 typedef struct lam_ctl lam_ctl;
 lam_ctl* lam_ctl_open(const char* name, int32_t create, int32_t n_nodes, int32_t slots, int32_t fsdp_size);
+/* Same, with the topology of a hop mode: LAM_HOP_MULTICAST = star (every relay's predecessor is node
+ * 0), LAM_HOP_HYBRID = chain whose fills also pin node 0's slot of their version (the multicast share
+ * is read from node 0's replica), others = chain. */
+lam_ctl* lam_ctl_open_mode(const char* name, int32_t create, int32_t n_nodes, int32_t slots, int32_t fsdp_size,
+                           int32_t hop_mode);
 void lam_ctl_close(lam_ctl*);
 lam_status lam_ctl_publish(lam_ctl*, uint64_t version, int32_t rank, int32_t* slot);  /* ESTALE, EBUSY */
 int32_t lam_ctl_pack_done(lam_ctl*, int32_t slot, uint64_t version);                  /* 1 = changed */

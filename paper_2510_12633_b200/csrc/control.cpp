@@ -361,7 +361,8 @@ struct lam_ctl {
   char name[64];
 };
 
-extern "C" lam_ctl* lam_ctl_open(const char* name, int32_t create, int32_t n_nodes, int32_t slots, int32_t fsdp) {
+extern "C" lam_ctl* lam_ctl_open_mode(const char* name, int32_t create, int32_t n_nodes, int32_t slots,
+                                      int32_t fsdp, int32_t hop_mode) {
   if (n_nodes < 1 || n_nodes > LAM_MAX_NODES + 1 || slots < 2 || slots > LAM_MAX_SLOTS || fsdp < 1 ||
       fsdp > LAM_MAX_RANKS)
     return nullptr;
@@ -378,8 +379,12 @@ extern "C" lam_ctl* lam_ctl_open(const char* name, int32_t create, int32_t n_nod
     delete c;
     return nullptr;
   }
-  if (create || !c->mapped) ctl::init(c->sh, n_nodes);
+  if (create || !c->mapped) ctl::init(c->sh, n_nodes, hop_mode == LAM_HOP_MULTICAST, hop_mode == LAM_HOP_HYBRID);
   return c;
+}
+
+extern "C" lam_ctl* lam_ctl_open(const char* name, int32_t create, int32_t n_nodes, int32_t slots, int32_t fsdp) {
+  return lam_ctl_open_mode(name, create, n_nodes, slots, fsdp, LAM_HOP_KERNEL);
 }
 
 extern "C" void lam_ctl_close(lam_ctl* c) {

@@ -468,10 +468,12 @@ class Ctl:
     """The control plane alone (lam_ctl_*; host-only, no GPU): the version-table state machine the
     runtime uses, on a POSIX shared-memory block shared by several processes (name != "")."""
 
-    def __init__(self, name: str, create: bool, n_nodes: int, slots: int = 2, fsdp: int = 1):
+    def __init__(self, name: str, create: bool, n_nodes: int, slots: int = 2, fsdp: int = 1,
+                 hop_mode: int = LAM_HOP_KERNEL):
         L = self.L = load()
         P, V, I32, U64 = C.POINTER, C.c_void_p, C.c_int32, C.c_uint64
-        for fn, res, args in [("lam_ctl_open", V, [C.c_char_p, I32, I32, I32, I32]), ("lam_ctl_close", None, [V]),
+        for fn, res, args in [("lam_ctl_open", V, [C.c_char_p, I32, I32, I32, I32]),
+                              ("lam_ctl_open_mode", V, [C.c_char_p, I32, I32, I32, I32, I32]), ("lam_ctl_close", None, [V]),
                               ("lam_ctl_publish", I32, [V, U64, I32, P(I32)]), ("lam_ctl_pack_done", I32, [V, I32, U64]),
                               ("lam_ctl_start", I32, [V, I32, P(U64), P(I32)]),
                               ("lam_ctl_part_done", I32, [V, I32, I32, U64, I32, I32]),
@@ -483,7 +485,7 @@ class Ctl:
                               ("lam_ctl_dead_procs", U64, [V])]:
             f = getattr(L, fn)
             f.restype, f.argtypes = res, args
-        self.h = L.lam_ctl_open(name.encode(), int(create), n_nodes, slots, fsdp)
+        self.h = L.lam_ctl_open_mode(name.encode(), int(create), n_nodes, slots, fsdp, hop_mode)
         if not self.h:
             raise LamError(LAM_EIPC, "lam_ctl_open")
 

@@ -323,8 +323,28 @@ recipe_r2n() {
   timeout 600 ncu --metrics gpu__time_duration.sum,nvltx__bytes.sum,nvlrx__bytes.sum,nvltx__bytes.sum.per_second,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:k_pack --csv --log-file gpurun_out/r2n/mc_pack_ncu.csv python tools/mc_profile.py > gpurun_out/r2n/mc_ncu.log 2>&1
 }
 
+recipe_r2o() {
+  # does a slower, SM-confined pack leave GPU 0's HBM to the first hop's peer reads? (chain N=2/4)
+  mkdir -p gpurun_out/r2o
+  python -c "import __graft_entry__ as g; g.build()" > gpurun_out/r2o/build.log 2>&1
+  for n in 2 4; do for k in 48 80; do
+  timeout 300 python bench.py --gpus $n --steps 10 --warmup 3 --no-e2e --no-cpu-baseline --pack-sms $k > gpurun_out/r2o/n${n}_sms$k.log 2>&1; echo rc=$? >> gpurun_out/r2o/n${n}_sms$k.log
+  done; done
+}
+
+recipe_r2p() {
+  # does the relay's streaming reshard slow its hop? (chain N=2: pulls streamed with fewer CTAs / not streamed)
+  mkdir -p gpurun_out/r2p
+  python -c "import __graft_entry__ as g; g.build()" > gpurun_out/r2p/build.log 2>&1
+  timeout 300 python bench.py --gpus 2 --steps 10 --warmup 3 --no-e2e --no-cpu-baseline --stream-pull off > gpurun_out/r2p/n2_nostream.log 2>&1
+  for k in 24 48; do
+  timeout 300 python bench.py --gpus 2 --steps 10 --warmup 3 --no-e2e --no-cpu-baseline --pull-ctas $k > gpurun_out/r2p/n2_pull$k.log 2>&1
+  done
+  timeout 300 python bench.py --gpus 4 --steps 10 --warmup 3 --no-e2e --no-cpu-baseline --pull-ctas 48 > gpurun_out/r2p/n4_pull48.log 2>&1
+}
+
 if [ $# -ne 1 ] || ! declare -F "recipe_$1" > /dev/null; then
-  echo "usage: bash tools/gpu_recipes.sh <recipe>; recipes: sweep4 n4 v9 v10 v15 host4 v5 v12 dyn v13 final r2c v14 r2b ncu2 v7 r2d r2a v11 v6 v8 r2e r2f r2g r2h r2j r2l r2m r2n"
+  echo "usage: bash tools/gpu_recipes.sh <recipe>; recipes: sweep4 n4 v9 v10 v15 host4 v5 v12 dyn v13 final r2c v14 r2b ncu2 v7 r2d r2a v11 v6 v8 r2e r2f r2g r2h r2j r2l r2m r2n r2o r2p"
   exit 2
 fi
 "recipe_$1"
