@@ -343,8 +343,21 @@ recipe_r2p() {
   timeout 300 python bench.py --gpus 4 --steps 10 --warmup 3 --no-e2e --no-cpu-baseline --pull-ctas 48 > gpurun_out/r2p/n4_pull48.log 2>&1
 }
 
+recipe_r2q() {
+  # host-memory relay tier (NEXT-3): k_hop with TMA bulk stores into pinned host memory vs 16-B stores
+  mkdir -p gpurun_out/r2q
+  python -c "import __graft_entry__ as g; g.build()" > gpurun_out/r2q/build.log 2>&1
+  timeout 600 python -m pytest tests/test_gpu_parity.py -q -x -rs -k "host" > gpurun_out/r2q/pytest_host.log 2>&1; echo rc=$? >> gpurun_out/r2q/pytest_host.log
+  timeout 900 python -m pytest tests/test_gpu_multiproc.py -q -x -rs -k "14 or 15 or 16" > gpurun_out/r2q/pytest_host_mp.log 2>&1; echo rc=$? >> gpurun_out/r2q/pytest_host_mp.log
+  for h in 32 96; do
+  timeout 600 python bench.py --config host --steps 3 --warmup 1 --no-e2e --no-cpu-baseline --hop-ctas $h > gpurun_out/r2q/host_n1_bulk_h$h.log 2>&1
+  LAM_HOP_NO_BULK=1 timeout 600 python bench.py --config host --steps 3 --warmup 1 --no-e2e --no-cpu-baseline --hop-ctas $h > gpurun_out/r2q/host_n1_st_h$h.log 2>&1
+  done
+  timeout 600 python bench.py --gpus 2 --config host --steps 3 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/r2q/host_n2_bulk.log 2>&1
+}
+
 if [ $# -ne 1 ] || ! declare -F "recipe_$1" > /dev/null; then
-  echo "usage: bash tools/gpu_recipes.sh <recipe>; recipes: sweep4 n4 v9 v10 v15 host4 v5 v12 dyn v13 final r2c v14 r2b ncu2 v7 r2d r2a v11 v6 v8 r2e r2f r2g r2h r2j r2l r2m r2n r2o r2p"
+  echo "usage: bash tools/gpu_recipes.sh <recipe>; recipes: sweep4 n4 v9 v10 v15 host4 v5 v12 dyn v13 final r2c v14 r2b ncu2 v7 r2d r2a v11 v6 v8 r2e r2f r2g r2h r2j r2l r2m r2n r2o r2p r2q"
   exit 2
 fi
 "recipe_$1"
