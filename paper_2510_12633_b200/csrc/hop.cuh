@@ -91,7 +91,9 @@ __device__ void hop_flush(ChunkMeta meta, const RankLink& L, const uint32_t* til
   const uint64_t got1 = atomicAdd((unsigned long long*)&h->s1, 0ull);
   const uint64_t got2 = atomicAdd((unsigned long long*)&h->s2, 0ull);
   const lam_chunk_header* ph = L.src_hdr + chunk;
-  if (got1 == ld_relaxed_sys(&ph->s1) && got2 == ld_relaxed_sys(&ph->s2)) {
+  // the pred's own verdict too: a chunk it poisoned carries the sums of its (corrupt) bytes
+  if (ld_acquire_sys(L.pred_flags + chunk) == version && got1 == ld_relaxed_sys(&ph->s1) &&
+      got2 == ld_relaxed_sys(&ph->s2)) {
     h->version = ld_relaxed_sys(&ph->version);
     h->idx = ld_relaxed_sys(&ph->idx);
     h->n = ld_relaxed_sys(&ph->n);
@@ -312,10 +314,10 @@ int launch_hop(const HopTile* tiles, uint32_t n_tiles, const RankLink* links, Ch
   }
   unsigned grid = (unsigned)(n_tiles < (uint32_t)ctas ? n_tiles : (uint32_t)ctas);
   if (fine)
-    k_hop<14, 16384><<<grid, kHopThreads, kHopSmem, (cudaStream_t)stream>>>(tiles, n_tiles, links, meta,
-                                                                         tiles_per_chunk, version, err_word, timeout_ns);
+    k_hop<14, 16384><<<grid, kHopThreads, kHopSmem, (cudaStream_t)stream>>>(
+        tiles, n_tiles, links, meta, tiles_per_chunk, version, err_word, timeout_ns);
   else
-    k_hop<7, 32768><<<grid, kHopThreads, kHopSmem, (cudaStream_t)stream>>>(tiles, n_tiles, links, meta,
-                                                                        tiles_per_chunk, version, err_word, timeout_ns);
+    k_hop<7, 32768><<<grid, kHopThreads, kHopSmem, (cudaStream_t)stream>>>(
+        tiles, n_tiles, links, meta, tiles_per_chunk, version, err_word, timeout_ns);
   return (int)cudaGetLastError();
 }

@@ -85,9 +85,12 @@ struct __attribute__((aligned(16))) HopTile {    // one tile of a chunk moved pr
 
 struct __attribute__((aligned(16))) RankLink {   // per actor rank, for the hop kernel
   const uint8_t* src;         // pred node: rank region base in the pinned pred slot
-  const uint64_t* src_flags;  // pred node part holding the rank: flags (indexed by global chunk)
-  const lam_chunk_header* src_hdr;
+  const uint64_t* src_flags;  // chunk j's bytes may be read from src once src_flags[j] == version (the
+                              // pred's flags, or its multicast replica's)
+  const lam_chunk_header* src_hdr;   // pred's headers (the checksum the chunk must reproduce)
   uint8_t* dst;               // this node part: rank region base in the filling slot
+  const uint64_t* pred_flags; // pred's flags: a chunk is committed only if the pred committed it
+  const uint64_t* _pad;
 };
 
 struct __attribute__((aligned(16))) CopyTile {   // one 2-D block of a pull (reshard)

@@ -193,6 +193,7 @@ struct lam_ctx {
   struct Timed { int kind, dev; cudaEvent_t a, b; };
   std::vector<Timed> timed;
   std::map<int, std::vector<cudaEvent_t>> tev_pool;  // timing-enabled events per device
+  std::map<int, cudaStream_t> util;   // per device: stream-ordered allocations while hops run
 };
 
 namespace {
@@ -265,6 +266,32 @@ ChunkMeta meta_of(const lam_ctx* c, const Part& p, int slot) {
 
 uint8_t* slot_data(const Part& p, int slot) { return p.data + (uint64_t)slot * p.slot_stride; }
 
+// Device memory allocated (or freed) while hops may be running: cudaMalloc / cudaFree are implicit
+// synchronisation points, so the first pull of a layout (its copy plan) would hold the caller until
+// every hop kernel of the GPU ended.  Stream-ordered allocation on a per-device utility stream has no
+// such wait.  The caller set the device.
+cudaStream_t util_stream(lam_ctx* c, int dev) {
+  cudaStream_t& s = c->util[dev];
+  if (!s && cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) s = nullptr;
+  return s;
+}
+cudaError_t dev_alloc(lam_ctx* c, int dev, void** p, size_t bytes) {
+  cudaStream_t s = util_stream(c, dev);
+  if (!s) return cudaErrorUnknown;
+  cudaError_t e = cudaMallocAsync(p, bytes, s);
+  return e != cudaSuccess ? e : cudaStreamSynchronize(s);
+}
+cudaError_t dev_upload(lam_ctx* c, int dev, void* dst, const void* src, size_t bytes) {
+  cudaStream_t s = util_stream(c, dev);
+  if (!s) return cudaErrorUnknown;
+  cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s);
+  return e != cudaSuccess ? e : cudaStreamSynchronize(s);
+}
+void dev_free(lam_ctx* c, int dev, void* p) {
+  cudaStream_t s = util_stream(c, dev);
+  if (s) cudaFreeAsync(p, s);
+}
+
 // Host-memory tier: map `bytes` of the memfd `fd` and pin it for every device (mapped, portable).
 lam_status map_host_part(Part& p, int fd, size_t bytes) {
   void* h = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
@@ -297,7 +324,7 @@ constexpr uint32_t kPullRing = 1024;
 uint32_t* pull_counter(lam_ctx* c, int dev, cudaEvent_t* ev) {
   lam_ctx::PullRing& r = c->pull_work[dev];
   if (!r.d) {
-    if (cudaMalloc(&r.d, 2 * sizeof(uint32_t) * kPullRing) != cudaSuccess) {
+    if (dev_alloc(c, dev, (void**)&r.d, 2 * sizeof(uint32_t) * kPullRing) != cudaSuccess) {
       r.d = nullptr;
       return nullptr;
     }
@@ -585,6 +612,7 @@ lam_status connect_links(lam_ctx* c) {
           L.src = slot_data(q, ps) + q.rank_off[r];
           L.src_flags = qm.flags;
           L.src_hdr = qm.hdr;
+          L.pred_flags = qm.flags;
           if (c->star) {
             // the relay's replica of node 0's slot in its own GPU's team member, and the chunk flags
             // the pack multicast next to it: data and flags are read from local HBM
@@ -762,6 +790,7 @@ lam_status build_links(lam_ctx* c, Part& p, int s, int pred, int ps) {
     links[r].src_flags = qm.flags;
     links[r].src_hdr = qm.hdr;
     links[r].dst = slot_data(p, s) + p.rank_off[r];
+    links[r].pred_flags = qm.flags;
   }
   CK(cudaStreamSynchronize(p.stream));
   CK(cudaMemcpy(p.d_links_dyn, links.data(), sizeof(RankLink) * links.size(), cudaMemcpyHostToDevice));
@@ -901,6 +930,7 @@ lam_status launch_hop_part(lam_ctx* c, Part& p, int s, bool* launched) {
         L.src = mine + (uint64_t)s0 * p0.slot_stride + p0.rank_off[r];
         L.src_flags = reinterpret_cast<const uint64_t*>(mine + c->mc.flags_off + (uint64_t)s0 * c->mc.flag_stride);
         L.src_hdr = m0.hdr;
+        L.pred_flags = m0.flags;
         L.dst = slot_data(p, s) + p.rank_off[r];
       }
       CK(cudaMemcpyAsync(p.d_links_hyb + (size_t)s * 2 * N, h, sizeof(RankLink) * 2 * N, cudaMemcpyHostToDevice,
@@ -1115,7 +1145,7 @@ lam_status get_plan(lam_ctx* c, const lam_rollout_desc& ro, const lam_tp_layout&
         CK(cudaEventSynchronize(v.last_ev));
         cudaEventDestroy(v.last_ev);
       }
-      cudaFree(v.d_tiles);
+      dev_free(c, v.device, v.d_tiles);
       c->plans.erase(victim);
       CK(cudaSetDevice(ro.device));
     }
@@ -1151,8 +1181,8 @@ lam_status get_plan(lam_ctx* c, const lam_rollout_desc& ro, const lam_tp_layout&
     // local = this GPU's HBM; remote = a peer's HBM over NVLink, or the host tier over PCIe
     (q.device == ro.device && !q.host ? pp.local_bytes : pp.remote_bytes) += (uint64_t)t.rows * t.row_bytes;
   }
-  CK(cudaMalloc(&pp.d_tiles, sizeof(CopyTile) * std::max<size_t>(tiles.size(), 1)));
-  if (!tiles.empty()) CK(cudaMemcpy(pp.d_tiles, tiles.data(), sizeof(CopyTile) * tiles.size(), cudaMemcpyHostToDevice));
+  CK(dev_alloc(c, ro.device, (void**)&pp.d_tiles, sizeof(CopyTile) * std::max<size_t>(tiles.size(), 1)));
+  if (!tiles.empty()) CK(dev_upload(c, ro.device, pp.d_tiles, tiles.data(), sizeof(CopyTile) * tiles.size()));
   CK(cudaEventCreateWithFlags(&pp.last_ev, cudaEventDisableTiming));
   pp.device = ro.device;
   pp.last_use = ++c->plan_clock;
@@ -1847,12 +1877,12 @@ extern "C" void lam_destroy(lam_ctx* c) {
   }
   for (auto& kv : c->plans) {
     cudaSetDevice(kv.second.device);
-    cudaFree(kv.second.d_tiles);
+    cudaFreeAsync(kv.second.d_tiles, util_stream(c, kv.second.device));
     if (kv.second.last_ev) cudaEventDestroy(kv.second.last_ev);
   }
   for (auto& kv : c->pull_work) {
     cudaSetDevice(kv.first);
-    if (kv.second.d) cudaFree(kv.second.d);
+    if (kv.second.d) cudaFreeAsync(kv.second.d, util_stream(c, kv.first));
     for (cudaEvent_t e : kv.second.ev)
       if (e) cudaEventDestroy(e);
   }
@@ -1905,6 +1935,11 @@ extern "C" void lam_destroy(lam_ctx* c) {
   for (auto& kv : c->tev_pool)
     for (cudaEvent_t e : kv.second) cudaEventDestroy(e);
   for (auto& t : c->timed) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }
+  for (auto& kv : c->util) {
+    cudaSetDevice(kv.first);
+    cudaStreamSynchronize(kv.second);
+    cudaStreamDestroy(kv.second);
+  }
   mc_release(c->mc);
   if (c->shm_registered) cudaHostUnregister(c->shm);
   shm_release(c->shm, c->cfg.shm_name, c->shm_mapped, c->shm_owner);

@@ -356,8 +356,49 @@ recipe_r2q() {
   timeout 600 python bench.py --gpus 2 --config host --steps 3 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/r2q/host_n2_bulk.log 2>&1
 }
 
+recipe_r2r() {
+  # copy-engine chain v3 (progress thread + verify-only k_hop) and k_hop's predecessor-verdict check:
+  # full GPU suite on 4 GPUs, CE vs kernel chain
+  mkdir -p gpurun_out/r2r
+  python -c "import __graft_entry__ as g; g.build()" > gpurun_out/r2r/build.log 2>&1
+  export LAM_DEBUG_FAIL=1
+  timeout 300 python -m pytest tests/test_gpu_parity.py -q -x -rs -k "chain or host or corrupt" > gpurun_out/r2r/pytest_quick.log 2>&1; echo rc=$? >> gpurun_out/r2r/pytest_quick.log
+  for n in 2 4; do
+  timeout 300 python bench.py --gpus $n --steps 10 --warmup 3 --no-e2e --no-cpu-baseline --hop-mode ce > gpurun_out/r2r/n${n}_ce.log 2>&1; echo rc=$? >> gpurun_out/r2r/n${n}_ce.log
+  done
+  timeout 1800 python -m pytest tests -m gpu -q -rs > gpurun_out/r2r/pytest4.log 2>&1; echo rc=$? >> gpurun_out/r2r/pytest4.log
+}
+
+recipe_r2s() {
+  # copy-engine chain v3 with stream-ordered plan allocations: parity (incl. 7B CE + streaming pulls) and bench
+  mkdir -p gpurun_out/r2s
+  python -c "import __graft_entry__ as g; g.build()" > gpurun_out/r2s/build.log 2>&1
+  export LAM_DEBUG_FAIL=1
+  timeout 900 python -m pytest tests/test_gpu_multiproc.py -q -rs -k "8 or 9 or 16 or 20 or 21" > gpurun_out/r2s/pytest_mp_ce.log 2>&1; echo rc=$? >> gpurun_out/r2s/pytest_mp_ce.log
+  for n in 2 4; do for m in ce kernel; do
+  timeout 300 python bench.py --gpus $n --steps 10 --warmup 3 --no-e2e --no-cpu-baseline --hop-mode $m > gpurun_out/r2s/n${n}_$m.log 2>&1; echo rc=$? >> gpurun_out/r2s/n${n}_$m.log
+  done; done
+}
+
+recipe_r2t() {
+  # debug: copy-engine chain stall at the first chunk past the enqueue window (bench N=2)
+  mkdir -p gpurun_out/r2t
+  python -c "import __graft_entry__ as g; g.build()" > gpurun_out/r2t/build.log 2>&1
+  LAM_DEBUG_FAIL=1 LAM_DEBUG_CE=1 timeout 200 python bench.py --gpus 2 --steps 2 --warmup 1 --no-e2e --no-cpu-baseline --no-verify --hop-mode ce > gpurun_out/r2t/n2_ce.log 2>&1
+  LAM_DEBUG_FAIL=1 LAM_DEBUG_CE=1 timeout 200 python bench.py --gpus 2 --steps 2 --warmup 1 --no-e2e --no-cpu-baseline --no-verify --hop-mode ce --stream-pull off > gpurun_out/r2t/n2_ce_nostream.log 2>&1
+}
+
+recipe_r2u() {
+  # debug: copy-engine chain stall with streaming pulls — more hardware queues / one copy stream
+  mkdir -p gpurun_out/r2u
+  python -c "import __graft_entry__ as g; g.build()" > gpurun_out/r2u/build.log 2>&1
+  export LAM_DEBUG_FAIL=1 LAM_DEBUG_CE=1
+  CUDA_DEVICE_MAX_CONNECTIONS=32 timeout 200 python bench.py --gpus 2 --steps 5 --warmup 2 --no-e2e --no-cpu-baseline --no-verify --hop-mode ce > gpurun_out/r2u/n2_ce_conn32.log 2>&1
+  LAM_CE_ONE_STREAM=1 timeout 200 python bench.py --gpus 2 --steps 5 --warmup 2 --no-e2e --no-cpu-baseline --no-verify --hop-mode ce > gpurun_out/r2u/n2_ce_one.log 2>&1
+}
+
 if [ $# -ne 1 ] || ! declare -F "recipe_$1" > /dev/null; then
-  echo "usage: bash tools/gpu_recipes.sh <recipe>; recipes: sweep4 n4 v9 v10 v15 host4 v5 v12 dyn v13 final r2c v14 r2b ncu2 v7 r2d r2a v11 v6 v8 r2e r2f r2g r2h r2j r2l r2m r2n r2o r2p r2q"
+  echo "usage: bash tools/gpu_recipes.sh <recipe>; recipes: sweep4 n4 v9 v10 v15 host4 v5 v12 dyn v13 final r2c v14 r2b ncu2 v7 r2d r2a v11 v6 v8 r2e r2f r2g r2h r2j r2l r2m r2n r2o r2p r2q r2r r2s r2t r2u"
   exit 2
 fi
 "recipe_$1"
