@@ -397,8 +397,25 @@ recipe_r2u() {
   LAM_CE_ONE_STREAM=1 timeout 200 python bench.py --gpus 2 --steps 5 --warmup 2 --no-e2e --no-cpu-baseline --no-verify --hop-mode ce > gpurun_out/r2u/n2_ce_one.log 2>&1
 }
 
+recipe_r2v() {
+  # round-2 final validation on 4 GPUs: smoke, pytest -m gpu, bench N=1 (driver K/W), N=2/4 chain,
+  # N=4 multicast, stress, reference arm
+  mkdir -p gpurun_out/r2v
+  (nvidia-smi -L; nproc; lscpu | grep "Model name") > gpurun_out/r2v/box.txt 2>&1
+  python -c "import __graft_entry__ as g; g.build()" > gpurun_out/r2v/build.log 2>&1
+  timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r2v/smoke.log 2>&1; echo rc=$? >> gpurun_out/r2v/smoke.log
+  LAM_DEBUG_FAIL=1 timeout 1800 python -m pytest tests -m gpu -q -rs --durations=10 > gpurun_out/r2v/pytest4.log 2>&1; echo rc=$? >> gpurun_out/r2v/pytest4.log
+  CUDA_VISIBLE_DEVICES=0 timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/r2v/n1.log 2>&1; echo rc=$? >> gpurun_out/r2v/n1.log
+  for n in 2 4; do
+  timeout 400 python bench.py --gpus $n --steps 20 --warmup 5 > gpurun_out/r2v/n$n.log 2>&1; echo rc=$? >> gpurun_out/r2v/n$n.log
+  done
+  timeout 400 python bench.py --gpus 4 --steps 10 --warmup 3 --no-e2e --no-cpu-baseline --hop-mode mc > gpurun_out/r2v/n4_mc.log 2>&1; echo rc=$? >> gpurun_out/r2v/n4_mc.log
+  timeout 600 python bench.py --gpus 4 --config stress --stress-steps 40 > gpurun_out/r2v/stress4.log 2>&1; echo rc=$? >> gpurun_out/r2v/stress4.log
+  CUDA_VISIBLE_DEVICES=0 timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/r2v/ref1.log 2>&1; echo rc=$? >> gpurun_out/r2v/ref1.log
+}
+
 if [ $# -ne 1 ] || ! declare -F "recipe_$1" > /dev/null; then
-  echo "usage: bash tools/gpu_recipes.sh <recipe>; recipes: sweep4 n4 v9 v10 v15 host4 v5 v12 dyn v13 final r2c v14 r2b ncu2 v7 r2d r2a v11 v6 v8 r2e r2f r2g r2h r2j r2l r2m r2n r2o r2p r2q r2r r2s r2t r2u"
+  echo "usage: bash tools/gpu_recipes.sh <recipe>; recipes: sweep4 n4 v9 v10 v15 host4 v5 v12 dyn v13 final r2c v14 r2b ncu2 v7 r2d r2a v11 v6 v8 r2e r2f r2g r2h r2j r2l r2m r2n r2o r2p r2q r2r r2s r2t r2u r2v"
   exit 2
 fi
 "recipe_$1"
