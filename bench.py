@@ -495,10 +495,14 @@ class Dist:
     def __init__(self, torch, N, rank):
         import torch.distributed as dist
         self.dist, self.torch, self.N, self.rank = dist, torch, N, rank
-        self.gloo = None
+        self.gloo = self.gloo_extra = None
         if N > 1:
+            from datetime import timedelta
             dist.init_process_group("nccl", device_id=torch.device("cuda", rank))
             self.gloo = dist.new_group(backend="gloo")
+            # the extra (headline) configurations run on a group with a 15 min timeout: a rank that failed
+            # alone turns the others' wait into an exception instead of a hang that would cost the line
+            self.gloo_extra = dist.new_group(backend="gloo", timeout=timedelta(seconds=900))
 
     def barrier(self):
         if self.gloo is not None:
@@ -1004,6 +1008,7 @@ def main():
     headline = None
     if args.headline == "on" or (args.headline == "auto" and N == 8):
         headline = {}
+        main_group, D.gloo = D.gloo, D.gloo_extra or D.gloo
         for name, model, config, tp in HEADLINE:
             if config == "relay-tp" and N < 2 or config == "colocated" and N % tp:
                 continue
@@ -1033,6 +1038,7 @@ def main():
                 import torch
                 torch.cuda.synchronize()
                 torch.cuda.empty_cache()
+        D.gloo = main_group
 
     if rank == 0:
         M = summ
