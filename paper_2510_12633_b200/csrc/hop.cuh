@@ -20,8 +20,10 @@
 //     last tile of that chunk: each consumer warp fences its stores, reduces its sums by shuffles and
 //     lane 0 deposits them (double-buffered) and arrives on the chunk's flush mbarrier; the flusher
 //     sums the 16 partials and does the 3 atomics; the CTA completing the chunk compares with the
-//     predecessor's header and releases the flag (st.release.sys) — or poisons it on mismatch so the
-//     successor aborts too.  v4 did this on consumer thread 0 between two CTA-wide
+//     predecessor's header (and re-reads the predecessor's flag: a chunk the predecessor poisoned
+//     carries the sums of its own corrupt bytes) and releases the flag (st.release.sys) — or poisons
+//     it on mismatch so the successor aborts too.  Multicast modes read the chunk from
+//     this GPU's replica of node 0's slot instead of the predecessor's memory (links[].src).  v4 did this on consumer thread 0 between two CTA-wide
 //     named barriers: ~10 % of the consumers' time (remote header loads, system fences).
 //   Failure (predecessor poisoned, abort, timeout): the producer records the job index it stopped
 //     at and arrives (without bytes) on that stage's full barrier; consumers finish every earlier
