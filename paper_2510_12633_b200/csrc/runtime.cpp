@@ -90,6 +90,9 @@ struct Part {
   HopTile* d_tiles_hyb = nullptr;
   RankLink* d_links_hyb = nullptr;   // [S][2N] (my slot): filled per launch from h_links_hyb
   RankLink* h_links_hyb = nullptr;   // pinned staging
+  std::vector<HopTile> h_tiles_hyb;  // host copy of d_tiles_hyb
+  const RankLink* last_links[LAM_MAX_SLOTS] = {};   // link table of the slot's last launch
+  int mc_retry[LAM_MAX_SLOTS] = {};  // multicast modes: verification retries of the slot's fill
   unsigned long long* prof_host = nullptr;  // LAM_HOP_PROF counters (host-mapped)
 };
 
@@ -530,6 +533,7 @@ lam_status alloc_parts(lam_ctx* c) {
         std::vector<HopTile> th = tiles;
         for (HopTile& t : th)
           if (c->chunk_mc[t.chunk]) t.rank += (uint32_t)N;
+        p.h_tiles_hyb = th;
         CK(cudaMalloc(&p.d_tiles_hyb, sizeof(HopTile) * std::max<size_t>(th.size(), 1)));
         if (!th.empty()) CK(cudaMemcpy(p.d_tiles_hyb, th.data(), sizeof(HopTile) * th.size(), cudaMemcpyHostToDevice));
         CK(cudaMalloc(&p.d_links_hyb, sizeof(RankLink) * 2 * N * S));
@@ -757,7 +761,8 @@ cudaError_t abort_part_kernel(lam_ctx* c, Part& p, int s) {
 
 // Resume list after a rebuild: every tile of every chunk the slot has not verified yet, with the
 // chunk's header sums and counter reset (chunks already verified keep their bytes and header).
-lam_status build_resume(lam_ctx* c, Part& p, int s, uint64_t u, uint32_t* n_out) {
+lam_status build_resume(lam_ctx* c, Part& p, int s, uint64_t u, uint32_t* n_out,
+                        const std::vector<HopTile>* from = nullptr) {
   ChunkMeta m = meta_of(c, p, s);
   const uint64_t total = c->plan.total_chunks;
   std::vector<uint64_t> flags(total);
@@ -765,7 +770,7 @@ lam_status build_resume(lam_ctx* c, Part& p, int s, uint64_t u, uint32_t* n_out)
   CK(cudaMemcpy(flags.data(), m.flags, 8 * total, cudaMemcpyDeviceToHost));
   std::vector<HopTile> res;
   std::vector<uint32_t> missing;
-  for (const HopTile& t : p.h_tiles) {
+  for (const HopTile& t : from ? *from : p.h_tiles) {
     if (flags[t.chunk] == u) continue;
     if (missing.empty() || missing.back() != t.chunk) missing.push_back(t.chunk);
     res.push_back(t);
@@ -938,6 +943,8 @@ lam_status launch_hop_part(lam_ctx* c, Part& p, int s, bool* launched) {
       links = p.d_links_hyb + (size_t)s * 2 * N;
       tiles = p.d_tiles_hyb;
     }
+    p.last_links[s] = links;
+    p.mc_retry[s] = 0;
     int rc = launch_hop(tiles, n_tiles, links, m, p.d_tiles_per_chunk, u, p.err_dev + s, c->timeout_ns,
                         // host-tier destination: PCIe stores need more CTAs in flight (v6 box run:
                         // 32 CTAs 29 GB/s, 148 CTAs 47 GB/s but starved the concurrent pulls)
@@ -954,6 +961,30 @@ lam_status launch_hop_part(lam_ctx* c, Part& p, int s, bool* launched) {
   sl.launched_mask |= 1ull << p.pos;
   c->shm->stats.hops_launched++;
   *launched = true;
+  return LAM_OK;
+}
+
+// Multicast modes: relaunch slot s's fill for the chunks it has not committed (kept chunks keep their
+// bytes, header and flag), with the link table of its last launch.
+lam_status retry_part(lam_ctx* c, Part& p, int s) {
+  ShmSlot& sl = c->shm->node[p.node].slot[s];
+  const uint64_t u = p.inflight_version[s];
+  CK(cudaSetDevice(p.device));
+  uint32_t n = 0;
+  const bool hyb_tiles = c->hyb && p.last_links[s] == p.d_links_hyb + (size_t)s * 2 * c->cfg.fsdp_size;
+  lam_status st = build_resume(c, p, s, u, &n, hyb_tiles ? &p.h_tiles_hyb : nullptr);
+  if (st != LAM_OK) return st;
+  p.err_host[s] = 0;
+  p.mc_retry[s]++;
+  fprintf(stderr, "liblam: node %d slot %d v%llu: re-verifying %u tiles from the multicast replica (retry %d)\n",
+          p.node, s, (unsigned long long)u, n, p.mc_retry[s]);
+  ChunkMeta m = meta_of(c, p, s);
+  if (launch_hop(p.d_resume, n, p.last_links[s], m, p.d_tiles_per_chunk, u, p.err_dev + s, c->timeout_ns, c->hop_ctas,
+                 p.stream))
+    return LAM_ECUDA;
+  if (n) c->shm->stats.kernel_launches++;
+  CK(cudaEventRecord(p.done_ev[s], p.stream));
+  (void)sl;
   return LAM_OK;
 }
 
@@ -1054,6 +1085,15 @@ lam_status step_locked(lam_ctx* c, int* transitions, bool* busy) {
         memset(p.prof_host, 0, 64);
       }
       const lam_status e = p.err_host[s] ? -(lam_status)p.err_host[s] : LAM_OK;
+      if (e == LAM_ECHECKSUM && c->mcast && p.mc_retry[s] < 2) {
+        // multicast modes: bytes stored through the switch may land at a replica after the chunk's flag
+        // (a rare mismatch under load, 7B hybrid on 4 GPUs): verify the failed chunks again from the
+        // replica before giving the version up.  A chunk whose bytes are really wrong fails again.
+        lam_status rs = retry_part(c, p, s);
+        if (rs != LAM_OK) return rs;
+        *busy = true;
+        continue;
+      }
       if (e != LAM_OK && getenv("LAM_DEBUG_FAIL")) {   // diagnostics: which chunk failed first
         std::vector<uint64_t> f(c->plan.total_chunks);
         ChunkMeta fm = meta_of(c, p, s);

@@ -414,8 +414,19 @@ recipe_r2v() {
   CUDA_VISIBLE_DEVICES=0 timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/r2v/ref1.log 2>&1; echo rc=$? >> gpurun_out/r2v/ref1.log
 }
 
+recipe_r2w() {
+  # multicast / hybrid verification retry: their parity tests, twice
+  mkdir -p gpurun_out/r2w
+  python -c "import __graft_entry__ as g; g.build()" > gpurun_out/r2w/build.log 2>&1
+  export LAM_DEBUG_FAIL=1
+  timeout 400 python -m pytest tests/test_gpu_parity.py -q -rs -k "multicast or hybrid" > gpurun_out/r2w/pytest_sp.log 2>&1; echo rc=$? >> gpurun_out/r2w/pytest_sp.log
+  for k in 1 2; do
+  timeout 900 python -m pytest tests/test_gpu_multiproc.py -q -rs -k "17 or 18 or 19 or 21 or 22 or 23" > gpurun_out/r2w/pytest_mp$k.log 2>&1; echo rc=$? >> gpurun_out/r2w/pytest_mp$k.log
+  done
+}
+
 if [ $# -ne 1 ] || ! declare -F "recipe_$1" > /dev/null; then
-  echo "usage: bash tools/gpu_recipes.sh <recipe>; recipes: sweep4 n4 v9 v10 v15 host4 v5 v12 dyn v13 final r2c v14 r2b ncu2 v7 r2d r2a v11 v6 v8 r2e r2f r2g r2h r2j r2l r2m r2n r2o r2p r2q r2r r2s r2t r2u r2v"
+  echo "usage: bash tools/gpu_recipes.sh <recipe>; recipes: sweep4 n4 v9 v10 v15 host4 v5 v12 dyn v13 final r2c v14 r2b ncu2 v7 r2d r2a v11 v6 v8 r2e r2f r2g r2h r2j r2l r2m r2n r2o r2p r2q r2r r2s r2t r2u r2v r2w"
   exit 2
 fi
 "recipe_$1"
