@@ -32,3 +32,34 @@ def test_reference_arm_other_ranks_exit_quietly():
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "2"],
                        capture_output=True, text=True, timeout=120, cwd=ROOT, env=env)
     assert r.returncode == 0 and not [l for l in r.stdout.splitlines() if l.startswith("{")]
+
+
+def test_nvlink_bound_chain_vs_multicast():
+    """The publish->all lower bound bench.py divides by: in the chain every middle relay
+    receives and forwards the image; with multicast (NEXT-2) node 0's GPU sends it once and no relay
+    forwards — the per-GPU maximum is M either way, only the distribution differs."""
+    sys.path.insert(0, ROOT)
+    import bench
+    P = 1000
+    T = bench.topology("chain", 4, 0)
+    ing, egr = bench.nvlink_bound(T, 4, P)
+    assert [ing[d] for d in range(4)] == [0, 2 * P, 2 * P, 2 * P]
+    assert [egr[d] for d in range(4)] == [2 * P, 2 * P, 2 * P, 0]
+    ing, egr = bench.nvlink_bound(T, 4, P, multicast=True)
+    assert [ing[d] for d in range(4)] == [0, 2 * P, 2 * P, 2 * P]
+    assert [egr[d] for d in range(4)] == [2 * P, 0, 0, 0]
+    T = bench.topology("colocated", 4, 2)          # FSDP-4 colocated: no hop, pulls gather instead
+    ing, egr = bench.nvlink_bound(T, 4, P, pull_in={0: 7.0})
+    assert ing[0] == 7.0 and max(egr.values()) == 0
+
+
+def test_line_config_is_shared_by_both_arms():
+    """The driver compares the two arms only on the same `config` object."""
+    sys.path.insert(0, ROOT)
+    import bench
+    import argparse
+    args = argparse.Namespace(model="7b", config="chain", tp=0, hop_mode="kernel")
+    c1, c2 = bench.line_config(args, 1), bench.line_config(args, 1)
+    assert c1 == c2 and c1["params"] == 7615616512 and c1["snapshot_bytes"] == 2 * 7615616512
+    args.hop_mode = "mc"
+    assert bench.line_config(args, 4)["parallelism"] == "chain N=4 hop=mc"

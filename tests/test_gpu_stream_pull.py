@@ -169,6 +169,39 @@ def test_colocated_subscription(model, N):
     ctx.close()
 
 
+def test_subscription_refused_when_actor_ranks_span_gpus():
+    """the pack writes only the shards packed on the rollout's own GPU, so a colocated
+    subscription is refused (LAM_EINVAL) unless every actor rank is on that GPU — the rollout would
+    otherwise run with a partial version.  The same rollout pulls the version normally instead."""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs >= 2 GPUs")
+    od = OMODELS["tiny"]
+    ctx = lam.Context(lam.Config(model=MODELS["tiny"], fsdp_size=2, actor_devices=[0, 1], rollouts=[(0, 0)],
+                                 chunk_bytes=16 * 4096))
+    rb = RolloutBuffers(MODELS["tiny"], 1, 0, 0)
+    with pytest.raises(lam.LamError) as e:
+        ctx.subscribe(0, rb.tp, None)
+    assert e.value.status == lam.LAM_EINVAL
+    shards = [ActorShard(MODELS["tiny"], 2, r, r) for r in range(2)]
+    for sh in shards:
+        sh.fill(SEED, 1, specials=True)
+    torch.cuda.synchronize()
+    for r, sh in enumerate(shards):
+        with torch.cuda.device(r):
+            assert ctx.publish(1, r, sh.shards(), torch.cuda.current_stream().cuda_stream) == lam.LAM_OK
+    for _ in range(100000):
+        if ctx.relay_step()[0] == lam.LAM_IDLE:
+            break
+    s = torch.cuda.Stream(device=0)
+    assert ctx.pull(0, rb.tp, s.cuda_stream) == 1      # gathers rank 1's region from GPU 1 over NVLink
+    s.synchronize()
+    want = direct_pull(od, 1, 0, SEED, 1, specials=True)
+    for name, t in rb.bufs.items():
+        g = t.view(torch.int16).cpu().numpy().view(np.uint16)
+        assert np.array_equal(g, want[name].reshape(g.shape)), name
+    ctx.close()
+
+
 def test_stream_pull_of_a_corrupt_version_fails():
     ctx = lam.Context(lam.Config(model=MODELS["tiny"], relays=[[0]], rollouts=[(1, 0)], chunk_bytes=16 * 4096))
     shard = ActorShard(MODELS["tiny"], 1, 0, 0)
