@@ -913,6 +913,11 @@ def summarize(P: Placement, res, steps, rank0_extra=None):
                     algorithmic_bytes_per_launch=dom["bytes"], launch_ms=dom["ms"], peak_source=src)
         if dom["bound"] == "nvlink":
             roof["per_link_gbs"] = ach / 18.0       # 18 NVLink 5 links per GPU, 50 GB/s/dir each
+            # what the fabric gives each transport on this pool (tools/chain_bench.cu, 1 GiB per hop, every
+            # hop at once): a relay that also serves its successor tops out below a lone hop
+            roof["transport_ceilings_gbs"] = dict(single_hop_tma_pull=782, middle_relay_tma_pull=668,
+                                                  middle_relay_copy_engines=765, multicast_store=558,
+                                                  source="profiles/r2/r2f_chain_bench_4gpu.txt, r2g_mc_bench.txt")
             nvl = traffic_of("nvlink:" + dom["kernel"], P.model_name, N, P.config)
             if nvl:   # ncu nvlrx/nvltx of the same kernel (raw link bytes incl. packet headers / read requests)
                 roof["nvlink_traffic"] = dict(nvl, source="ncu nvlrx__bytes.sum / nvltx__bytes.sum per launch")
