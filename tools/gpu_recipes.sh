@@ -425,8 +425,17 @@ recipe_r2w() {
   done
 }
 
+recipe_r2x() {
+  # K-major reshard: double-buffered k_pull_t (12 warps x 2 blocks) vs the round-1 single buffer
+  mkdir -p gpurun_out/r2x
+  python -c "import __graft_entry__ as g; g.build()" > gpurun_out/r2x/build.log 2>&1
+  timeout 600 python -m pytest tests/test_gpu_parity.py -q -x -rs -k "k_major or pull_rules" > gpurun_out/r2x/pytest_kmajor.log 2>&1; echo rc=$? >> gpurun_out/r2x/pytest_kmajor.log
+  timeout 300 python tools/pull_bench.py --tps 1,2,4 --layouts k-major > gpurun_out/r2x/pull_dbl.log 2>&1
+  LAM_PULL_T_SINGLE=1 timeout 300 python tools/pull_bench.py --tps 1,2,4 --layouts k-major > gpurun_out/r2x/pull_single.log 2>&1
+}
+
 if [ $# -ne 1 ] || ! declare -F "recipe_$1" > /dev/null; then
-  echo "usage: bash tools/gpu_recipes.sh <recipe>; recipes: sweep4 n4 v9 v10 v15 host4 v5 v12 dyn v13 final r2c v14 r2b ncu2 v7 r2d r2a v11 v6 v8 r2e r2f r2g r2h r2j r2l r2m r2n r2o r2p r2q r2r r2s r2t r2u r2v r2w"
+  echo "usage: bash tools/gpu_recipes.sh <recipe>; recipes: sweep4 n4 v9 v10 v15 host4 v5 v12 dyn v13 final r2c v14 r2b ncu2 v7 r2d r2a v11 v6 v8 r2e r2f r2g r2h r2j r2l r2m r2n r2o r2p r2q r2r r2s r2t r2u r2v r2w r2x"
   exit 2
 fi
 "recipe_$1"
