@@ -434,8 +434,18 @@ recipe_r2x() {
   LAM_PULL_T_SINGLE=1 timeout 300 python tools/pull_bench.py --tps 1,2,4 --layouts k-major > gpurun_out/r2x/pull_single.log 2>&1
 }
 
+recipe_r2y() {
+  # HEAD validation on 4 GPUs after the last changes: smoke, pytest -m gpu, bench N=1 and N=4
+  mkdir -p gpurun_out/r2y
+  python -c "import __graft_entry__ as g; g.build()" > gpurun_out/r2y/build.log 2>&1
+  timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r2y/smoke.log 2>&1; echo rc=$? >> gpurun_out/r2y/smoke.log
+  LAM_DEBUG_FAIL=1 timeout 1800 python -m pytest tests -m gpu -q -rs --durations=10 > gpurun_out/r2y/pytest4.log 2>&1; echo rc=$? >> gpurun_out/r2y/pytest4.log
+  CUDA_VISIBLE_DEVICES=0 timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/r2y/n1.log 2>&1; echo rc=$? >> gpurun_out/r2y/n1.log
+  timeout 400 python bench.py --gpus 4 --steps 20 --warmup 5 > gpurun_out/r2y/n4.log 2>&1; echo rc=$? >> gpurun_out/r2y/n4.log
+}
+
 if [ $# -ne 1 ] || ! declare -F "recipe_$1" > /dev/null; then
-  echo "usage: bash tools/gpu_recipes.sh <recipe>; recipes: sweep4 n4 v9 v10 v15 host4 v5 v12 dyn v13 final r2c v14 r2b ncu2 v7 r2d r2a v11 v6 v8 r2e r2f r2g r2h r2j r2l r2m r2n r2o r2p r2q r2r r2s r2t r2u r2v r2w r2x"
+  echo "usage: bash tools/gpu_recipes.sh <recipe>; recipes: sweep4 n4 v9 v10 v15 host4 v5 v12 dyn v13 final r2c v14 r2b ncu2 v7 r2d r2a v11 v6 v8 r2e r2f r2g r2h r2j r2l r2m r2n r2o r2p r2q r2r r2s r2t r2u r2v r2w r2x r2y"
   exit 2
 fi
 "recipe_$1"
