@@ -141,9 +141,11 @@ typedef struct {
 
 /* How a relay moves a chunk from its predecessor (all chunk-pipelined and verified):
  *  LAM_HOP_KERNEL       k_hop: TMA bulk copies through shared memory by ~32 SMs, checksum on the fly
- *  LAM_HOP_COPY_ENGINE  copy engines (zero SMs for the transfer): per chunk the relay's stream waits
- *                       for the predecessor's flag (stream memory op), cudaMemcpyAsync pulls the chunk
- *                       over NVLink, then k_verify checksums it in local HBM and releases the flag.
+ *  LAM_HOP_COPY_ENGINE  copy engines (zero SMs for the transfer): lam_relay_step enqueues a chunk's
+ *                       cudaMemcpyAsync once the host mirror shows the predecessor's flag (without the
+ *                       mapped control block: behind a stream wait on the flag), then k_verify
+ *                       checksums it in local HBM and releases the flag.  Slower than LAM_HOP_KERNEL in
+ *                       multi-process runs.
  *  LAM_HOP_MULTICAST    NVSwitch multicast broadcast (the bandwidth
  *                       term M·T_byte is the floor): no chain — every relay's predecessor is node 0.  The
  *                       pack stores the bf16 image once through a multicast object (multimem.st) bound
@@ -151,8 +153,10 @@ typedef struct {
  *                       followed by each chunk's flag; each relay's k_hop then verifies and commits the
  *                       chunk from its local replica (HBM -> HBM).  The source GPU sends M once, relays
  *                       forward nothing.  Requires every actor rank on one GPU, HBM relay nodes, node-0
- *                       rollouts on that GPU, and multicast-capable devices (NVSwitch); costs each relay
- *                       GPU S extra image-sized replicas.  LAM_EINVAL otherwise. */
+ *                       rollouts on that GPU, and multicast-capable devices (NVSwitch, >= 2 GPUs); costs
+ *                       each relay GPU S extra image-sized replicas.  LAM_EINVAL otherwise.  A chunk that
+ *                       fails verification from the replica is re-verified (twice) before the version
+ *                       is given up: switch-stored bytes may land after the chunk's flag. */
 /*  LAM_HOP_HYBRID       both at once (B200-native; NEXT-2 and the chain of P:L661-665 share the links):
  *                       the pack multicasts a share of the chunks (hybrid_mc_pct) into every relay GPU's
  *                       replica and stores the others locally; each relay's k_hop takes the multicast
