@@ -166,7 +166,16 @@ typedef struct {
  *                       chain no longer both serves and receives the whole image.  Same requirements as
  *                       LAM_HOP_MULTICAST, plus no relay part on the actor GPU.  A relay that starts a
  *                       version node 0 no longer holds pulls every chunk from its predecessor. */
-enum { LAM_HOP_KERNEL = 0, LAM_HOP_COPY_ENGINE = 1, LAM_HOP_MULTICAST = 2, LAM_HOP_HYBRID = 3 };
+/*  LAM_HOP_TREE         two-level broadcast over the same TMA hop kernel: relay k owns the chunks j with
+ *                       j mod R == k-1 (R relays) and pulls them from node 0; every other chunk it pulls
+ *                       from the relay that owns it, in an order staggered by k so the R-1 pullers of a
+ *                       moment read from different owners.  Every relay receives M and forwards
+ *                       (R-1)/R of it, pipeline depth 2 (the chain: forwards M, depth R).  Control plane:
+ *                       every relay's predecessor is node 0; the first relay to start v opens v at every
+ *                       idle relay (gang start) and each fill pins the slot of v at the relays it reads
+ *                       from; a chunk whose owner is not filling v comes from node 0.  Requires relay
+ *                       nodes stored whole on distinct GPUs that are not actor GPUs, in HBM. */
+enum { LAM_HOP_KERNEL = 0, LAM_HOP_COPY_ENGINE = 1, LAM_HOP_MULTICAST = 2, LAM_HOP_HYBRID = 3, LAM_HOP_TREE = 4 };
 
 /* One fp32 master shard piece owned by the caller: elements [elem_offset, elem_offset+elem_count)
  * of the flattened tensor `tensor_id`, at `ptr` (device memory of the actor rank's GPU). */
@@ -384,7 +393,7 @@ typedef struct lam_ctl lam_ctl;
 lam_ctl* lam_ctl_open(const char* name, int32_t create, int32_t n_nodes, int32_t slots, int32_t fsdp_size);
 /* Same, with the topology of a hop mode: LAM_HOP_MULTICAST = star (every relay's predecessor is node
  * 0), LAM_HOP_HYBRID = chain whose fills also pin node 0's slot of their version (the multicast share
- * is read from node 0's replica), others = chain. */
+ * is read from node 0's replica), LAM_HOP_TREE = star + gang start + peer pins, others = chain. */
 lam_ctl* lam_ctl_open_mode(const char* name, int32_t create, int32_t n_nodes, int32_t slots, int32_t fsdp_size,
                            int32_t hop_mode);
 void lam_ctl_close(lam_ctl*);

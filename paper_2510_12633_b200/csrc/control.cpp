@@ -12,6 +12,8 @@
 #include <unistd.h>
 
 #include <new>
+#include <utility>
+#include <vector>
 
 namespace lam {
 
@@ -138,16 +140,18 @@ static void open_slot(ShmSlot& sl, uint64_t v, int src_slot) {
   sl.err = 0;
   sl.src_slot = src_slot;
   sl.src0_slot = -1;
+  sl.peer_mask = 0;
   sl.launched_mask = 0;
   sl.epoch++;
 }
 
-void init(Shm* sh, int n_nodes, bool star, bool hybrid) {
+void init(Shm* sh, int n_nodes, bool star, bool hybrid, bool tree) {
   sh->n_nodes = n_nodes;
   sh->hybrid = hybrid ? 1 : 0;
+  sh->tree = tree ? 1 : 0;
   for (int i = 0; i <= LAM_MAX_NODES; ++i) {
     sh->node[i].dead = 0;
-    sh->node[i].pred = star && i > 0 ? 0 : i - 1;
+    sh->node[i].pred = (star || tree) && i > 0 ? 0 : i - 1;
   }
 }
 
@@ -155,6 +159,33 @@ void init(Shm* sh, int n_nodes, bool star, bool hybrid) {
 static void unpin_src0(Shm* sh, ShmSlot& sl) {
   if (sl.src0_slot >= 0 && sh->node[0].slot[sl.src0_slot].readers > 0) sh->node[0].slot[sl.src0_slot].readers--;
   sl.src0_slot = -1;
+}
+
+// A two-level fill's pins of its peers' slots of the same version end with the fill (or one peer's:
+// the failed one, whose chunks the fill then takes from node 0).
+static void unpin_peer(Shm* sh, ShmSlot& sl, int o) {
+  if (!(sl.peer_mask >> o & 1ull)) return;
+  ShmSlot& ps = sh->node[o].slot[sl.peer_slot[o]];
+  if (ps.readers > 0) ps.readers--;
+  sl.peer_mask &= ~(1ull << o);
+}
+static void unpin_peers(Shm* sh, ShmSlot& sl) {
+  for (int o = 1; o <= LAM_MAX_NODES && sl.peer_mask; ++o) unpin_peer(sh, sl, o);
+}
+
+// Two-level fill of `node` in slot s: pin the slot of its version at every other live relay that holds
+// it (FILLING or COMPLETE) — their chunks come from them, the rest from node 0.
+static void pin_peers(Shm* sh, int S, int node, int s) {
+  ShmSlot& sl = sh->node[node].slot[s];
+  for (int o = 1; o < sh->n_nodes; ++o) {
+    if (o == node || sh->node[o].dead) continue;
+    int ps = find_slot(sh->node[o], S, sl.version, S_COMPLETE);
+    if (ps < 0) ps = find_slot(sh->node[o], S, sl.version, S_FILLING);
+    if (ps < 0) continue;
+    sh->node[o].slot[ps].readers++;
+    sl.peer_slot[o] = (int8_t)ps;
+    sl.peer_mask |= 1ull << o;
+  }
 }
 
 bool fail_node(Shm* sh, int S, int node, uint64_t now_ns) {
@@ -170,11 +201,26 @@ bool fail_node(Shm* sh, int S, int node, uint64_t now_ns) {
     if (sl.state == S_FILLING) {
       if (sl.src_slot >= 0 && sh->node[d.pred].slot[sl.src_slot].readers > 0) sh->node[d.pred].slot[sl.src_slot].readers--;
       unpin_src0(sh, sl);
+      unpin_peers(sh, sl);
       sl.state = S_FREE;
       sl.version = 0;
       sl.src_slot = -1;
     }
   }
+  // two-level broadcast: fills that pull chunks from the dead relay restart (new epoch): their runtime
+  // takes the missing chunks from node 0
+  if (sh->tree)
+    for (int j = 1; j < sh->n_nodes; ++j) {
+      if (j == node || sh->node[j].dead) continue;
+      for (int s = 0; s < S; ++s) {
+        ShmSlot& sl = sh->node[j].slot[s];
+        if (sl.state != S_FILLING || !(sl.peer_mask >> node & 1ull)) continue;
+        unpin_peer(sh, sl, node);
+        sl.launched_mask = 0;
+        sl.parts_done = sl.parts_finished = 0;
+        sl.epoch++;
+      }
+    }
   // O(1) rebuild: the (single) successor links to the failed node's predecessor
   for (int j = node + 1; j < sh->n_nodes; ++j) {
     ShmNode& n = sh->node[j];
@@ -252,9 +298,36 @@ int start(Shm* sh, int S, int node, bool* started) {
   if (u <= n.started) return -1;
   const int s = acquire_slot(n, S);
   if (s < 0) return -1;
-  if (n.started && u > n.started + 1) {
+  if (!sh->tree && n.started && u > n.started + 1) {
     n.skipped += u - n.started - 1;
     sh->stats.versions_skipped += u - n.started - 1;
+  }
+  if (sh->tree) {
+    // two-level broadcast: gang start — open u at every idle live relay that can take it (this one
+    // included), then every newly opened fill pins the slot of u at each other relay holding it
+    int mine = -1;
+    std::vector<std::pair<int, int>> opened;
+    for (int o = 1; o < sh->n_nodes; ++o) {
+      ShmNode& no = sh->node[o];
+      if (no.dead || u <= no.started) continue;
+      bool filling = false;
+      for (int k = 0; k < S; ++k) filling |= no.slot[k].state == S_FILLING;
+      if (filling) continue;
+      const int so = o == node ? s : acquire_slot(no, S);
+      if (so < 0) continue;
+      if (no.started && u > no.started + 1) {
+        no.skipped += u - no.started - 1;
+        sh->stats.versions_skipped += u - no.started - 1;
+      }
+      open_slot(no.slot[so], u, ps);
+      sh->node[no.pred].slot[ps].readers++;
+      no.started = u;
+      opened.push_back({o, so});
+      if (o == node) mine = so;
+    }
+    for (auto& os : opened) pin_peers(sh, S, os.first, os.second);
+    *started = mine >= 0;
+    return mine;
   }
   open_slot(n.slot[s], u, ps);
   pred.slot[ps].readers++;
@@ -289,6 +362,7 @@ bool part_done(Shm* sh, int node, int slot, uint64_t v, int n_parts, lam_status 
       if (src.readers > 0) src.readers--;
     }
     unpin_src0(sh, sl);
+    unpin_peers(sh, sl);
     if (sl.err == 0) {
       sl.state = S_COMPLETE;
       if (v > n.latest) n.latest = v;
@@ -379,7 +453,8 @@ extern "C" lam_ctl* lam_ctl_open_mode(const char* name, int32_t create, int32_t 
     delete c;
     return nullptr;
   }
-  if (create || !c->mapped) ctl::init(c->sh, n_nodes, hop_mode == LAM_HOP_MULTICAST, hop_mode == LAM_HOP_HYBRID);
+  if (create || !c->mapped)
+    ctl::init(c->sh, n_nodes, hop_mode == LAM_HOP_MULTICAST, hop_mode == LAM_HOP_HYBRID, hop_mode == LAM_HOP_TREE);
   return c;
 }
 

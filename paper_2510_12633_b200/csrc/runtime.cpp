@@ -86,6 +86,9 @@ struct Part {
   std::vector<HopTile> h_tiles;      // host copy of the full tile list
   HopTile* d_resume = nullptr;       // tiles of the chunks still missing after a rebuild
   RankLink* d_links_dyn = nullptr;   // links to a predecessor other than node - 1
+  // tree: per-launch tiles (staggered, links index = source node * N + rank) and links [(R+1) N]
+  HopTile* d_tiles_tree = nullptr;
+  RankLink* d_links_tree = nullptr;
   // hybrid: tiles of multicast chunks index links[N + rank] (the replica), the others links[rank]
   HopTile* d_tiles_hyb = nullptr;
   RankLink* d_links_hyb = nullptr;   // [S][2N] (my slot): filled per launch from h_links_hyb
@@ -161,6 +164,7 @@ struct lam_ctx {
   bool star = false;                          // LAM_HOP_MULTICAST: every relay is fed by node 0
   bool hyb = false;                           // LAM_HOP_HYBRID: chain + multicast share
   bool mcast = false;                         // a multicast team exists (star or hybrid)
+  bool tree = false;                          // LAM_HOP_TREE: two-level broadcast
   McTeam mc;                                  // the multicast team (NEXT-2)
   std::vector<uint8_t> chunk_mc;              // hybrid: 1 = chunk goes by multicast
   std::map<std::string, PullPlan> plans;
@@ -212,7 +216,7 @@ int node_part_device(const lam_ctx* c, int node, int rank) {
 }
 
 // The predecessor a relay node has while nobody failed: node - 1 (chain), or node 0 (multicast star).
-int base_pred(const lam_ctx* c, int node) { return c->star ? 0 : node - 1; }
+int base_pred(const lam_ctx* c, int node) { return c->star || c->tree ? 0 : node - 1; }
 
 #define CK(x)                                             \
   do {                                                    \
@@ -364,8 +368,18 @@ lam_status validate(const lam_config& c, std::string* why) {
       return bad("rollout " + std::to_string(i));
   if (c.n_procs > 1 && c.shm_name[0] == 0) return bad("shm_name required with n_procs > 1");
   if (c.hop_mode != LAM_HOP_KERNEL && c.hop_mode != LAM_HOP_COPY_ENGINE && c.hop_mode != LAM_HOP_MULTICAST &&
-      c.hop_mode != LAM_HOP_HYBRID)
+      c.hop_mode != LAM_HOP_HYBRID && c.hop_mode != LAM_HOP_TREE)
     return bad("hop_mode");
+  if (c.hop_mode == LAM_HOP_TREE) {   // relays read each other's slots: whole, in HBM, one per GPU, off the actors
+    std::set<int> used(c.actor_device, c.actor_device + c.fsdp_size);
+    for (int i = 0; i < c.n_relays; ++i) {
+      const int d = c.relay[i].part_device[0];
+      for (int r = 1; r < c.fsdp_size; ++r)
+        if (c.relay[i].part_device[r] != d) return bad("tree hops: a relay node split over GPUs");
+      if (c.relay[i].host_memory) return bad("tree hops need HBM relay nodes");
+      if (!used.insert(d).second) return bad("tree hops: relays must sit on distinct non-actor GPUs");
+    }
+  }
   if (c.hop_mode == LAM_HOP_HYBRID) {   // a relay waiting on its replica must not share the pack's GPU
     for (int i = 0; i < c.n_relays; ++i)
       for (int r = 0; r < c.fsdp_size; ++r)
@@ -529,6 +543,10 @@ lam_status alloc_parts(lam_ctx* c) {
       }
       CK(cudaMalloc(&p.d_resume, sizeof(HopTile) * std::max<size_t>(tiles.size(), 1)));
       CK(cudaMalloc(&p.d_links_dyn, sizeof(RankLink) * N));
+      if (c->tree) {
+        CK(cudaMalloc(&p.d_tiles_tree, sizeof(HopTile) * std::max<size_t>(tiles.size(), 1)));
+        CK(cudaMalloc(&p.d_links_tree, sizeof(RankLink) * N * c->n_nodes));
+      }
       if (c->hyb) {
         std::vector<HopTile> th = tiles;
         for (HopTile& t : th)
@@ -920,6 +938,51 @@ lam_status launch_hop_part(lam_ctx* c, Part& p, int s, bool* launched) {
       lam_status st = build_links(c, p, s, pred, ps);
       if (st != LAM_OK) return st;
       links = p.d_links_dyn;
+    } else if (c->tree && !resume) {
+      // two-level broadcast: sources = node 0 (links [0, N)) and every relay this fill pinned (links
+      // [o N, (o+1) N)); chunk g comes from its owner (g mod R) + 1 when pinned, else from node 0;
+      // chunks are walked in groups of R, rotated by this node, so concurrent pullers hit different owners
+      const int R = c->n_nodes - 1;
+      std::vector<RankLink> tl((size_t)c->n_nodes * N);
+      for (int src = 0; src < c->n_nodes; ++src) {
+        if (src == p.node || (src > 0 && !(sl.peer_mask >> src & 1ull))) continue;
+        const int qs = src == 0 ? ps : sl.peer_slot[src];
+        for (int r : p.ranks) {
+          const Part& q = c->parts[c->node_rank_part[src][r]];
+          ChunkMeta qm = meta_of(c, q, qs);
+          RankLink& L = tl[(size_t)src * N + r];
+          L.src = slot_data(q, qs) + q.rank_off[r];
+          L.src_flags = qm.flags;
+          L.src_hdr = qm.hdr;
+          L.pred_flags = qm.flags;
+          L.dst = slot_data(p, s) + p.rank_off[r];
+        }
+      }
+      // chunk runs of the tile list, in chunk order
+      std::vector<std::pair<uint32_t, uint32_t>> runs;   // [begin, end) into h_tiles
+      for (uint32_t i = 0; i < p.h_tiles.size(); ++i)
+        if (runs.empty() || p.h_tiles[runs.back().first].chunk != p.h_tiles[i].chunk) runs.push_back({i, i + 1});
+        else runs.back().second = i + 1;
+      std::vector<HopTile> tt;
+      tt.reserve(p.h_tiles.size());
+      for (size_t g0 = 0; g0 < runs.size(); g0 += R) {
+        const size_t gn = std::min<size_t>(R, runs.size() - g0);
+        for (size_t k = 0; k < gn; ++k) {
+          const auto& run = runs[g0 + (k + (size_t)(p.node - 1)) % gn];
+          for (uint32_t i = run.first; i < run.second; ++i) {
+            HopTile t = p.h_tiles[i];
+            const int owner = (int)(t.chunk % (uint32_t)R) + 1;
+            const int src = owner != p.node && (sl.peer_mask >> owner & 1ull) ? owner : 0;
+            t.rank += (uint32_t)(src * N);
+            tt.push_back(t);
+          }
+        }
+      }
+      CK(cudaStreamSynchronize(p.stream));   // the previous launch (another version) used these tables
+      CK(cudaMemcpy(p.d_links_tree, tl.data(), sizeof(RankLink) * tl.size(), cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(p.d_tiles_tree, tt.data(), sizeof(HopTile) * tt.size(), cudaMemcpyHostToDevice));
+      links = p.d_links_tree;
+      tiles = p.d_tiles_tree;
     } else if (c->hyb && !resume && sl.src0_slot >= 0) {
       // hybrid: links [0, N) = the chain predecessor's slot, [N, 2N) = this GPU's replica of node 0's
       // slot holding u (pinned by this fill); the multicast chunks' tiles point at the latter
@@ -1326,7 +1389,8 @@ extern "C" lam_status lam_init(const lam_config* cfg, lam_ctx** out) {
   }
   st = setup_shm(c.get());
   if (st != LAM_OK) return st;
-  if (cfg->n_procs == 1 || cfg->proc_rank == 0) ctl::init(c->shm, c->n_nodes, c->star, c->hyb);
+  c->tree = cfg->hop_mode == LAM_HOP_TREE;
+  if (cfg->n_procs == 1 || cfg->proc_rank == 0) ctl::init(c->shm, c->n_nodes, c->star, c->hyb, c->tree);
   c->streams.resize(cfg->n_rollouts);
   // map the control block for the producer kernels' chunk-flag mirror (streaming pulls)
   for (int d = 0; d < LAM_MAX_DEVICES; ++d)
@@ -1958,6 +2022,8 @@ extern "C" void lam_destroy(lam_ctx* c) {
     if (p.d_tiles_per_chunk) cudaFree(p.d_tiles_per_chunk);
     if (p.d_links) cudaFree(p.d_links);
     if (p.d_tiles_hyb) cudaFree(p.d_tiles_hyb);
+    if (p.d_tiles_tree) cudaFree(p.d_tiles_tree);
+    if (p.d_links_tree) cudaFree(p.d_links_tree);
     if (p.d_links_hyb) cudaFree(p.d_links_hyb);
     if (p.h_links_hyb) cudaFreeHost(p.h_links_hyb);
     if (p.d_my_chunks) cudaFree(p.d_my_chunks);

@@ -22,7 +22,7 @@ LAM_ESHUTDOWN, LAM_EBUSY, LAM_ETIMEOUT, LAM_EIPC = -6, -7, -8, -9
 LAM_FSDP2_DIM0, LAM_FSDP1_FLAT = 0, 1
 LAM_REPLICATE, LAM_SHARD_DIM0, LAM_SHARD_DIM1, LAM_VOCAB_DIM0, LAM_HEAD_DIM0 = 0, 1, 2, 3, 4
 LAM_TILE_TRANSPOSE, LAM_TILE_ZERO = 0x100, 0xFFFFFFFF
-LAM_HOP_KERNEL, LAM_HOP_COPY_ENGINE, LAM_HOP_MULTICAST, LAM_HOP_HYBRID = 0, 1, 2, 3
+LAM_HOP_KERNEL, LAM_HOP_COPY_ENGINE, LAM_HOP_MULTICAST, LAM_HOP_HYBRID, LAM_HOP_TREE = 0, 1, 2, 3, 4
 
 
 class lam_model_dims(C.Structure):

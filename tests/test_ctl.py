@@ -375,3 +375,63 @@ def test_hybrid_fill_of_a_version_node0_no_longer_holds():
     assert c.slot(1, [k for k in (0, 1) if c.slot(1, k)[0] == 2][0])[2] == 1
     assert c.part_done(2, s2, 2) and c.latest(2) == 2
     c.close()
+
+
+def test_tree_gang_start_and_peer_pins():
+    """LAM_HOP_TREE: the first relay to start a version opens it at every idle relay (gang start); each
+    fill pins node 0's slot and the slot of the version at every other relay holding it; pins end with
+    the fills; a relay that fails mid-broadcast releases its pins and restarts its readers' fills."""
+    c = lam.Ctl("", True, n_nodes=4, slots=2, hop_mode=lam.LAM_HOP_TREE)
+    assert [c.pred(n) for n in (1, 2, 3)] == [0, 0, 0]
+    s0 = _publish(c, 1)
+    s1, v, opened = c.start(1)                    # opens v1 at relays 1, 2 and 3 at once
+    assert (v, opened) == (1, True)
+    fills = {1: s1}
+    for node in (2, 3):
+        s, u, op = c.start(node)                  # already FILLING: returned, not reopened
+        assert u == 1 and not op
+        fills[node] = s
+    assert c.slot(0, s0)[2] == 3                  # node 0 pinned by the three fills
+    for node in (1, 2, 3):                        # each pinned by the other two
+        assert c.slot(node, fills[node])[2] == 2
+    c.pack_done(s0, 1)
+    assert c.fail(3)                              # relay 3 dies mid-broadcast
+    assert c.slot(0, s0)[2] == 2                  # its own pin of node 0 is gone
+    assert c.slot(1, fills[1])[2] == 1 and c.slot(2, fills[2])[2] == 1   # and of its peers
+    for node in (1, 2):                           # the survivors no longer pin relay 3
+        assert c.part_done(node, fills[node], 1)
+    assert c.slot(0, s0)[2] == 0 and c.latest(1) == c.latest(2) == 1
+    assert [c.slot(n, fills[n])[2] for n in (1, 2)] == [0, 0]
+    c.close()
+
+
+def test_tree_late_relay_pins_only_holders():
+    """A relay still filling the previous version misses the gang start of the next; it starts that
+    version later and then pins the relays that hold it, while their earlier fills do not pin it."""
+    c = lam.Ctl("", True, n_nodes=3, slots=2, hop_mode=lam.LAM_HOP_TREE)
+
+    def filling(node, v):
+        return [k for k in (0, 1) if c.slot(node, k)[:2] == (v, FILLING)][0]
+
+    s = _publish(c, 1)
+    c.pack_done(s, 1)
+    c.start(1)                                    # gang: v1 at relays 1 and 2
+    for node in (1, 2):
+        assert c.part_done(node, filling(node, 1), 1)
+    s = _publish(c, 2)
+    c.pack_done(s, 2)
+    c.start(1)                                    # gang: v2 at relays 1 and 2
+    assert c.part_done(1, filling(1, 2), 2)       # relay 2 is still receiving v2
+    s = _publish(c, 3)
+    c.pack_done(s, 3)
+    c.start(1)                                    # gang: only relay 1 is idle
+    k13 = filling(1, 3)
+    assert c.slot(1, k13)[2] == 0                 # relay 2 does not hold v3: nothing pinned
+    assert c.part_done(2, filling(2, 2), 2)
+    s2, u, opened = c.start(2)                    # late start of v3 at relay 2
+    assert (u, opened) == (3, True)
+    assert c.slot(1, k13)[2] == 1                 # relay 2 pins relay 1's v3 (it reads relay 1's chunks)
+    assert c.slot(2, s2)[2] == 0                  # relay 1's fill did not pin relay 2
+    assert c.part_done(1, k13, 3) and c.part_done(2, s2, 3)
+    assert c.slot(1, k13)[2] == 0 and c.latest(1) == c.latest(2) == 3
+    c.close()

@@ -389,6 +389,34 @@ def test_tiny_hybrid_broadcast(pct):
     ctx.close()
 
 
+def test_tiny_tree_broadcast():
+    """LAM_HOP_TREE: each relay pulls its own share of the chunks from node 0 and the others from the
+    relays that own them; three versions with specials, full image/header compare at every node and
+    TP=1 / TP=2 pulls at every relay against the oracle."""
+    n = ngpu()
+    if n < 3:
+        pytest.skip("needs >= 3 GPUs (two relays reading each other)")
+    od = OMODELS["tiny"]
+    C = 8 * 4096
+    relays = [[d] for d in range(1, n)]
+    rollouts = [(i + 1, relays[i][0]) for i in range(len(relays))]
+    ctx = make_ctx("tiny", 1, [0], relays, rollouts, C=C, hop_mode=lam.LAM_HOP_TREE)
+    shard = ActorShard(MODELS["tiny"], 1, 0, 0)
+    plan = image_plan([s for _, s in otensors(od)], 1, C)
+    for v in (1, 2, 3):
+        publish_all(ctx, [shard], v, True)
+        until_idle(ctx)
+        oimg, ohdr = publish(plan, SEED, v, specials=True)
+        for node in range(len(relays) + 1):
+            assert ctx.latest(node) == v
+            check_image(ctx, node, v, oimg, ohdr, C)
+        for rid, (_, dev) in enumerate(rollouts):
+            check_pull(ctx, rid, 1, 0, dev, v, True, od)
+            check_pull(ctx, rid, 2, v % 2, dev, v, True, od)
+    assert ctx.stats()["checksum_errors"] == 0
+    ctx.close()
+
+
 def test_multicast_corrupt_replica_is_never_committed():
     """A byte flipped in GPU 1's multicast replica of node 0's slot after the pack: relay 1's k_hop
     recomputes the checksum from that replica, rejects the version, and keeps serving v1 (SPEC L643);

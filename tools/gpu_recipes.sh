@@ -444,8 +444,20 @@ recipe_r2y() {
   timeout 400 python bench.py --gpus 4 --steps 20 --warmup 5 > gpurun_out/r2y/n4.log 2>&1; echo rc=$? >> gpurun_out/r2y/n4.log
 }
 
+recipe_r2z() {
+  # two-level broadcast (LAM_HOP_TREE): parity single/multi-process, bench N=2/4 vs the chain
+  mkdir -p gpurun_out/r2z
+  python -c "import __graft_entry__ as g; g.build()" > gpurun_out/r2z/build.log 2>&1
+  export LAM_DEBUG_FAIL=1
+  timeout 300 python -m pytest tests/test_gpu_parity.py -q -x -rs -k "tree" > gpurun_out/r2z/pytest_sp.log 2>&1; echo rc=$? >> gpurun_out/r2z/pytest_sp.log
+  timeout 900 python -m pytest tests/test_gpu_multiproc.py -q -x -rs -k "24 or 25" > gpurun_out/r2z/pytest_mp.log 2>&1; echo rc=$? >> gpurun_out/r2z/pytest_mp.log
+  for n in 4 3; do
+  timeout 300 python bench.py --gpus $n --steps 10 --warmup 3 --no-e2e --no-cpu-baseline --hop-mode tree > gpurun_out/r2z/n${n}_tree.log 2>&1; echo rc=$? >> gpurun_out/r2z/n${n}_tree.log
+  done
+}
+
 if [ $# -ne 1 ] || ! declare -F "recipe_$1" > /dev/null; then
-  echo "usage: bash tools/gpu_recipes.sh <recipe>; recipes: sweep4 n4 v9 v10 v15 host4 v5 v12 dyn v13 final r2c v14 r2b ncu2 v7 r2d r2a v11 v6 v8 r2e r2f r2g r2h r2j r2l r2m r2n r2o r2p r2q r2r r2s r2t r2u r2v r2w r2x r2y"
+  echo "usage: bash tools/gpu_recipes.sh <recipe>; recipes: sweep4 n4 v9 v10 v15 host4 v5 v12 dyn v13 final r2c v14 r2b ncu2 v7 r2d r2a v11 v6 v8 r2e r2f r2g r2h r2j r2l r2m r2n r2o r2p r2q r2r r2s r2t r2u r2v r2w r2x r2y r2z"
   exit 2
 fi
 "recipe_$1"
