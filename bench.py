@@ -59,12 +59,10 @@ def parse(argv=None):
     ap.add_argument("--tp", type=int, default=0, help="rollout TP size (colocated / relay-tp)")
     ap.add_argument("--chunk-mb", type=int, default=0, help="chunk size; 0 = Appendix D k*")
     ap.add_argument("--hop-ctas", type=int, default=0)
-    ap.add_argument("--hop-mode", default="kernel", choices=["kernel", "ce", "mc", "hybrid", "tree"],
+    ap.add_argument("--hop-mode", default="kernel", choices=["kernel", "ce", "mc", "tree"],
                     help="relay hop: TMA kernel, copy engines + k_verify, NVSwitch multicast (NEXT-2: the "
-                         "pack stores once through a multicast object, every relay verifies its replica), or "
-                         "hybrid (a share of the chunks by multicast, the rest down the TMA chain), or tree "
+                         "pack stores once through a multicast object, every relay verifies its replica), or tree "
                          "(two-level: each relay pulls its 1/R of the chunks from node 0, the rest from their owners)")
-    ap.add_argument("--mc-pct", type=int, default=0, help="hybrid: multicast share of the chunks (0 = 60 %%)")
     ap.add_argument("--stream-pull", default="auto", choices=["auto", "on", "off"],
                     help="on: rollouts reshard chunk by chunk while their relay receives (lam_pull_stream); "
                          "off: pull once the relay committed (lam_pull); auto: on for chain / relay-tp, off for "
@@ -559,9 +557,7 @@ class Placement:
                          pack_ctas=args.pack_ctas, pull_ctas=args.pull_ctas, pack_sms=args.pack_sms,
                          slots=args.slots or (3 if config == "stress" and N > 1 else 2),
                          hop_mode={"ce": lam.LAM_HOP_COPY_ENGINE, "mc": lam.LAM_HOP_MULTICAST,
-                                   "hybrid": lam.LAM_HOP_HYBRID, "tree": lam.LAM_HOP_TREE}.get(args.hop_mode,
-                                                                                              lam.LAM_HOP_KERNEL),
-                         hybrid_mc_pct=args.mc_pct,
+                                   "tree": lam.LAM_HOP_TREE}.get(args.hop_mode, lam.LAM_HOP_KERNEL),
                          host_relays=T.get("host_relays", []))
         self.ctx = ctx = lam.Context(cfg)
         if N > 1:

@@ -135,8 +135,6 @@ typedef struct {
   int32_t pack_sms;                        /* > 0: the pack runs on SMs 0..pack_sms-1 only (every SM
                                               fully occupied), leaving the others to the trainer's
                                               kernels (actor stall); 0 = all SMs */
-  int32_t hybrid_mc_pct;                   /* LAM_HOP_HYBRID: share of the chunks (percent, spread evenly)
-                                              that go by multicast; 0 => 60 */
 } lam_config;
 
 /* How a relay moves a chunk from its predecessor (all chunk-pipelined and verified):
@@ -157,15 +155,6 @@ typedef struct {
  *                       each relay GPU S extra image-sized replicas.  LAM_EINVAL otherwise.  A chunk that
  *                       fails verification from the replica is re-verified (twice) before the version
  *                       is given up: switch-stored bytes may land after the chunk's flag. */
-/*  LAM_HOP_HYBRID       both at once (B200-native; NEXT-2 and the chain of P:L661-665 share the links):
- *                       the pack multicasts a share of the chunks (hybrid_mc_pct) into every relay GPU's
- *                       replica and stores the others locally; each relay's k_hop takes the multicast
- *                       chunks from its replica (local HBM) and pulls the rest from its chain
- *                       predecessor, verifying all of them.  A relay GPU's ingress is still M, but the
- *                       multicast share costs no relay egress and no read requests, so the middle of the
- *                       chain no longer both serves and receives the whole image.  Same requirements as
- *                       LAM_HOP_MULTICAST, plus no relay part on the actor GPU.  A relay that starts a
- *                       version node 0 no longer holds pulls every chunk from its predecessor. */
 /*  LAM_HOP_TREE         two-level broadcast over the same TMA hop kernel: relay k owns the chunks j with
  *                       j mod R == k-1 (R relays) and pulls them from node 0; every other chunk it pulls
  *                       from the relay that owns it, in an order staggered by k so the R-1 pullers of a
@@ -175,7 +164,7 @@ typedef struct {
  *                       idle relay (gang start) and each fill pins the slot of v at the relays it reads
  *                       from; a chunk whose owner is not filling v comes from node 0.  Requires relay
  *                       nodes stored whole on distinct GPUs that are not actor GPUs, in HBM. */
-enum { LAM_HOP_KERNEL = 0, LAM_HOP_COPY_ENGINE = 1, LAM_HOP_MULTICAST = 2, LAM_HOP_HYBRID = 3, LAM_HOP_TREE = 4 };
+enum { LAM_HOP_KERNEL = 0, LAM_HOP_COPY_ENGINE = 1, LAM_HOP_MULTICAST = 2, LAM_HOP_TREE = 4 };  /* 3: withdrawn */
 
 /* One fp32 master shard piece owned by the caller: elements [elem_offset, elem_offset+elem_count)
  * of the flattened tensor `tensor_id`, at `ptr` (device memory of the actor rank's GPU). */
@@ -392,8 +381,7 @@ int64_t lam_plan_copy_tiles(const lam_model_dims*, int32_t actor_layout, int32_t
 typedef struct lam_ctl lam_ctl;
 lam_ctl* lam_ctl_open(const char* name, int32_t create, int32_t n_nodes, int32_t slots, int32_t fsdp_size);
 /* Same, with the topology of a hop mode: LAM_HOP_MULTICAST = star (every relay's predecessor is node
- * 0), LAM_HOP_HYBRID = chain whose fills also pin node 0's slot of their version (the multicast share
- * is read from node 0's replica), LAM_HOP_TREE = star + gang start + peer pins, others = chain. */
+ * 0), LAM_HOP_TREE = star + gang start + peer pins, others = chain. */
 lam_ctl* lam_ctl_open_mode(const char* name, int32_t create, int32_t n_nodes, int32_t slots, int32_t fsdp_size,
                            int32_t hop_mode);
 void lam_ctl_close(lam_ctl*);

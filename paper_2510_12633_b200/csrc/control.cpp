@@ -139,26 +139,18 @@ static void open_slot(ShmSlot& sl, uint64_t v, int src_slot) {
   sl.parts_done = sl.parts_finished = 0;
   sl.err = 0;
   sl.src_slot = src_slot;
-  sl.src0_slot = -1;
   sl.peer_mask = 0;
   sl.launched_mask = 0;
   sl.epoch++;
 }
 
-void init(Shm* sh, int n_nodes, bool star, bool hybrid, bool tree) {
+void init(Shm* sh, int n_nodes, bool star, bool tree) {
   sh->n_nodes = n_nodes;
-  sh->hybrid = hybrid ? 1 : 0;
   sh->tree = tree ? 1 : 0;
   for (int i = 0; i <= LAM_MAX_NODES; ++i) {
     sh->node[i].dead = 0;
     sh->node[i].pred = (star || tree) && i > 0 ? 0 : i - 1;
   }
-}
-
-// A hybrid fill's pin of node 0's slot (the multicast source) ends with the fill.
-static void unpin_src0(Shm* sh, ShmSlot& sl) {
-  if (sl.src0_slot >= 0 && sh->node[0].slot[sl.src0_slot].readers > 0) sh->node[0].slot[sl.src0_slot].readers--;
-  sl.src0_slot = -1;
 }
 
 // A two-level fill's pins of its peers' slots of the same version end with the fill (or one peer's:
@@ -200,7 +192,6 @@ bool fail_node(Shm* sh, int S, int node, uint64_t now_ns) {
     ShmSlot& sl = d.slot[s];
     if (sl.state == S_FILLING) {
       if (sl.src_slot >= 0 && sh->node[d.pred].slot[sl.src_slot].readers > 0) sh->node[d.pred].slot[sl.src_slot].readers--;
-      unpin_src0(sh, sl);
       unpin_peers(sh, sl);
       sl.state = S_FREE;
       sl.version = 0;
@@ -239,8 +230,7 @@ bool fail_node(Shm* sh, int S, int node, uint64_t now_ns) {
         sl.parts_done = sl.parts_finished = 0;
         sl.epoch++;
       } else {                             // abandon: start over with what the new predecessor has
-        unpin_src0(sh, sl);
-        sl.state = S_FREE;
+          sl.state = S_FREE;
         sl.version = 0;
         sl.src_slot = -1;
         n.started = n.latest;
@@ -331,15 +321,6 @@ int start(Shm* sh, int S, int node, bool* started) {
   }
   open_slot(n.slot[s], u, ps);
   pred.slot[ps].readers++;
-  if (sh->hybrid && node > 0) {              // multicast share of v: node 0's slot, if it still holds v
-    ShmNode& n0 = sh->node[0];
-    int s0 = find_slot(n0, S, u, S_COMPLETE);
-    if (s0 < 0) s0 = find_slot(n0, S, u, S_FILLING);
-    if (s0 >= 0) {
-      n0.slot[s0].readers++;
-      n.slot[s].src0_slot = s0;
-    }
-  }
   n.started = u;
   *started = true;
   return s;
@@ -361,7 +342,6 @@ bool part_done(Shm* sh, int node, int slot, uint64_t v, int n_parts, lam_status 
       ShmSlot& src = sh->node[n.pred].slot[sl.src_slot];
       if (src.readers > 0) src.readers--;
     }
-    unpin_src0(sh, sl);
     unpin_peers(sh, sl);
     if (sl.err == 0) {
       sl.state = S_COMPLETE;
@@ -454,7 +434,7 @@ extern "C" lam_ctl* lam_ctl_open_mode(const char* name, int32_t create, int32_t 
     return nullptr;
   }
   if (create || !c->mapped)
-    ctl::init(c->sh, n_nodes, hop_mode == LAM_HOP_MULTICAST, hop_mode == LAM_HOP_HYBRID, hop_mode == LAM_HOP_TREE);
+    ctl::init(c->sh, n_nodes, hop_mode == LAM_HOP_MULTICAST, hop_mode == LAM_HOP_TREE);
   return c;
 }
 

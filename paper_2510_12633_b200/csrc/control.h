@@ -29,7 +29,6 @@ struct ShmSlot {
   int32_t err, src_slot;               // first error; predecessor slot pinned while FILLING
   uint64_t launched_mask;              // node 0: ranks published; relays: parts launched
   uint32_t epoch;                      // bumped when the fill restarts from a new predecessor
-  int32_t src0_slot;                   // hybrid broadcast: node 0's slot pinned as the multicast source
   uint64_t peer_mask;                  // two-level broadcast: relays whose slot of `version` this fill
                                        // pinned (it pulls the chunks they own from them) ...
   int8_t peer_slot[LAM_MAX_NODES + 1]; // ... and which slot of each
@@ -50,8 +49,7 @@ struct Shm {
   uint64_t fail_ns[LAM_MAX_NODES + 1]; // steady-clock time each node was declared failed
   uint64_t hb_ns[LAM_MAX_DEVICES];     // per process heartbeat (steady clock, ns)
   uint64_t dead_procs;                 // bit mask
-  int32_t hybrid;                      // LAM_HOP_HYBRID: relays also read node 0's multicast replica
-  int32_t tree;                        // LAM_HOP_TREE: two-level broadcast (gang start, peer pins)
+  int32_t tree, _pad2;                 // LAM_HOP_TREE: two-level broadcast (gang start, peer pins)
   uint64_t last_fail_ns;               // most recent failure (repair-time accounting)
   ShmNode node[LAM_MAX_NODES + 1];
   // Host-visible mirror of every slot's chunk flags, written by the producer kernels through a
@@ -95,13 +93,11 @@ void unpin(Shm* sh, int node, int slot);
 // Anything FILLING, or a node behind its predecessor?
 bool busy(Shm* sh, int S, int n_nodes);
 // Chain of n_nodes (called once by the creator): every node alive, pred = node - 1; star (the
-// LAM_HOP_MULTICAST broadcast, NEXT-2): every relay's predecessor is node 0.  hybrid (LAM_HOP_HYBRID):
-// a chain whose relays also read part of every version from node 0's multicast replica, so a relay
-// that starts v also pins node 0's slot of v (while node 0 still holds it) until its fill ends.
+// LAM_HOP_MULTICAST broadcast, NEXT-2): every relay's predecessor is node 0.
 // tree (LAM_HOP_TREE): star for the predecessor (node 0), plus a gang start — the first relay to start
 // v opens v at every idle relay at once — and each fill pins the slot of v at every other relay that
 // holds v (it pulls the chunks those relays own from them).
-void init(Shm* sh, int n_nodes, bool star = false, bool hybrid = false, bool tree = false);
+void init(Shm* sh, int n_nodes, bool star = false, bool tree = false);
 // Relay failure: mark `node` dead and rebuild the chain in O(1): its successor is
 // linked to its (live) predecessor.  A successor that was filling from it re-pins the same version
 // at the new predecessor and restarts (slot epoch++, launch mask cleared: the runtime resumes from

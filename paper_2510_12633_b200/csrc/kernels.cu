@@ -70,7 +70,7 @@ __device__ __forceinline__ void mc_st_release_u64(uint64_t* p, uint64_t v) {
 // mode: the flag also goes through the switch to every relay GPU's member (after the chunk's data,
 // which took the same path), where that relay polls it in local HBM.
 __device__ __forceinline__ void publish_flag(const ChunkMeta& meta, uint32_t chunk, uint64_t value) {
-  if (meta.mc_flags && (!meta.mc_class || meta.mc_class[chunk])) mc_st_release_u64(meta.mc_flags + chunk, value);
+  if (meta.mc_flags) mc_st_release_u64(meta.mc_flags + chunk, value);
   st_release_sys(meta.flags + chunk, value);
   if (meta.mirror) st_release_sys(meta.mirror + chunk, value);
 }
@@ -167,10 +167,9 @@ __device__ void pack_flush(ChunkMeta meta, const uint32_t* units_per_chunk, cons
 }
 
 // SUB: compiled with the colocated-subscriber stores (separate instantiation: the plain pack keeps
-// its register budget and occupancy).  MC: `mc_dst` is the multicast VA of node 0's slot (NEXT-2): the
-// 16-B stores of a multicast chunk (every chunk, or those meta.mc_class marks — LAM_HOP_HYBRID) are
-// multimem.st, so its bf16 bytes land in the actor GPU's slot and in every relay GPU's replica in the
-// same pass; other chunks go to `dst` (the actor GPU's slot) only.
+// its register budget and occupancy).  MC: `mc_dst` is the multicast VA of node 0's slot (NEXT-2): every
+// 16-B store is a multimem.st, so the bf16 bytes land in the actor GPU's slot and in every relay GPU's
+// replica in the same pass.
 template <bool SUB, bool MC>
 __global__ void __launch_bounds__(kPackThreads) k_pack(const PackUnit* __restrict__ units, uint32_t n_units,
                                                        const float* const* __restrict__ shard_ptrs,
@@ -220,7 +219,7 @@ __global__ void __launch_bounds__(kPackThreads) k_pack(const PackUnit* __restric
       acc_n = 0;
     }
     const float* src = shard_ptrs[u.shard] + u.src_elem;
-    const bool mcs = MC && (!meta.mc_class || meta.mc_class[u.chunk]);   // uniform per unit
+    const bool mcs = MC;
     uint8_t* out = (mcs ? mc_dst : dst) + u.dst_off;
     // colocated subscriber (lam_subscribe): the same bf16 bytes also go to its TP=1 buffer
     uint8_t* out2 = SUB ? sub_dst[ui] : nullptr;

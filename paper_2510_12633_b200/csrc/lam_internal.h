@@ -132,11 +132,10 @@ struct ChunkMeta {          // device view of one slot's metadata in a node part
   int32_t* abort_flag;      // [1]
   uint64_t* mirror;         // [total_chunks] host-visible copy of flags (shared memory) or null
   uint64_t* mc_flags;       // LAM_HOP_MULTICAST pack: multicast VA of the slot's flag array, else null
-  const uint8_t* mc_class;  // LAM_HOP_HYBRID pack: [total_chunks] 1 = multicast chunk (null: every chunk)
 };
 constexpr uint32_t kMirrorChunks = 2048;  // chunks per slot mirrored to the host (streaming pulls)
 
-// mc_dst: multicast VA of the same slot (multicast / hybrid modes, with meta.mc_flags), else null
+// mc_dst: multicast VA of the same slot (LAM_HOP_MULTICAST, with meta.mc_flags), else null
 int launch_pack(const PackUnit* units, uint32_t n_units, const float* const* shard_ptrs, uint8_t* dst, uint8_t* mc_dst,
                 ChunkMeta meta, const uint32_t* units_per_chunk, uint64_t version, uint64_t n_total,
                 const uint64_t* chunk_len, int ctas, void* stream, uint8_t* const* sub_dst, uint32_t* work,

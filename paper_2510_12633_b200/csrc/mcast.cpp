@@ -8,8 +8,7 @@
 // relay GPU it is the local replica ("mirror") of node 0's slots that the relay's verify-and-commit
 // hop reads from local HBM.  The pack stores through the multicast VA (multimem.st), which exists
 // only in the process of the actor GPU.  The actor GPU's member is also handed to the other processes
-// (mapped there, read over NVLink): LAM_HOP_HYBRID relays pull the chunks that do not go by multicast
-// from it.
+// (mapped there): node 0's slot data is then a valid mapping in every process.
 //
 // Driver API through cudaGetDriverEntryPoint (the library does not link libcuda).  With one process
 // per GPU the multicast handle (a POSIX file descriptor) travels from the actor's process to the
@@ -239,8 +238,8 @@ lam_status mc_alloc_members(McTeam& t, const std::vector<int>& local_devs, uint6
       return LAM_ECUDA;
     }
     t.va[dev] = (uint8_t*)(uintptr_t)va;
-    // the owner's member (node 0's slots) is also read by this process's other team GPUs (single-process
-    // hybrid relays pull non-multicast chunks from it over NVLink); every other member only locally
+    // the owner's member (node 0's slots) is readable by this process's other team GPUs too (node 0's
+    // slot data mapped everywhere); every other member only locally
     std::vector<CUmemAccessDesc> acc;
     for (int other : local_devs)
       if (other == dev || dev == t.owner_dev) {
@@ -264,8 +263,7 @@ lam_status mc_setup(McTeam& t, const std::vector<int>& local_devs, bool owner, i
     CUmulticastObjectProp mp = mc_prop((int)t.devices.size(), t.size);
     if (!cu_ok(d.create(&t.mc, &mp), "cuMulticastCreate")) return LAM_ECUDA;
     if (n_peer_procs > 0) {
-      // the multicast object, and the owner's member (node 0's slot data: relays of the hybrid mode
-      // pull the chunks that do not go by multicast from it)
+      // the multicast object, and the owner's member (node 0's slot data, mapped in every process)
       int fds[2] = {-1, -1};
       if (!cu_ok(d.exp(&fds[0], t.mc, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0), "cuMemExportToShareableHandle") ||
           !cu_ok(d.exp(&fds[1], t.mem.at(t.owner_dev), CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0),

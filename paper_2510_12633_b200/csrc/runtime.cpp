@@ -89,11 +89,6 @@ struct Part {
   // tree: per-launch tiles (staggered, links index = source node * N + rank) and links [(R+1) N]
   HopTile* d_tiles_tree = nullptr;
   RankLink* d_links_tree = nullptr;
-  // hybrid: tiles of multicast chunks index links[N + rank] (the replica), the others links[rank]
-  HopTile* d_tiles_hyb = nullptr;
-  RankLink* d_links_hyb = nullptr;   // [S][2N] (my slot): filled per launch from h_links_hyb
-  RankLink* h_links_hyb = nullptr;   // pinned staging
-  std::vector<HopTile> h_tiles_hyb;  // host copy of d_tiles_hyb
   const RankLink* last_links[LAM_MAX_SLOTS] = {};   // link table of the slot's last launch
   int mc_retry[LAM_MAX_SLOTS] = {};  // multicast modes: verification retries of the slot's fill
   unsigned long long* prof_host = nullptr;  // LAM_HOP_PROF counters (host-mapped)
@@ -140,7 +135,6 @@ struct PendingPull {
 
 struct DevLocal {
   uint64_t* d_chunk_len = nullptr;   // per device: [total_chunks]
-  uint8_t* d_chunk_mc = nullptr;     // hybrid: [total_chunks] multicast class (actor GPU)
   uint32_t* d_pack_work = nullptr;   // k_pack's dynamic unit counter (packs are serialised on `side`)
   cudaStream_t side = nullptr;
 };
@@ -162,11 +156,9 @@ struct lam_ctx {
   std::vector<RankPub> pubs;                  // [N]; local ranks only used
   std::map<int, DevLocal> dev;                // devices owned by this process
   bool star = false;                          // LAM_HOP_MULTICAST: every relay is fed by node 0
-  bool hyb = false;                           // LAM_HOP_HYBRID: chain + multicast share
-  bool mcast = false;                         // a multicast team exists (star or hybrid)
+  bool mcast = false;                         // a multicast team exists (LAM_HOP_MULTICAST)
   bool tree = false;                          // LAM_HOP_TREE: two-level broadcast
   McTeam mc;                                  // the multicast team (NEXT-2)
-  std::vector<uint8_t> chunk_mc;              // hybrid: 1 = chunk goes by multicast
   std::map<std::string, PullPlan> plans;
   uint64_t plan_clock = 0;
   struct PullRing { uint32_t* d = nullptr; uint32_t next = 0; std::vector<cudaEvent_t> ev; };
@@ -267,7 +259,6 @@ ChunkMeta meta_of(const lam_ctx* c, const Part& p, int slot) {
   cm.abort_flag = reinterpret_cast<int32_t*>(m + c->sm.abort);
   cm.mirror = c->mirror_dev ? c->mirror_dev + ((uint64_t)p.node * LAM_MAX_SLOTS + slot) * kShmMirrorChunks : nullptr;
   cm.mc_flags = nullptr;
-  cm.mc_class = nullptr;
   return cm;
 }
 
@@ -368,7 +359,7 @@ lam_status validate(const lam_config& c, std::string* why) {
       return bad("rollout " + std::to_string(i));
   if (c.n_procs > 1 && c.shm_name[0] == 0) return bad("shm_name required with n_procs > 1");
   if (c.hop_mode != LAM_HOP_KERNEL && c.hop_mode != LAM_HOP_COPY_ENGINE && c.hop_mode != LAM_HOP_MULTICAST &&
-      c.hop_mode != LAM_HOP_HYBRID && c.hop_mode != LAM_HOP_TREE)
+      c.hop_mode != LAM_HOP_TREE)
     return bad("hop_mode");
   if (c.hop_mode == LAM_HOP_TREE) {   // relays read each other's slots: whole, in HBM, one per GPU, off the actors
     std::set<int> used(c.actor_device, c.actor_device + c.fsdp_size);
@@ -380,13 +371,7 @@ lam_status validate(const lam_config& c, std::string* why) {
       if (!used.insert(d).second) return bad("tree hops: relays must sit on distinct non-actor GPUs");
     }
   }
-  if (c.hop_mode == LAM_HOP_HYBRID) {   // a relay waiting on its replica must not share the pack's GPU
-    for (int i = 0; i < c.n_relays; ++i)
-      for (int r = 0; r < c.fsdp_size; ++r)
-        if (c.relay[i].part_device[r] == c.actor_device[0]) return bad("hybrid hops: a relay part on the actor GPU");
-    if (c.hybrid_mc_pct < 0 || c.hybrid_mc_pct > 100) return bad("hybrid_mc_pct");
-  }
-  if (c.hop_mode == LAM_HOP_MULTICAST || c.hop_mode == LAM_HOP_HYBRID) {
+  if (c.hop_mode == LAM_HOP_MULTICAST) {
     // one source GPU (the multicast writer), HBM relays, node-0 readers on the source GPU
     for (int r = 1; r < c.fsdp_size; ++r)
       if (c.actor_device[r] != c.actor_device[0]) return bad("multicast hops need every actor rank on one GPU");
@@ -452,13 +437,6 @@ lam_status alloc_parts(lam_ctx* c) {
     p.meta_stride = c->sm.bytes;
     p.alloc_bytes = p.meta_base + p.meta_stride * S;
   }
-  if (c->hyb) {
-    // hybrid: spread the multicast share evenly over the chunks (chunk g goes by multicast iff
-    // floor((g+1) pct / 100) > floor(g pct / 100))
-    const uint64_t pct = c->cfg.hybrid_mc_pct > 0 ? (uint64_t)c->cfg.hybrid_mc_pct : 60;
-    c->chunk_mc.assign(total, 0);
-    for (uint64_t g = 0; g < total; ++g) c->chunk_mc[g] = (g + 1) * pct / 100 > g * pct / 100;
-  }
   if (c->mcast) {
     // multicast team members (NEXT-2): node 0's S slots followed by S flag arrays, on the actor GPU
     // and every relay GPU this process owns
@@ -521,10 +499,6 @@ lam_status alloc_parts(lam_ctx* c) {
       if (total) CK(cudaMemcpy(dl.d_chunk_len, len.data(), 8 * total, cudaMemcpyHostToDevice));
       CK(cudaStreamCreateWithPriority(&dl.side, cudaStreamNonBlocking, lo));
       CK(cudaMalloc(&dl.d_pack_work, sizeof(uint32_t)));
-      if (c->hyb && total) {
-        CK(cudaMalloc(&dl.d_chunk_mc, total));
-        CK(cudaMemcpy(dl.d_chunk_mc, c->chunk_mc.data(), total, cudaMemcpyHostToDevice));
-      }
       c->dev[p.device] = dl;
     }
     if (p.node > 0) {
@@ -546,16 +520,6 @@ lam_status alloc_parts(lam_ctx* c) {
       if (c->tree) {
         CK(cudaMalloc(&p.d_tiles_tree, sizeof(HopTile) * std::max<size_t>(tiles.size(), 1)));
         CK(cudaMalloc(&p.d_links_tree, sizeof(RankLink) * N * c->n_nodes));
-      }
-      if (c->hyb) {
-        std::vector<HopTile> th = tiles;
-        for (HopTile& t : th)
-          if (c->chunk_mc[t.chunk]) t.rank += (uint32_t)N;
-        p.h_tiles_hyb = th;
-        CK(cudaMalloc(&p.d_tiles_hyb, sizeof(HopTile) * std::max<size_t>(th.size(), 1)));
-        if (!th.empty()) CK(cudaMemcpy(p.d_tiles_hyb, th.data(), sizeof(HopTile) * th.size(), cudaMemcpyHostToDevice));
-        CK(cudaMalloc(&p.d_links_hyb, sizeof(RankLink) * 2 * N * S));
-        CK(cudaHostAlloc(&p.h_links_hyb, sizeof(RankLink) * 2 * N * S, cudaHostAllocPortable));
       }
       p.h_tiles = tiles;
       CK(cudaMalloc(&p.d_tiles_per_chunk, 4 * std::max<uint64_t>(total, 1)));
@@ -779,8 +743,7 @@ cudaError_t abort_part_kernel(lam_ctx* c, Part& p, int s) {
 
 // Resume list after a rebuild: every tile of every chunk the slot has not verified yet, with the
 // chunk's header sums and counter reset (chunks already verified keep their bytes and header).
-lam_status build_resume(lam_ctx* c, Part& p, int s, uint64_t u, uint32_t* n_out,
-                        const std::vector<HopTile>* from = nullptr) {
+lam_status build_resume(lam_ctx* c, Part& p, int s, uint64_t u, uint32_t* n_out) {
   ChunkMeta m = meta_of(c, p, s);
   const uint64_t total = c->plan.total_chunks;
   std::vector<uint64_t> flags(total);
@@ -788,7 +751,7 @@ lam_status build_resume(lam_ctx* c, Part& p, int s, uint64_t u, uint32_t* n_out,
   CK(cudaMemcpy(flags.data(), m.flags, 8 * total, cudaMemcpyDeviceToHost));
   std::vector<HopTile> res;
   std::vector<uint32_t> missing;
-  for (const HopTile& t : from ? *from : p.h_tiles) {
+  for (const HopTile& t : p.h_tiles) {
     if (flags[t.chunk] == u) continue;
     if (missing.empty() || missing.back() != t.chunk) missing.push_back(t.chunk);
     res.push_back(t);
@@ -983,28 +946,6 @@ lam_status launch_hop_part(lam_ctx* c, Part& p, int s, bool* launched) {
       CK(cudaMemcpy(p.d_tiles_tree, tt.data(), sizeof(HopTile) * tt.size(), cudaMemcpyHostToDevice));
       links = p.d_links_tree;
       tiles = p.d_tiles_tree;
-    } else if (c->hyb && !resume && sl.src0_slot >= 0) {
-      // hybrid: links [0, N) = the chain predecessor's slot, [N, 2N) = this GPU's replica of node 0's
-      // slot holding u (pinned by this fill); the multicast chunks' tiles point at the latter
-      const int s0 = sl.src0_slot;
-      const Part& p0 = c->parts[c->node_parts[0][0]];
-      ChunkMeta m0 = meta_of(c, p0, s0);
-      RankLink* h = p.h_links_hyb + (size_t)s * 2 * N;
-      CK(cudaStreamSynchronize(p.stream));   // the staging row of slot s is reused: its last copy is done
-      CK(cudaMemcpy(h, links, sizeof(RankLink) * N, cudaMemcpyDeviceToHost));
-      uint8_t* mine = c->mc.va.at(p.device);
-      for (int r : p.ranks) {
-        RankLink& L = h[N + r];
-        L.src = mine + (uint64_t)s0 * p0.slot_stride + p0.rank_off[r];
-        L.src_flags = reinterpret_cast<const uint64_t*>(mine + c->mc.flags_off + (uint64_t)s0 * c->mc.flag_stride);
-        L.src_hdr = m0.hdr;
-        L.pred_flags = m0.flags;
-        L.dst = slot_data(p, s) + p.rank_off[r];
-      }
-      CK(cudaMemcpyAsync(p.d_links_hyb + (size_t)s * 2 * N, h, sizeof(RankLink) * 2 * N, cudaMemcpyHostToDevice,
-                         p.stream));
-      links = p.d_links_hyb + (size_t)s * 2 * N;
-      tiles = p.d_tiles_hyb;
     }
     p.last_links[s] = links;
     p.mc_retry[s] = 0;
@@ -1034,8 +975,7 @@ lam_status retry_part(lam_ctx* c, Part& p, int s) {
   const uint64_t u = p.inflight_version[s];
   CK(cudaSetDevice(p.device));
   uint32_t n = 0;
-  const bool hyb_tiles = c->hyb && p.last_links[s] == p.d_links_hyb + (size_t)s * 2 * c->cfg.fsdp_size;
-  lam_status st = build_resume(c, p, s, u, &n, hyb_tiles ? &p.h_tiles_hyb : nullptr);
+  lam_status st = build_resume(c, p, s, u, &n);
   if (st != LAM_OK) return st;
   p.err_host[s] = 0;
   p.mc_retry[s]++;
@@ -1150,7 +1090,7 @@ lam_status step_locked(lam_ctx* c, int* transitions, bool* busy) {
       const lam_status e = p.err_host[s] ? -(lam_status)p.err_host[s] : LAM_OK;
       if (e == LAM_ECHECKSUM && c->mcast && p.mc_retry[s] < 2) {
         // multicast modes: bytes stored through the switch may land at a replica after the chunk's flag
-        // (a rare mismatch under load, 7B hybrid on 4 GPUs): verify the failed chunks again from the
+        // (a rare mismatch under load, seen with a withdrawn multicast + chain mode): verify the failed chunks again from the
         // replica before giving the version up.  A chunk whose bytes are really wrong fails again.
         lam_status rs = retry_part(c, p, s);
         if (rs != LAM_OK) return rs;
@@ -1372,9 +1312,8 @@ extern "C" lam_status lam_init(const lam_config* cfg, lam_ctx** out) {
   c->pull_ctas = cfg->pull_ctas > 0 ? cfg->pull_ctas : 0;
   if (cfg->spin_timeout_s > 0) c->timeout_ns = (uint64_t)(cfg->spin_timeout_s * 1e9);
   c->pubs.resize(cfg->fsdp_size);
-  if (cfg->hop_mode == LAM_HOP_MULTICAST || cfg->hop_mode == LAM_HOP_HYBRID) {
-    c->star = cfg->hop_mode == LAM_HOP_MULTICAST;
-    c->hyb = cfg->hop_mode == LAM_HOP_HYBRID;
+  if (cfg->hop_mode == LAM_HOP_MULTICAST) {
+    c->star = true;
     c->mcast = true;
     std::set<int> team{cfg->actor_device[0]};
     for (int i = 0; i < cfg->n_relays; ++i)
@@ -1390,7 +1329,7 @@ extern "C" lam_status lam_init(const lam_config* cfg, lam_ctx** out) {
   st = setup_shm(c.get());
   if (st != LAM_OK) return st;
   c->tree = cfg->hop_mode == LAM_HOP_TREE;
-  if (cfg->n_procs == 1 || cfg->proc_rank == 0) ctl::init(c->shm, c->n_nodes, c->star, c->hyb, c->tree);
+  if (cfg->n_procs == 1 || cfg->proc_rank == 0) ctl::init(c->shm, c->n_nodes, c->star, c->tree);
   c->streams.resize(cfg->n_rollouts);
   // map the control block for the producer kernels' chunk-flag mirror (streaming pulls)
   for (int d = 0; d < LAM_MAX_DEVICES; ++d)
@@ -1620,7 +1559,6 @@ static lam_status publish_impl(lam_ctx* c, uint64_t v, int32_t rank, const lam_s
     if (!c->mc.mc_va) return LAM_ECUDA;
     mc_dst = c->mc.mc_va + (uint64_t)s * p.slot_stride;
     m.mc_flags = reinterpret_cast<uint64_t*>(c->mc.mc_va + c->mc.flags_off + (uint64_t)s * c->mc.flag_stride);
-    m.mc_class = c->hyb ? c->dev[dev].d_chunk_mc : nullptr;   // hybrid: only the multicast share
   }
   int rc = launch_pack(rp.d_units, rp.n_units, rp.d_ptrs, dst, mc_dst, m, rp.d_units_per_chunk, v,
                        c->plan.total_chunks, c->dev[dev].d_chunk_len, c->pack_ctas, side, sub,
@@ -1976,7 +1914,6 @@ extern "C" void lam_destroy(lam_ctx* c) {
     cudaDeviceSynchronize();
     if (kv.second.d_chunk_len) cudaFree(kv.second.d_chunk_len);
     if (kv.second.d_pack_work) cudaFree(kv.second.d_pack_work);
-    if (kv.second.d_chunk_mc) cudaFree(kv.second.d_chunk_mc);
     if (kv.second.side) cudaStreamDestroy(kv.second.side);
   }
   for (auto& kv : c->plans) {
@@ -2021,11 +1958,8 @@ extern "C" void lam_destroy(lam_ctx* c) {
     if (p.d_tiles) cudaFree(p.d_tiles);
     if (p.d_tiles_per_chunk) cudaFree(p.d_tiles_per_chunk);
     if (p.d_links) cudaFree(p.d_links);
-    if (p.d_tiles_hyb) cudaFree(p.d_tiles_hyb);
     if (p.d_tiles_tree) cudaFree(p.d_tiles_tree);
     if (p.d_links_tree) cudaFree(p.d_links_tree);
-    if (p.d_links_hyb) cudaFree(p.d_links_hyb);
-    if (p.h_links_hyb) cudaFreeHost(p.h_links_hyb);
     if (p.d_my_chunks) cudaFree(p.d_my_chunks);
     for (cudaEvent_t e : p.chunk_ev) cudaEventDestroy(e);
     if (p.vstream) cudaStreamDestroy(p.vstream);

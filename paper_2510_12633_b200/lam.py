@@ -22,7 +22,7 @@ LAM_ESHUTDOWN, LAM_EBUSY, LAM_ETIMEOUT, LAM_EIPC = -6, -7, -8, -9
 LAM_FSDP2_DIM0, LAM_FSDP1_FLAT = 0, 1
 LAM_REPLICATE, LAM_SHARD_DIM0, LAM_SHARD_DIM1, LAM_VOCAB_DIM0, LAM_HEAD_DIM0 = 0, 1, 2, 3, 4
 LAM_TILE_TRANSPOSE, LAM_TILE_ZERO = 0x100, 0xFFFFFFFF
-LAM_HOP_KERNEL, LAM_HOP_COPY_ENGINE, LAM_HOP_MULTICAST, LAM_HOP_HYBRID, LAM_HOP_TREE = 0, 1, 2, 3, 4
+LAM_HOP_KERNEL, LAM_HOP_COPY_ENGINE, LAM_HOP_MULTICAST, LAM_HOP_TREE = 0, 1, 2, 4
 
 
 class lam_model_dims(C.Structure):
@@ -47,8 +47,7 @@ class lam_config(C.Structure):
                 ("n_procs", C.c_int32), ("proc_of_device", C.c_int32 * LAM_MAX_DEVICES),
                 ("shm_name", C.c_char * 64), ("pack_ctas", C.c_int32), ("hop_ctas", C.c_int32),
                 ("pull_ctas", C.c_int32), ("spin_timeout_s", C.c_double), ("hop_mode", C.c_int32),
-                ("heartbeat_timeout_s", C.c_double), ("pack_sms", C.c_int32),
-                ("hybrid_mc_pct", C.c_int32)]
+                ("heartbeat_timeout_s", C.c_double), ("pack_sms", C.c_int32)]
 
 
 class lam_shard(C.Structure):
@@ -251,7 +250,6 @@ class Config:
     hop_mode: int = LAM_HOP_KERNEL
     heartbeat_timeout_s: float = 0.0
     pack_sms: int = 0                                            # > 0: pack confined to SMs 0..pack_sms-1
-    hybrid_mc_pct: int = 0                                       # LAM_HOP_HYBRID multicast share (0: 60 %)
     host_relays: list[int] = field(default_factory=list)     # relay nodes (1-based) kept in host memory
 
     def to_c(self) -> lam_config:
@@ -284,7 +282,6 @@ class Config:
         c.hop_mode = self.hop_mode
         c.heartbeat_timeout_s = self.heartbeat_timeout_s
         c.pack_sms = self.pack_sms
-        c.hybrid_mc_pct = self.hybrid_mc_pct
         return c
 
 

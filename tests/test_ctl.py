@@ -303,7 +303,7 @@ def test_sigkill_of_a_relay_process_is_detected_by_heartbeat_and_the_chain_rebui
     owner.close()
 
 
-# ---------------------------------------------------------------- multicast (star) and hybrid topologies
+# ---------------------------------------------------------------- multicast (star) and tree topologies
 def _publish(c, v):
     st, s = c.publish(v)
     assert st == lam.LAM_OK
@@ -329,51 +329,6 @@ def test_star_topology_every_relay_fed_by_node0():
     for node in (1, 3):
         assert c.part_done(node, fills[node], 1)
     assert c.slot(0, s0)[2] == 0 and c.latest(1) == c.latest(3) == 1
-    c.close()
-
-
-def test_hybrid_fills_pin_node0_until_done():
-    """LAM_HOP_HYBRID: a chain whose relays also read their version's multicast share from node 0's
-    replica — every fill pins node 0's slot of that version (besides its predecessor's) until it ends,
-    so node 0 cannot recycle the slot under a relay that is still reading its replica."""
-    c = lam.Ctl("", True, n_nodes=4, slots=2, hop_mode=lam.LAM_HOP_HYBRID)
-    assert [c.pred(n) for n in (1, 2, 3)] == [0, 1, 2]
-    s0 = _publish(c, 1)
-    s1, v, _ = c.start(1)                         # pins node 0 twice: predecessor + multicast source
-    assert v == 1 and c.slot(0, s0)[2] == 2
-    s2, v2, _ = c.start(2)                        # pins node 1 (predecessor) and node 0 (source)
-    assert v2 == 1 and c.slot(0, s0)[2] == 3 and c.slot(1, s1)[2] == 1
-    c.pack_done(s0, 1)
-    assert c.part_done(1, s1, 1)
-    assert c.slot(0, s0)[2] == 1                  # relay 2 still reads node 0's replica of v1
-    s3, _, _ = c.start(3)
-    assert c.slot(0, s0)[2] == 2
-    assert c.fail(2)                              # relay 3 resumes from relay 1, still pinning node 0
-    assert c.slot(0, s0)[2] == 1 and c.pred(3) == 1
-    assert c.part_done(3, s3, 1)
-    assert c.slot(0, s0)[2] == 0 and c.latest(3) == 1
-    c.close()
-
-
-def test_hybrid_fill_of_a_version_node0_no_longer_holds():
-    """A hybrid relay that starts a version node 0 already recycled pins only its predecessor (its
-    runtime then pulls every chunk down the chain)."""
-    c = lam.Ctl("", True, n_nodes=3, slots=2, hop_mode=lam.LAM_HOP_HYBRID)
-    for v in (1, 2):                              # relay 1 takes v1 and v2
-        s = _publish(c, v)
-        c.pack_done(s, v)
-        s1, u, _ = c.start(1)
-        assert u == v
-        assert c.part_done(1, s1, v)
-    for v in (3, 4):                              # node 0 runs ahead and recycles v2's slot
-        s = _publish(c, v)
-        c.pack_done(s, v)
-    assert {c.slot(0, k)[0] for k in (0, 1)} == {3, 4}
-    s2, u, _ = c.start(2)                         # relay 2 takes what relay 1 holds: v2
-    assert u == 2
-    assert [c.slot(0, k)[2] for k in (0, 1)] == [0, 0]     # no multicast source pinned
-    assert c.slot(1, [k for k in (0, 1) if c.slot(1, k)[0] == 2][0])[2] == 1
-    assert c.part_done(2, s2, 2) and c.latest(2) == 2
     c.close()
 
 

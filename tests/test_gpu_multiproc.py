@@ -48,10 +48,6 @@ CASES = [  # (min GPUs, args)
     (2, ["--config", "chain", "--model", "tiny", "--versions", "3", "--hop-mode", "2"]),
     (4, ["--config", "chain", "--model", "tiny", "--versions", "3", "--chunk-kb", "16", "--hop-mode", "2", "--stream"]),
     (4, ["--config", "chain", "--model", "7b", "--chunk-kb", str(128 << 10), "--hop-mode", "2"]),
-    # hybrid (multicast share + chain): the actor GPU's member crosses processes too
-    (2, ["--config", "chain", "--model", "tiny", "--versions", "3", "--hop-mode", "3"]),
-    (4, ["--config", "chain", "--model", "tiny", "--versions", "3", "--chunk-kb", "16", "--hop-mode", "3", "--stream"]),
-    (4, ["--config", "chain", "--model", "7b", "--chunk-kb", str(128 << 10), "--hop-mode", "3"]),
     # two-level broadcast: relays read each other's slots across processes
     (4, ["--config", "chain", "--model", "tiny", "--versions", "3", "--chunk-kb", "16", "--hop-mode", "4", "--stream"]),
     (4, ["--config", "chain", "--model", "7b", "--chunk-kb", str(128 << 10), "--hop-mode", "4", "--stream"]),

@@ -354,41 +354,6 @@ def test_tiny_multicast_broadcast():
     ctx.close()
 
 
-@pytest.mark.parametrize("pct", [60, 100, 0])
-def test_tiny_hybrid_broadcast(pct):
-    """LAM_HOP_HYBRID: the pack multicasts `pct` % of the chunks into every relay GPU's replica and the
-    relays chain-pull the rest; three versions with specials, full image/header compare at every node
-    and TP=1 / TP=2 pulls at every relay against the oracle (0 % = a plain chain, 100 % = every chunk
-    from the replica, still in chain order)."""
-    n = ngpu()
-    if n < 2:
-        pytest.skip("multicast needs >= 2 GPUs")
-    od = OMODELS["tiny"]
-    C = 8 * 4096
-    relays = [[d] for d in range(1, n)]
-    rollouts = [(i + 1, relays[i][0]) for i in range(len(relays))]
-    try:
-        ctx = make_ctx("tiny", 1, [0], relays, rollouts, C=C, hop_mode=lam.LAM_HOP_HYBRID, hybrid_mc_pct=pct)
-    except lam.LamError as e:
-        if e.status == lam.LAM_EINVAL:
-            pytest.skip("multicast objects not supported on this box")
-        raise
-    shard = ActorShard(MODELS["tiny"], 1, 0, 0)
-    plan = image_plan([s for _, s in otensors(od)], 1, C)
-    for v in (1, 2, 3):
-        publish_all(ctx, [shard], v, True)
-        until_idle(ctx)
-        oimg, ohdr = publish(plan, SEED, v, specials=True)
-        for node in range(len(relays) + 1):
-            assert ctx.latest(node) == v
-            check_image(ctx, node, v, oimg, ohdr, C)
-        for rid, (_, dev) in enumerate(rollouts):
-            check_pull(ctx, rid, 1, 0, dev, v, True, od)
-            check_pull(ctx, rid, 2, v % 2, dev, v, True, od)
-    assert ctx.stats()["checksum_errors"] == 0
-    ctx.close()
-
-
 def test_tiny_tree_broadcast():
     """LAM_HOP_TREE: each relay pulls its own share of the chunks from node 0 and the others from the
     relays that own them; three versions with specials, full image/header compare at every node and
