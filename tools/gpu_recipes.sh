@@ -456,8 +456,20 @@ recipe_r2z() {
   done
 }
 
+recipe_r2final() {
+  # after withdrawing the hybrid mode: smoke, every single-process parity test, the multi-process
+  # chain / multicast / tree / host cases
+  mkdir -p gpurun_out/r2final
+  python -c "import __graft_entry__ as g; g.build()" > gpurun_out/r2final/build.log 2>&1
+  timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r2final/smoke.log 2>&1; echo rc=$? >> gpurun_out/r2final/smoke.log
+  export LAM_DEBUG_FAIL=1
+  timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_stream_pull.py -q -rs > gpurun_out/r2final/pytest_sp.log 2>&1; echo rc=$? >> gpurun_out/r2final/pytest_sp.log
+  M=tests/test_gpu_multiproc.py::test_multiproc_parity
+  timeout 900 python -m pytest -q -rs "$M[0]" "$M[7]" "$M[14]" "$M[17]" "$M[18]" "$M[19]" "$M[21]" "$M[22]" > gpurun_out/r2final/pytest_mp.log 2>&1; echo rc=$? >> gpurun_out/r2final/pytest_mp.log
+}
+
 if [ $# -ne 1 ] || ! declare -F "recipe_$1" > /dev/null; then
-  echo "usage: bash tools/gpu_recipes.sh <recipe>; recipes: sweep4 n4 v9 v10 v15 host4 v5 v12 dyn v13 final r2c v14 r2b ncu2 v7 r2d r2a v11 v6 v8 r2e r2f r2g r2h r2j r2l r2m r2n r2o r2p r2q r2r r2s r2t r2u r2v r2w r2x r2y r2z"
+  echo "usage: bash tools/gpu_recipes.sh <recipe>; recipes: sweep4 n4 v9 v10 v15 host4 v5 v12 dyn v13 final r2c v14 r2b ncu2 v7 r2d r2a v11 v6 v8 r2e r2f r2g r2h r2j r2l r2m r2n r2o r2p r2q r2r r2s r2t r2u r2v r2w r2x r2y r2z r2final"
   exit 2
 fi
 "recipe_$1"
