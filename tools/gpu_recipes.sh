@@ -468,8 +468,17 @@ recipe_r2final() {
   timeout 900 python -m pytest -q -rs "$M[0]" "$M[7]" "$M[14]" "$M[17]" "$M[18]" "$M[19]" "$M[21]" "$M[22]" > gpurun_out/r2final/pytest_mp.log 2>&1; echo rc=$? >> gpurun_out/r2final/pytest_mp.log
 }
 
+recipe_r2driver() {
+  # what the driver runs at round end, on 1 GPU: smoke, pytest -m gpu, bench.py with its K/W
+  mkdir -p gpurun_out/r2driver
+  python -c "import __graft_entry__ as g; g.build()" > gpurun_out/r2driver/build.log 2>&1
+  timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r2driver/smoke.log 2>&1; echo rc=$? >> gpurun_out/r2driver/smoke.log
+  timeout 1200 python -m pytest tests -m gpu -q -rs > gpurun_out/r2driver/pytest1.log 2>&1; echo rc=$? >> gpurun_out/r2driver/pytest1.log
+  timeout 900 python bench.py --gpus 1 --steps 20 --warmup 5 > gpurun_out/r2driver/n1.log 2>&1; echo rc=$? >> gpurun_out/r2driver/n1.log
+}
+
 if [ $# -ne 1 ] || ! declare -F "recipe_$1" > /dev/null; then
-  echo "usage: bash tools/gpu_recipes.sh <recipe>; recipes: sweep4 n4 v9 v10 v15 host4 v5 v12 dyn v13 final r2c v14 r2b ncu2 v7 r2d r2a v11 v6 v8 r2e r2f r2g r2h r2j r2l r2m r2n r2o r2p r2q r2r r2s r2t r2u r2v r2w r2x r2y r2z r2final"
+  echo "usage: bash tools/gpu_recipes.sh <recipe>; recipes: sweep4 n4 v9 v10 v15 host4 v5 v12 dyn v13 final r2c v14 r2b ncu2 v7 r2d r2a v11 v6 v8 r2e r2f r2g r2h r2j r2l r2m r2n r2o r2p r2q r2r r2s r2t r2u r2v r2w r2x r2y r2z r2final r2driver"
   exit 2
 fi
 "recipe_$1"
