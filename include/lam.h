@@ -158,7 +158,9 @@ typedef struct {
 /*  LAM_HOP_TREE         two-level broadcast over the same TMA hop kernel: relay k owns the chunks j with
  *                       j mod R == k-1 (R relays) and pulls them from node 0; every other chunk it pulls
  *                       from the relay that owns it, in an order staggered by k so the R-1 pullers of a
- *                       moment read from different owners.  Every relay receives M and forwards
+ *                       moment read from different owners; a peer's 1 MiB tile is read as soon as it
+ *                       landed there (per-tile flags) and every chunk is verified against node 0's
+ *                       header and verdict.  Every relay receives M and forwards
  *                       (R-1)/R of it, pipeline depth 2 (the chain: forwards M, depth R).  Control plane:
  *                       every relay's predecessor is node 0; the first relay to start v opens v at every
  *                       idle relay (gang start) and each fill pins the slot of v at the relays it reads

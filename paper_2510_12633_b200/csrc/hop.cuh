@@ -147,7 +147,21 @@ __global__ void __launch_bounds__(kHopThreads, 1)
     for (uint32_t m = 0; m < my_tiles && status == kHopOk; ++m) {
       const HopTile T = tiles[blockIdx.x + m * gridDim.x];
       const uint8_t* src = links[T.rank].src + T.region_off;
-      if (T.chunk != waited) {
+      const uint64_t* tf = links[T.rank].tile_flags;
+      if (tf) {                                    // two-level broadcast, peer source: this tile only
+        if (prof) { t_b = clock64(); pc[1] += t_b - t_a; t_a = t_b; }
+        for (uint32_t spin = 0;; ++spin) {
+          const uint64_t f = ld_acquire_sys(tf + T.tile);
+          if (f == version) break;
+          if (*(volatile int32_t*)meta.abort_flag) { status = kHopAbort; break; }
+          if ((spin & 63) == 63 && globaltimer() > deadline) { status = kHopTimeout; break; }
+          __nanosleep(spin < 64 ? 64 : 512);
+        }
+        if (prof) { t_b = clock64(); pc[2] += t_b - t_a; t_a = t_b; }
+        if (status != kHopOk) { fail_chunk = T.chunk; break; }
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        waited = 0xFFFFFFFFu;                      // a later node-0 tile re-checks its chunk flag
+      } else if (T.chunk != waited) {
         const uint64_t* flag = links[T.rank].src_flags + T.chunk;
         if (prof) { t_b = clock64(); pc[1] += t_b - t_a; t_a = t_b; }
         for (uint32_t spin = 0;; ++spin) {
@@ -258,6 +272,11 @@ __global__ void __launch_bounds__(kHopThreads, 1)
       HOP_LAP(1)
     }
     if (failed) break;
+    if (meta.tile_flags) {                         // two-level broadcast: the tile is in our HBM — release it
+      __threadfence_system();                      // to the peers that pull it (before our chunk verdict)
+      asm volatile("bar.sync 1, %0;" ::"r"(kHopConsumers) : "memory");
+      if (threadIdx.x == 0) st_release_sys(meta.tile_flags + T.tile, version);
+    }
     const bool chunk_end = m + 1 >= my_tiles || tiles[blockIdx.x + (m + 1) * gridDim.x].chunk != T.chunk;
     if (chunk_end) {                               // this CTA's last tile of the chunk: hand its share over
       __threadfence_system();                      // this thread's stores before the header / flag

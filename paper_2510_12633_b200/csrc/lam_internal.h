@@ -81,6 +81,7 @@ struct __attribute__((aligned(16))) HopTile {    // one tile of a chunk moved pr
   uint32_t rank;       // actor rank whose region holds the chunk
   uint32_t bytes;      // multiple of 16
   uint32_t word0;      // u32 word index inside the chunk
+  uint32_t tile;       // index in the part's tile list (tile flags of the two-level broadcast)
 };
 
 struct __attribute__((aligned(16))) RankLink {   // per actor rank, for the hop kernel
@@ -90,7 +91,7 @@ struct __attribute__((aligned(16))) RankLink {   // per actor rank, for the hop 
   const lam_chunk_header* src_hdr;   // pred's headers (the checksum the chunk must reproduce)
   uint8_t* dst;               // this node part: rank region base in the filling slot
   const uint64_t* pred_flags; // pred's flags: a chunk is committed only if the pred committed it
-  const uint64_t* _pad;
+  const uint64_t* tile_flags; // two-level broadcast, peer source: wait per tile on these, not per chunk
 };
 
 struct __attribute__((aligned(16))) CopyTile {   // one 2-D block of a pull (reshard)
@@ -132,6 +133,7 @@ struct ChunkMeta {          // device view of one slot's metadata in a node part
   int32_t* abort_flag;      // [1]
   uint64_t* mirror;         // [total_chunks] host-visible copy of flags (shared memory) or null
   uint64_t* mc_flags;       // LAM_HOP_MULTICAST pack: multicast VA of the slot's flag array, else null
+  uint64_t* tile_flags;     // LAM_HOP_TREE hop: per-tile flags released as each tile lands, else null
 };
 constexpr uint32_t kMirrorChunks = 2048;  // chunks per slot mirrored to the host (streaming pulls)
 

@@ -149,6 +149,7 @@ void build_hop_tiles(const ImagePlan& p, const std::vector<int>& ranks, std::vec
   std::stable_sort(tiles->begin(), tiles->end(), [&](const HopTile& a, const HopTile& b) {
     return chunk_order(p, a.chunk, 0) < chunk_order(p, b.chunk, 0);
   });
+  for (size_t i = 0; i < tiles->size(); ++i) (*tiles)[i].tile = (uint32_t)i;
 }
 
 static uint32_t widest_align(uint64_t a, uint64_t b, uint64_t c, uint64_t d, uint64_t e) {

@@ -40,7 +40,7 @@ using ctl::find_slot;
 using ctl::newest_held;
 
 struct SlotMeta {   // byte offsets inside a slot's metadata block
-  uint64_t flags, hdr, cnt, abort, bytes;
+  uint64_t flags, hdr, cnt, abort, tflags, bytes;   // tflags: LAM_HOP_TREE per-tile flags
 };
 
 struct Part {
@@ -259,6 +259,7 @@ ChunkMeta meta_of(const lam_ctx* c, const Part& p, int slot) {
   cm.abort_flag = reinterpret_cast<int32_t*>(m + c->sm.abort);
   cm.mirror = c->mirror_dev ? c->mirror_dev + ((uint64_t)p.node * LAM_MAX_SLOTS + slot) * kShmMirrorChunks : nullptr;
   cm.mc_flags = nullptr;
+  cm.tile_flags = c->tree && p.node > 0 ? reinterpret_cast<uint64_t*>(m + c->sm.tflags) : nullptr;
   return cm;
 }
 
@@ -402,7 +403,17 @@ lam_status alloc_parts(lam_ctx* c) {
   c->sm.hdr = align_up(c->sm.flags + 8 * total, 64);
   c->sm.cnt = align_up(c->sm.hdr + sizeof(lam_chunk_header) * total, 64);
   c->sm.abort = align_up(c->sm.cnt + 4 * total, 64);
-  c->sm.bytes = align_up(c->sm.abort + 64, 4096);
+  c->sm.tflags = align_up(c->sm.abort + 64, 64);
+  uint64_t ntiles = 0;
+  if (c->cfg.hop_mode == LAM_HOP_TREE) {   // a whole node's tile list (every relay of the tree is whole)
+    std::vector<int> all(N);
+    for (int r = 0; r < N; ++r) all[r] = r;
+    std::vector<HopTile> tl;
+    std::vector<uint32_t> tpc;
+    build_hop_tiles(c->plan, all, &tl, &tpc);
+    ntiles = tl.size();
+  }
+  c->sm.bytes = align_up(c->sm.tflags + 8 * ntiles, 4096);
   c->node_parts.assign(c->n_nodes, {});
   c->node_rank_part.assign(c->n_nodes, std::vector<int>(N, -1));
   for (int node = 0; node < c->n_nodes; ++node) {
@@ -912,12 +923,16 @@ lam_status launch_hop_part(lam_ctx* c, Part& p, int s, bool* launched) {
         const int qs = src == 0 ? ps : sl.peer_slot[src];
         for (int r : p.ranks) {
           const Part& q = c->parts[c->node_rank_part[src][r]];
-          ChunkMeta qm = meta_of(c, q, qs);
+          const Part& q0 = c->parts[c->node_rank_part[0][r]];
+          ChunkMeta qm = meta_of(c, q, qs), q0m = meta_of(c, q0, ps);
           RankLink& L = tl[(size_t)src * N + r];
           L.src = slot_data(q, qs) + q.rank_off[r];
           L.src_flags = qm.flags;
-          L.src_hdr = qm.hdr;
-          L.pred_flags = qm.flags;
+          // a peer's tile is read as soon as it landed there (its tile flag), before the peer verified
+          // the chunk: the chunk is checked against node 0's header and verdict, which every copy shares
+          L.tile_flags = src > 0 ? qm.tile_flags : nullptr;
+          L.src_hdr = q0m.hdr;
+          L.pred_flags = q0m.flags;
           L.dst = slot_data(p, s) + p.rank_off[r];
         }
       }

@@ -486,8 +486,19 @@ recipe_r2tree2() {
   timeout 240 python bench.py --gpus 4 --steps 10 --warmup 3 --no-e2e --no-cpu-baseline --hop-mode tree > gpurun_out/r2tree2/n4_tree.log 2>&1; echo rc=$? >> gpurun_out/r2tree2/n4_tree.log
 }
 
+recipe_r2tree3() {
+  # two-level broadcast with per-tile flags (a peer's tile is pulled as soon as it landed): parity + bench N=4
+  mkdir -p gpurun_out/r2tree3
+  python -c "import __graft_entry__ as g; g.build()" > gpurun_out/r2tree3/build.log 2>&1
+  export LAM_DEBUG_FAIL=1
+  timeout 150 python -m pytest tests/test_gpu_parity.py -q -x -rs -k "tree" > gpurun_out/r2tree3/pytest_sp.log 2>&1; echo rc=$? >> gpurun_out/r2tree3/pytest_sp.log
+  timeout 150 python bench.py --gpus 4 --steps 10 --warmup 3 --no-e2e --no-cpu-baseline --hop-mode tree > gpurun_out/r2tree3/n4_tree.log 2>&1; echo rc=$? >> gpurun_out/r2tree3/n4_tree.log
+  M=tests/test_gpu_multiproc.py::test_multiproc_parity
+  timeout 200 python -m pytest -q -x -rs "$M[21]" "$M[22]" > gpurun_out/r2tree3/pytest_mp.log 2>&1; echo rc=$? >> gpurun_out/r2tree3/pytest_mp.log
+}
+
 if [ $# -ne 1 ] || ! declare -F "recipe_$1" > /dev/null; then
-  echo "usage: bash tools/gpu_recipes.sh <recipe>; recipes: sweep4 n4 v9 v10 v15 host4 v5 v12 dyn v13 final r2c v14 r2b ncu2 v7 r2d r2a v11 v6 v8 r2e r2f r2g r2h r2j r2l r2m r2n r2o r2p r2q r2r r2s r2t r2u r2v r2w r2x r2y r2z r2final r2driver r2tree2"
+  echo "usage: bash tools/gpu_recipes.sh <recipe>; recipes: sweep4 n4 v9 v10 v15 host4 v5 v12 dyn v13 final r2c v14 r2b ncu2 v7 r2d r2a v11 v6 v8 r2e r2f r2g r2h r2j r2l r2m r2n r2o r2p r2q r2r r2s r2t r2u r2v r2w r2x r2y r2z r2final r2driver r2tree2 r2tree3"
   exit 2
 fi
 "recipe_$1"
