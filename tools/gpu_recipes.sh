@@ -497,8 +497,17 @@ recipe_r2tree3() {
   timeout 200 python -m pytest -q -x -rs "$M[21]" "$M[22]" > gpurun_out/r2tree3/pytest_mp.log 2>&1; echo rc=$? >> gpurun_out/r2tree3/pytest_mp.log
 }
 
+recipe_r2last() {
+  # the chain after the last k_hop change (tile-flag branch): smoke, chain parity across 2 GPUs, bench N=2
+  mkdir -p gpurun_out/r2last
+  python -c "import __graft_entry__ as g; g.build()" > gpurun_out/r2last/build.log 2>&1
+  timeout 200 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r2last/smoke.log 2>&1; echo rc=$? >> gpurun_out/r2last/smoke.log
+  timeout 200 python -m pytest tests/test_gpu_parity.py -q -x -rs -k "chain or corrupt or multicast" > gpurun_out/r2last/pytest.log 2>&1; echo rc=$? >> gpurun_out/r2last/pytest.log
+  timeout 200 python bench.py --gpus 2 --steps 10 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/r2last/n2.log 2>&1; echo rc=$? >> gpurun_out/r2last/n2.log
+}
+
 if [ $# -ne 1 ] || ! declare -F "recipe_$1" > /dev/null; then
-  echo "usage: bash tools/gpu_recipes.sh <recipe>; recipes: sweep4 n4 v9 v10 v15 host4 v5 v12 dyn v13 final r2c v14 r2b ncu2 v7 r2d r2a v11 v6 v8 r2e r2f r2g r2h r2j r2l r2m r2n r2o r2p r2q r2r r2s r2t r2u r2v r2w r2x r2y r2z r2final r2driver r2tree2 r2tree3"
+  echo "usage: bash tools/gpu_recipes.sh <recipe>; recipes: sweep4 n4 v9 v10 v15 host4 v5 v12 dyn v13 final r2c v14 r2b ncu2 v7 r2d r2a v11 v6 v8 r2e r2f r2g r2h r2j r2l r2m r2n r2o r2p r2q r2r r2s r2t r2u r2v r2w r2x r2y r2z r2final r2driver r2tree2 r2tree3 r2last"
   exit 2
 fi
 "recipe_$1"
