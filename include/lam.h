@@ -155,8 +155,9 @@ typedef struct {
  *                       each relay GPU S extra image-sized replicas.  LAM_EINVAL otherwise.  A chunk that
  *                       fails verification from the replica is re-verified (twice) before the version
  *                       is given up: switch-stored bytes may land after the chunk's flag. */
-/*  LAM_HOP_TREE         two-level broadcast over the same TMA hop kernel: relay k owns the chunks j with
- *                       j mod R == k-1 (R relays) and pulls them from node 0; every other chunk it pulls
+/*  LAM_HOP_TREE         two-level broadcast over the same TMA hop kernel: relay k owns the j-th chunk of
+ *                       the hop order with j mod R == k-1 (R relays; the hop order interleaves the FSDP
+ *                       ranks' regions, see lam_plan_tree_tiles) and pulls it from node 0; every other chunk it pulls
  *                       from the relay that owns it, in an order staggered by k so the R-1 pullers of a
  *                       moment read from different owners; a peer's 1 MiB tile is read as soon as it
  *                       landed there (per-tile flags) and every chunk is verified against node 0's
@@ -374,6 +375,14 @@ typedef struct {
 } lam_copy_tile_info;
 int64_t lam_plan_copy_tiles(const lam_model_dims*, int32_t actor_layout, int32_t fsdp_size, uint64_t chunk_bytes,
                             const lam_tp_layout*, lam_copy_tile_info* out, int64_t cap);
+/* LAM_HOP_TREE: the hop tiles relay `node` (1..n_relays) walks, in order, and the node each one is read
+ * from (`source`: 0 = node 0, else the relay that owns the chunk, when it is in `peer_mask`). */
+typedef struct {
+  uint64_t region_off;
+  uint32_t chunk, rank, bytes, source;
+} lam_hop_tile_info;
+int64_t lam_plan_tree_tiles(const lam_model_dims*, int32_t actor_layout, int32_t fsdp_size, uint64_t chunk_bytes,
+                            int32_t n_relays, int32_t node, uint64_t peer_mask, lam_hop_tile_info* out, int64_t cap);
 
 /* ---- control plane (host-only; no GPU) ------------------------------------------------- */
 /* The version-table state machine the runtime runs under its cross-process lock, exposed so the

@@ -113,6 +113,10 @@ bool build_pack_units(const ImagePlan& p, const std::vector<Tensor>& ts, int ran
                       std::string* err);
 void build_hop_tiles(const ImagePlan& p, const std::vector<int>& ranks, std::vector<HopTile>* tiles,
                      std::vector<uint32_t>* tiles_per_chunk);
+// LAM_HOP_TREE: relay `node`'s walk of `tiles` (hop order) — chunk runs in groups of R, the j-th run of
+// a group owned by relay j + 1, rotated so the node's own run comes first; each tile's links index =
+// source * N + rank, source = the run's owner when it is another relay in `peer_mask`, else node 0.
+std::vector<HopTile> tree_hop_tiles(const std::vector<HopTile>& tiles, int R, int node, uint64_t peer_mask, int N);
 // dst_base[k] = device address of destination k; src rank alignment assumed >= 256 B.
 bool build_copy_tiles(const ImagePlan& p, const std::vector<Tensor>& ts, const lam_tp_layout& L,
                       std::vector<CopyTile>* tiles, uint64_t* bytes, std::string* err);

@@ -152,6 +152,30 @@ void build_hop_tiles(const ImagePlan& p, const std::vector<int>& ranks, std::vec
   for (size_t i = 0; i < tiles->size(); ++i) (*tiles)[i].tile = (uint32_t)i;
 }
 
+std::vector<HopTile> tree_hop_tiles(const std::vector<HopTile>& tiles, int R, int node, uint64_t peer_mask, int N) {
+  std::vector<std::pair<uint32_t, uint32_t>> runs;   // chunk runs [begin, end) of the tile list
+  for (uint32_t i = 0; i < tiles.size(); ++i)
+    if (runs.empty() || tiles[runs.back().first].chunk != tiles[i].chunk) runs.push_back({i, i + 1});
+    else runs.back().second = i + 1;
+  std::vector<HopTile> out;
+  out.reserve(tiles.size());
+  for (size_t g0 = 0; g0 < runs.size(); g0 += (size_t)R) {
+    const size_t gn = std::min<size_t>((size_t)R, runs.size() - g0);
+    for (size_t k = 0; k < gn; ++k) {
+      const size_t j = (k + (size_t)(node - 1)) % gn;   // owner of the group's j-th chunk run: relay j + 1
+      const auto& run = runs[g0 + j];
+      const int owner = (int)j + 1;
+      for (uint32_t i = run.first; i < run.second; ++i) {
+        HopTile t = tiles[i];
+        const int src = owner != node && (peer_mask >> owner & 1ull) ? owner : 0;
+        t.rank += (uint32_t)(src * N);
+        out.push_back(t);
+      }
+    }
+  }
+  return out;
+}
+
 static uint32_t widest_align(uint64_t a, uint64_t b, uint64_t c, uint64_t d, uint64_t e) {
   uint64_t x = a | b | c | d | e;
   if (x % 16 == 0) return 16;
@@ -452,6 +476,26 @@ extern "C" int64_t lam_plan_segments(const lam_model_dims* d, int32_t layout, in
     }
   }
   return (int64_t)p.segs.size();
+}
+
+extern "C" int64_t lam_plan_tree_tiles(const lam_model_dims* d, int32_t layout, int32_t N, uint64_t C,
+                                       int32_t n_relays, int32_t node, uint64_t peer_mask, lam_hop_tile_info* out,
+                                       int64_t cap) {
+  if (!d || !model_valid(*d) || n_relays < 1 || node < 1 || node > n_relays) return LAM_EINVAL;
+  std::vector<Tensor> ts = model_tensors(*d);
+  ImagePlan p;
+  if (!build_image_plan(ts, N, layout, C, &p)) return LAM_EINVAL;
+  std::vector<int> all(N);
+  for (int r = 0; r < N; ++r) all[r] = r;
+  std::vector<HopTile> tiles;
+  std::vector<uint32_t> tpc;
+  build_hop_tiles(p, all, &tiles, &tpc);
+  tiles = tree_hop_tiles(tiles, n_relays, node, peer_mask, N);
+  if (out)
+    for (size_t i = 0; i < tiles.size() && (int64_t)i < cap; ++i)
+      out[i] = lam_hop_tile_info{tiles[i].region_off, tiles[i].chunk, tiles[i].rank % (uint32_t)N, tiles[i].bytes,
+                                 tiles[i].rank / (uint32_t)N};
+  return (int64_t)tiles.size();
 }
 
 extern "C" int64_t lam_plan_copy_tiles(const lam_model_dims* d, int32_t layout, int32_t N, uint64_t C,

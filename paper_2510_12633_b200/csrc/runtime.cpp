@@ -914,8 +914,7 @@ lam_status launch_hop_part(lam_ctx* c, Part& p, int s, bool* launched) {
       links = p.d_links_dyn;
     } else if (c->tree && !resume) {
       // two-level broadcast: sources = node 0 (links [0, N)) and every relay this fill pinned (links
-      // [o N, (o+1) N)); chunk g comes from its owner (g mod R) + 1 when pinned, else from node 0;
-      // chunks are walked in groups of R, rotated by this node, so concurrent pullers hit different owners
+      // [o N, (o+1) N)); the tile order and each chunk's source come from tree_hop_tiles (plan.cpp)
       const int R = c->n_nodes - 1;
       std::vector<RankLink> tl((size_t)c->n_nodes * N);
       for (int src = 0; src < c->n_nodes; ++src) {
@@ -936,26 +935,7 @@ lam_status launch_hop_part(lam_ctx* c, Part& p, int s, bool* launched) {
           L.dst = slot_data(p, s) + p.rank_off[r];
         }
       }
-      // chunk runs of the tile list, in chunk order
-      std::vector<std::pair<uint32_t, uint32_t>> runs;   // [begin, end) into h_tiles
-      for (uint32_t i = 0; i < p.h_tiles.size(); ++i)
-        if (runs.empty() || p.h_tiles[runs.back().first].chunk != p.h_tiles[i].chunk) runs.push_back({i, i + 1});
-        else runs.back().second = i + 1;
-      std::vector<HopTile> tt;
-      tt.reserve(p.h_tiles.size());
-      for (size_t g0 = 0; g0 < runs.size(); g0 += R) {
-        const size_t gn = std::min<size_t>(R, runs.size() - g0);
-        for (size_t k = 0; k < gn; ++k) {
-          const auto& run = runs[g0 + (k + (size_t)(p.node - 1)) % gn];
-          for (uint32_t i = run.first; i < run.second; ++i) {
-            HopTile t = p.h_tiles[i];
-            const int owner = (int)(t.chunk % (uint32_t)R) + 1;
-            const int src = owner != p.node && (sl.peer_mask >> owner & 1ull) ? owner : 0;
-            t.rank += (uint32_t)(src * N);
-            tt.push_back(t);
-          }
-        }
-      }
+      const std::vector<HopTile> tt = tree_hop_tiles(p.h_tiles, R, p.node, sl.peer_mask, N);
       CK(cudaStreamSynchronize(p.stream));   // the previous launch (another version) used these tables
       CK(cudaMemcpy(p.d_links_tree, tl.data(), sizeof(RankLink) * tl.size(), cudaMemcpyHostToDevice));
       CK(cudaMemcpy(p.d_tiles_tree, tt.data(), sizeof(HopTile) * tt.size(), cudaMemcpyHostToDevice));

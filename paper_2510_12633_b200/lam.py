@@ -89,6 +89,11 @@ class lam_copy_tile_info(C.Structure):
                 ("rows", C.c_uint32), ("row_bytes", C.c_uint32), ("src_rank", C.c_uint32), ("align", C.c_uint32)]
 
 
+class lam_hop_tile_info(C.Structure):
+    _fields_ = [("region_off", C.c_uint64), ("chunk", C.c_uint32), ("rank", C.c_uint32), ("bytes", C.c_uint32),
+                ("source", C.c_uint32)]
+
+
 class lam_stats(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in ("publishes", "publish_busy", "hops_launched", "versions_skipped",
                                           "pulls", "checksum_errors", "timeouts", "plan_cache_hits",
@@ -136,6 +141,8 @@ def load() -> C.CDLL:
                                         C.c_int32, C.c_char_p, C.c_int32, P(C.c_int64), P(C.c_int64)]),
         "lam_plan_segments": (C.c_int64, [P(lam_model_dims), C.c_int32, C.c_int32, C.c_uint64,
                                           P(lam_segment_info), C.c_int64]),
+        "lam_plan_tree_tiles": (C.c_int64, [P(lam_model_dims), C.c_int32, C.c_int32, C.c_uint64, C.c_int32, C.c_int32,
+                                            C.c_uint64, P(lam_hop_tile_info), C.c_int64]),
         "lam_plan_copy_tiles": (C.c_int64, [P(lam_model_dims), C.c_int32, C.c_int32, C.c_uint64, P(lam_tp_layout),
                                             P(lam_copy_tile_info), C.c_int64]),
         "lam_optimal_chunks": (C.c_int64, [C.c_int32, C.c_double, C.c_double, C.c_double, C.c_int64]),
@@ -155,7 +162,7 @@ def load() -> C.CDLL:
 EXPORTED = ["lam_config_size", "lam_init", "lam_export_ipc", "lam_import_ipc", "lam_connect", "lam_destroy", "lam_strerror",
             "lam_publish", "lam_relay_step", "lam_pull", "lam_latest", "lam_get_plan_info", "lam_get_stats",
             "lam_read_image", "lam_read_headers", "lam_debug_region", "lam_debug_replica", "lam_set_profiling", "lam_kernel_times", "lam_pull_bytes", "lam_model_n_tensors", "lam_model_tensor", "lam_vllm_layout",
-            "lam_plan_segments", "lam_plan_copy_tiles", "lam_optimal_chunks", "lam_chain_latency"]
+            "lam_plan_segments", "lam_plan_copy_tiles", "lam_plan_tree_tiles", "lam_optimal_chunks", "lam_chain_latency"]
 
 
 class LamError(RuntimeError):
@@ -451,6 +458,17 @@ def plan_copy_tiles(d: lam_model_dims, layout: int, N: int, C_bytes: int, tp: TP
     arr = (lam_copy_tile_info * max(1, n))()
     L.lam_plan_copy_tiles(C.byref(d), layout, N, C_bytes, C.byref(tp.c), arr, n)
     return list(arr[:n])
+
+
+def plan_tree_tiles(d: lam_model_dims, layout: int, N: int, C_bytes: int, n_relays: int, node: int,
+                    peer_mask: int) -> list[tuple[int, int, int, int, int]]:
+    """LAM_HOP_TREE: (region_off, chunk, rank, bytes, source node) of the tiles relay `node` walks, in order."""
+    L = load()
+    n = L.lam_plan_tree_tiles(C.byref(d), layout, N, C_bytes, n_relays, node, peer_mask, None, 0)
+    _check(0 if n >= 0 else int(n), "lam_plan_tree_tiles")
+    arr = (lam_hop_tile_info * max(1, n))()
+    L.lam_plan_tree_tiles(C.byref(d), layout, N, C_bytes, n_relays, node, peer_mask, arr, n)
+    return [(a.region_off, a.chunk, a.rank, a.bytes, a.source) for a in arr[:n]]
 
 
 def optimal_chunks(p: int, M: float, t_byte: float, t_start: float, k_cap: int = 1024) -> int:

@@ -207,3 +207,39 @@ def test_full_size_8gpu_placements_fit_hbm(config, model, tp):
     for _, dev, tpr, _ in T["rollouts"]:
         per_gpu[dev] += 2 * P / tpr
     assert max(per_gpu.values()) < 180e9, per_gpu
+
+
+@pytest.mark.parametrize("name,layout,N,C,R", [("tiny", FSDP2_DIM0, 1, 1 << 16, 3), ("tiny", FSDP1_FLAT, 2, 1 << 15, 4),
+                                               ("odd", FSDP2_DIM0, 3, 1 << 16, 2)])
+def test_tree_tile_order(name, layout, N, C, R):
+    """LAM_HOP_TREE: every relay walks the same tiles, a chunk's tiles stay together, each
+    group of R chunk runs (in the hop order, which interleaves the FSDP ranks' regions; relay 1 walks it
+    unrotated) starts at the run the relay owns (the j-th run of a group belongs to relay j + 1), and a
+    tile is read from its owner relay when that relay is pinned in the mask, else from node 0."""
+    d, lay = MODELS[name], LAYOUT[layout]
+
+    def runs_of(tiles):
+        ch = [t[1] for t in tiles]
+        return [c for i, c in enumerate(ch) if i == 0 or ch[i - 1] != c]
+
+    base = lam.plan_tree_tiles(d, lay, N, C, R, 1, 0)
+    base_runs = runs_of(base)
+    assert len(base_runs) == len(set(base_runs)) > R    # contiguous per chunk, several groups
+    assert sorted(base_runs) == list(range(len(base_runs)))
+    owner = {c: i % R + 1 for i, c in enumerate(base_runs)}
+    ref = sorted(t[:4] for t in base)
+    assert len(set(ref)) == len(ref)
+    for mask in (0, sum(1 << n for n in range(1, R + 1)), 1 << R):
+        for node in range(1, R + 1):
+            tiles = lam.plan_tree_tiles(d, lay, N, C, R, node, mask)
+            assert sorted(t[:4] for t in tiles) == ref
+            runs = runs_of(tiles)
+            assert len(runs) == len(base_runs)
+            for g in range(0, len(runs), R):
+                grp, mine = base_runs[g:g + R], runs[g:g + R]
+                assert mine == grp[(node - 1) % len(grp):] + grp[:(node - 1) % len(grp)]
+            for _, c, rank, _, src in tiles:
+                assert rank < N
+                assert src == (owner[c] if owner[c] != node and mask >> owner[c] & 1 else 0)
+    with pytest.raises(lam.LamError):
+        lam.plan_tree_tiles(d, lay, N, C, R, R + 1, 0)
