@@ -170,12 +170,12 @@ def test_fail_abandons_version_the_new_predecessor_lacks():
 
 
 # ------------------------------------------------------------------------------ two processes
-def _worker(rank, world, port, name, versions, q):
+def _worker(rank, world, port, name, versions, q, hop_mode=lam.LAM_HOP_KERNEL):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     errors = []
     try:
-        c = lam.Ctl(name, rank == 0, n_nodes=3, slots=2)
+        c = lam.Ctl(name, rank == 0, n_nodes=3, slots=2, hop_mode=hop_mode)
         dist.barrier()
         rng = random.Random(rank)
         if rank == 0:                                        # the actor: publish as fast as it can
@@ -213,6 +213,9 @@ def _worker(rank, world, port, name, versions, q):
             final = [c.latest(n) for n in range(3)]
             if final != [versions] * 3:
                 errors.append(f"not quiescent at the newest version: {final}")
+            pins = [c.slot(n, k)[2] for n in range(3) for k in range(2)]
+            if any(pins):                                    # every pin (readers, fills, peers) released
+                errors.append(f"readers left at quiescence: {pins}")
         dist.barrier()
         c.close()
     except Exception as e:  # pragma: no cover - reported to the parent
@@ -221,12 +224,15 @@ def _worker(rank, world, port, name, versions, q):
     dist.destroy_process_group()
 
 
-def test_two_processes_share_the_version_table():
+@pytest.mark.parametrize("hop_mode", [lam.LAM_HOP_KERNEL, lam.LAM_HOP_MULTICAST, lam.LAM_HOP_TREE])
+def test_two_processes_share_the_version_table(hop_mode):
+    """Chain, star (multicast) and two-level (gang start + peer pins) control planes, across processes."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    name = f"lam_ctl_test_{os.getpid()}"
+    name = f"lam_ctl_test_{os.getpid()}_{hop_mode}"
     versions = 60
-    procs = [ctx.Process(target=_worker, args=(r, 2, 29500 + os.getpid() % 1000, name, versions, q)) for r in range(2)]
+    port = 29500 + (os.getpid() * 3 + hop_mode) % 1000
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, name, versions, q, hop_mode)) for r in range(2)]
     for pr in procs:
         pr.start()
     results = [q.get(timeout=120) for _ in range(3)]
@@ -389,4 +395,66 @@ def test_tree_late_relay_pins_only_holders():
     assert c.slot(2, s2)[2] == 0                  # relay 1's fill did not pin relay 2
     assert c.part_done(1, k13, 3) and c.part_done(2, s2, 3)
     assert c.slot(1, k13)[2] == 0 and c.latest(1) == c.latest(2) == 3
+    c.close()
+
+
+@pytest.mark.parametrize("hop_mode,seed", [(m, s) for m in (lam.LAM_HOP_KERNEL, lam.LAM_HOP_MULTICAST, lam.LAM_HOP_TREE)
+                                           for s in range(4)])
+def test_random_interleavings_keep_the_slot_invariants(hop_mode, seed):
+    """Seeded random publish / pack / fill / corrupt-fill / rollout pin-unpin interleavings in every
+    topology (chain, star, two-level): latest never goes back, a pinned slot is COMPLETE at the
+    pinned version, reader counts stay >= 0, and once progress runs without faults
+    every relay serves the newest version and every pin (rollout, fill, peer) has been released."""
+    rng = random.Random(seed)
+    n = 4
+    c = lam.Ctl("", True, n_nodes=n, slots=2, hop_mode=hop_mode)
+    seen = [0] * n
+    pins = []
+    v = 0
+
+    def check():
+        for node in range(n):
+            lt = c.latest(node)
+            assert lt >= seen[node], (node, seen[node], lt)
+            seen[node] = lt
+            for k in range(2):
+                assert c.slot(node, k)[2] >= 0
+
+    def step(node, p_done, p_bad):
+        s, u, _ = c.start(node)
+        if s >= 0 and rng.random() < p_done:
+            c.part_done(node, s, u, 1, lam.LAM_ECHECKSUM if rng.random() < p_bad else lam.LAM_OK)
+        return s
+
+    for _ in range(600):
+        r = rng.random()
+        if r < 0.15:
+            st, s = c.publish(v + 1)
+            if st == lam.LAM_OK:
+                v += 1
+                if rng.random() < 0.8:
+                    c.pack_done(s, v)
+                else:
+                    pending = (s, v)
+                    step(rng.randrange(1, n), 0.5, 0.0)   # relays may start v before the pack ends
+                    c.pack_done(*pending)
+        elif r < 0.75:
+            step(rng.randrange(1, n), 0.6, 0.05)
+        elif r < 0.9:
+            node = rng.randrange(1, n)
+            got, slot = c.pin(node)
+            if got:
+                assert c.slot(node, slot)[:2] == (got, COMPLETE)
+                pins.append((node, slot))
+        elif pins:
+            c.unpin(*pins.pop(rng.randrange(len(pins))))
+        check()
+    while pins:
+        c.unpin(*pins.pop())
+    for _ in range(100):                                   # fault-free progress to quiescence
+        if all(step(node, 1.0, 0.0) < 0 for node in range(1, n)):
+            break
+        check()
+    assert [c.latest(node) for node in range(n)] == [v] * n
+    assert [c.slot(node, k)[2] for node in range(n) for k in range(2)] == [0] * (2 * n)
     c.close()
