@@ -118,7 +118,9 @@ typedef struct {
   int32_t n_relays;                        /* relay nodes 1..n_relays, chain order 0->1->... */
   lam_node_desc relay[LAM_MAX_NODES];      /* relay[i-1] describes node i */
   int32_t slots;                           /* ring slots per node, 2..LAM_MAX_SLOTS */
-  uint64_t chunk_bytes;                    /* C, multiple of 4096; 0 => Appendix D k* (below) */
+  uint64_t chunk_bytes;                    /* C, multiple of 4096; 0 => Appendix D k* (below) with p =
+                                              n_relays + 2 (chain + pack), 3 (multicast) or 4 (tree),
+                                              capped at 128 MiB */
   double t_start_s, t_byte_s;              /* Appendix D parameters used when chunk_bytes == 0 */
   int32_t n_rollouts;
   lam_rollout_desc rollout[LAM_MAX_ROLLOUTS];

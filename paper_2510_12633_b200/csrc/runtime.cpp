@@ -1292,8 +1292,11 @@ extern "C" lam_status lam_init(const lam_config* cfg, lam_ctx** out) {
     // --chunk-mb sweep at N=4: 64 MB 38.0 ms, 138 MB 34.2 ms, 256 MB 33.1 ms) implied ~20 us; with the
     // flusher warp (v5) 128 MB beats 256 MB at N=4 (25.5 vs 25.9 ms): ~10 us
     double tsu = cfg->t_start_s > 0 ? cfg->t_start_s : 10e-6;
-    // the pack is one more pipeline stage ahead of the chain (reading R12)
-    int64_t k = lam_optimal_chunks(c->n_nodes + 1, 2.0 * (double)c->params, tb, tsu, 1024);
+    // the pack is one more pipeline stage ahead of the chain (reading R12); the star
+    // (multicast pack, then each relay's verify) and the two-level tree (node 0 -> owner -> peer) have
+    // fixed depths of 3 and 4 nodes whatever the relay count
+    const int depth = cfg->hop_mode == LAM_HOP_MULTICAST ? 3 : cfg->hop_mode == LAM_HOP_TREE ? 4 : c->n_nodes + 1;
+    int64_t k = lam_optimal_chunks(depth, 2.0 * (double)c->params, tb, tsu, 1024);
     C = align_up(cdiv(2 * c->params, (uint64_t)k), kChunkAlign);
     // practical cap: the chunk is also the checksum / completion-signal unit
     C = std::min<uint64_t>(C, 128ull << 20);
