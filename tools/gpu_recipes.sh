@@ -506,8 +506,15 @@ recipe_r2last() {
   timeout 200 python bench.py --gpus 2 --steps 10 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/r2last/n2.log 2>&1; echo rc=$? >> gpurun_out/r2last/n2.log
 }
 
+recipe_r2fin() {
+  # the driver's 1-GPU round-end sequence at HEAD (smoke, pytest -m gpu)
+  mkdir -p gpurun_out
+  timeout 120 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/r2fin_smoke.txt 2>&1
+  timeout 220 python -m pytest tests -m gpu -x -q > gpurun_out/r2fin_pytest_gpu.txt 2>&1
+}
+
 if [ $# -ne 1 ] || ! declare -F "recipe_$1" > /dev/null; then
-  echo "usage: bash tools/gpu_recipes.sh <recipe>; recipes: sweep4 n4 v9 v10 v15 host4 v5 v12 dyn v13 final r2c v14 r2b ncu2 v7 r2d r2a v11 v6 v8 r2e r2f r2g r2h r2j r2l r2m r2n r2o r2p r2q r2r r2s r2t r2u r2v r2w r2x r2y r2z r2final r2driver r2tree2 r2tree3 r2last"
+  echo "usage: bash tools/gpu_recipes.sh <recipe>; recipes: sweep4 n4 v9 v10 v15 host4 v5 v12 dyn v13 final r2c v14 r2b ncu2 v7 r2d r2a v11 v6 v8 r2e r2f r2g r2h r2j r2l r2m r2n r2o r2p r2q r2r r2s r2t r2u r2v r2w r2x r2y r2z r2final r2driver r2tree2 r2tree3 r2last r2fin"
   exit 2
 fi
 "recipe_$1"
