@@ -229,6 +229,20 @@ def test_tree_tile_order(name, layout, N, C, R):
     owner = {c: i % R + 1 for i, c in enumerate(base_runs)}
     ref = sorted(t[:4] for t in base)
     assert len(set(ref)) == len(ref)
+    # the tiles cover every chunk of the oracle's image exactly: rank r's chunk j is the
+    # bytes [j C, j C + len) of r's region, cut into consecutive tiles
+    op = image_plan([s for _, s in otensors(OMODELS[name])], N, C, layout)
+    cover = {}
+    for off, g, rank, nb, _ in base:
+        cover.setdefault(g, []).append((off, nb, rank))
+    assert sorted(cover) == list(range(op.total_chunks))
+    for g, ts in cover.items():
+        r = op.chunk_rank(g)
+        pos = (g - op.chunk_base[r]) * C
+        for off, nb, rank in sorted(ts):
+            assert (off, rank) == (pos, r) and 0 < nb
+            pos += nb
+        assert pos == (g - op.chunk_base[r]) * C + op.chunk_len(g)
     for mask in (0, sum(1 << n for n in range(1, R + 1)), 1 << R):
         for node in range(1, R + 1):
             tiles = lam.plan_tree_tiles(d, lay, N, C, R, node, mask)
